@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""PYRIT ring-codec benchmark on B200 (see DESIGN.md section "Measurement").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl b200|reference]
+
+One step = one pass of the fused encode (or decode) kernel over this rank's
+byte-offset shard of every strip of the workload (BASELINE.json config 5 by
+default: GF(2^12) in R_{2,13}, k=16, m=4, 512 MiB fragments, 8 GiB of source
+sharded across the N GPUs -- total work fixed, so scaling is "strong").
+`value` = source bytes of the whole job / max-over-ranks device time (inputs
+resident in HBM, larger than L2; smaller workloads rotate buffer sets so the
+working set exceeds L2).  `e2e` = the same metric through the public
+host-buffer C ABI (pyrit_encode_host / pyrit_decode_host) with pinned host
+buffers, H2D and D2H inside the timed region.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PYRIT encode/decode GB/s (source bytes) at 1/2/4/8 B200; % of HBM roofline"
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline(wl, steps=None, warmup=1, budget_s=12.0, sample_frag=None):
+    """Reference CPU path (oracle/_ref, the unmodified reference headers) on a bounded sample."""
+    import numpy as np
+
+    import oracle as O
+
+    threads = os.cpu_count() or 1
+    f = O.Field(wl.fld.w, wl.fld.n, wl.fld.kind, wl.fld.s, wl.fld.r_esp or wl.fld.w, wl.fld.modulus)
+    q = 16 * wl.fld.w
+    frag = sample_frag or min(wl.frag, max(q, (16 << 20) // q * q))
+    # ring schedule where the reference's ring path is valid (AOP/ESP moduli);
+    # CRS bitmatrix schedule for R_{2,17} (the reference's ring path truncates
+    # 17-bit ring elements); decode = decode_matrix + CRS passes
+    aop_esp = wl.fld.n <= 16
+    mode = (0 if aop_esp else 1) if wl.op == "encode" else (3 if aop_esp else 2)
+    kind = "reference"
+    try:
+        plan = O.RefPlan(f, wl.k, wl.m, mode, frag, wl.erased)
+    except Exception:
+        plan = None
+    if plan is None:
+        return None
+    rng = np.random.default_rng(wl.seed)
+    for s in range(wl.k + wl.m):
+        plan.symbol(s)[:] = rng.integers(0, 256, frag, dtype=np.uint8)
+    for _ in range(warmup):
+        plan.run(threads)
+    times = []
+    t_start = time.perf_counter()
+    n = 0
+    while True:
+        t0 = time.perf_counter()
+        plan.run(threads)
+        times.append(time.perf_counter() - t0)
+        n += 1
+        if steps is not None and n >= steps:
+            break
+        if steps is None and (time.perf_counter() - t_start > budget_s or n >= 50):
+            break
+    plan.close()
+    src = wl.k * frag
+    t = statistics.median(times)
+    names = {0: "ring schedule (compile_schedule + parallel_replay)",
+             1: "CRS bitmatrix schedule (compile_crs_schedule + parallel_replay)",
+             2: "decode_matrix + CRS parallel_replay, then CRS parity rows (decode() restated)",
+             3: "decode_matrix + ring parallel_replay, then ring parity rows (decode())"}
+    return {"value": src / t / 1e9, "unit": "GB/s", "cores": threads, "kind": kind,
+            "sample": f"{wl.k}x{frag}-byte fragments ({src / 2**20:.0f} MiB source) of the {wl.name} shape, "
+                      f"{names[mode]}, {threads} threads, median of {len(times)} runs",
+            "times_s": [round(x, 5) for x in times]}
+
+
+def run_reference(args, rank, world):
+    from paper_1709_00178_b200.workloads import WORKLOADS
+    if rank != 0:
+        return 0
+    wl = WORKLOADS[args.config]
+    res = cpu_baseline(wl, steps=args.steps, warmup=args.warmup)
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpyrit_ref.so not built"}))
+        return 0
+    times = res.pop("times_s")
+    ms = statistics.mean(times) * 1e3
+    line = {"metric": METRIC, "value": res["value"], "unit": "GB/s", "n_gpus": world, "steps": len(times),
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded uniform bytes)",
+            "config": {"workload": wl.name, "sample_of_full_workload": True}, "impl": "reference",
+            "cpu_baseline": res,
+            "e2e": {"value": res["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--lanes", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0)
+    args = ap.parse_args(argv)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if args.warmup < 3:
+        args.warmup = 3  # contract: at least 3 warm-up steps
+
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1709_00178_b200 as P
+    from paper_1709_00178_b200 import _lib as L
+    from paper_1709_00178_b200.workloads import WORKLOADS, shard
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = L.load()
+    if args.lanes:
+        L.check(lib.pyrit_set_lanes(args.lanes))
+    wl = WORKLOADS[args.config]
+    w = wl.fld.w
+    lo, hi = shard(wl.strip, rank, world)
+    Ls = hi - lo
+    n_in, n_out = wl.k, wl.n_out
+    sym = w * Ls  # the shard of every fragment is itself a SymbolBuffer of w strips of Ls bytes
+    stream = torch.cuda.current_stream(dev)
+
+    def fill_symbol(t, frag):
+        for s in range(w):
+            P.fill(t[s * Ls:(s + 1) * Ls], wl.seed, frag, begin=s * wl.strip + lo, valid=wl.valid)
+
+    # ---- device-resident inputs (rotating sets when one set fits in L2)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    moved_rank = (n_in + n_out) * sym
+    nsets = 1 if moved_rank >= 4 * l2 else -(-4 * l2 // moved_rank)
+    code = wl.code
+    if wl.op == "encode":
+        plan = P.Plan.encode(code)
+        sets = []
+        for _ in range(nsets):
+            data = torch.empty((wl.k, sym), dtype=torch.uint8, device=dev)
+            for j in range(wl.k):
+                fill_symbol(data[j], j)
+            par = torch.empty((wl.m, sym), dtype=torch.uint8, device=dev)
+            sets.append(([data[j].data_ptr() for j in range(wl.k)], [par[i].data_ptr() for i in range(wl.m)],
+                         data, par))
+    else:
+        enc = P.Plan.encode(code)
+        plan = P.Plan.decode(code, wl.erased)
+        sets = []
+        for _ in range(nsets):
+            full = torch.empty((wl.k + wl.m, sym), dtype=torch.uint8, device=dev)
+            for j in range(wl.k):
+                fill_symbol(full[j], j)
+            enc.apply([full[j].data_ptr() for j in range(wl.k)],
+                      [full[wl.k + i].data_ptr() for i in range(wl.m)], Ls, stream=stream.cuda_stream)
+            sets.append(([full[s].data_ptr() for s in plan.survivors], [full[o].data_ptr() for o in plan.outputs],
+                         full, None))
+    torch.cuda.synchronize(dev)
+
+    def step(i):
+        ins, outs = sets[i % nsets][0], sets[i % nsets][1]
+        plan.apply(ins, outs, Ls, 0, Ls, stream=stream.cuda_stream)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches0 = lib.pyrit_kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    launches = lib.pyrit_kernel_launches() - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = wl.source_bytes() / (ms_max * 1e-3) / 1e9
+
+    # ---- self-check outside the timed region: erase 4 data symbols (or, for
+    # decode, compare against the pre-erasure symbols) and repair on the GPU;
+    # digests of repaired vs original bytes must match on every rank (K3 digests
+    # gathered over NCCL -- the only collective, verification only).
+    verified = verify(P, wl, plan, sets[0], sym, Ls, dev, stream, world)
+
+    # ---- end to end through the public host-buffer API
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(P, wl, sets[0], sym, Ls, dev, world, args.e2e_steps or min(args.steps, 10))
+
+    peak, peak_src = measured_peaks()
+    alg_bytes = (n_in + n_out) * sym
+    achieved = alg_bytes / (ms * 1e-3) / 1e9
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl)
+        if cpu:
+            cpu.pop("times_s", None)
+    st = plan.stats()
+    if rank == 0:
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                traffic = json.load(f).get(wl.name, {}).get(str(world))
+        except Exception:
+            pass
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded uniform bytes, counter-based mix64)",
+            "config": {"workload": wl.name, "op": wl.op, "k": wl.k, "m": wl.m, "w": w, "n": wl.fld.n,
+                       "p": hex(wl.fld.modulus), "fragment_bytes": wl.frag, "strip_bytes": wl.strip,
+                       "shard_strip_bytes": Ls, "erased": list(wl.erased), "parallelism": f"byte-offset shards x{world}",
+                       "l2": "inputs larger than L2" if nsets == 1 else f"{nsets} rotating buffer sets > L2",
+                       "kernel": plan.source(1)[0], "xors_per_column_word": st["xors"],
+                       "reference_region_ops": st["ref_region_ops"]},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": alg_bytes, "launch_ms": ms,
+                         "frac_of_8TBps_nominal": achieved / 8000.0},
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": int(launches),
+            "verified": verified,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def verify(P, wl, plan, s0, sym, Ls, dev, stream, world):
+    import torch
+    import torch.distributed as dist
+    ok = True
+    if wl.op == "encode":
+        full = torch.empty((wl.k + wl.m, sym), dtype=torch.uint8, device=dev)
+        full[: wl.k].copy_(s0[2])
+        full[wl.k:].copy_(s0[3])
+        erase = list(range(min(wl.m, wl.k)))
+        ref = [P.digest(full[e]) for e in erase]
+        dplan = P.Plan.decode(wl.code, erase)
+        full[erase] = 0xA5
+        dplan.apply([full[s].data_ptr() for s in dplan.survivors], [full[o].data_ptr() for o in dplan.outputs],
+                    Ls, stream=stream.cuda_stream)
+        got = [P.digest(full[e]) for e in erase]
+    else:
+        full = s0[2]
+        ref = [P.digest(full[o]) for o in plan.outputs]  # repaired in the timed loop
+        saved = full[plan.outputs].clone()
+        full[plan.outputs] = 0x5A
+        plan.apply([full[s].data_ptr() for s in plan.survivors], [full[o].data_ptr() for o in plan.outputs], Ls,
+                   stream=stream.cuda_stream)
+        got = [P.digest(full[o]) for o in plan.outputs]
+        ok = bool(torch.equal(saved, full[plan.outputs]))
+    dg = torch.cat([torch.cat(ref), torch.cat(got)])
+    if world > 1:
+        allg = [torch.empty_like(dg) for _ in range(world)]
+        dist.all_gather(allg, dg)
+        dg = torch.stack(allg)
+    dg = dg.view(-1, 2, len(ref))
+    return bool(ok and torch.equal(dg[:, 0], dg[:, 1]))
+
+
+def run_e2e(P, wl, s0, sym, Ls, dev, world, steps):
+    import torch
+    import torch.distributed as dist
+    local = dev.index
+    if wl.op == "encode":
+        host_in = torch.empty((wl.k, sym), dtype=torch.uint8, pin_memory=True)
+        host_in.copy_(s0[2])
+        host_out = torch.empty((wl.m, sym), dtype=torch.uint8, pin_memory=True)
+        a_in, a_out = host_in.numpy(), host_out.numpy()
+
+        def call():
+            P.encode_host(a_in, wl.code, device=local, parity=a_out)
+        h2d, d2h = wl.k * sym, wl.m * sym
+    else:
+        host = torch.empty((wl.k + wl.m, sym), dtype=torch.uint8, pin_memory=True)
+        host.copy_(s0[2])
+        a = host.numpy()
+
+        def call():
+            P.decode_host(a, wl.erased, wl.code, device=local)
+        h2d, d2h = wl.k * sym, len(wl.erased) * sym
+    for _ in range(2):
+        call()
+    times = []
+    for _ in range(steps):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        call()
+        times.append(time.perf_counter() - t0)
+    t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ok = True
+    if wl.op == "encode":
+        ok = bool(torch.equal(host_out.to(dev), s0[3]))
+    return {"value": wl.source_bytes() / t.item() / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": t.item() * 1e3, "steps": steps,
+            "api": "pyrit_encode_host" if wl.op == "encode" else "pyrit_decode_host", "pinned": True,
+            "matches_device_path": ok}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

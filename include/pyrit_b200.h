@@ -1,0 +1,167 @@
+/*
+ * pyrit_b200.h -- C ABI of the B200-native PYRIT ring codec.
+ *
+ * Drop-in boundary for the reference's hot path (paths relative to
+ * /root/reference/proj/include/pyrit/):
+ *
+ *   reference (C++, header only)                    here
+ *   ----------------------------------------------  -------------------------------
+ *   FieldSpec            field.hpp:116-137          pyrit_field
+ *   CodeSpec             matrix.hpp:263-270         pyrit_code
+ *   cauchy_parity_matrix matrix.hpp:301-327         pyrit_cauchy_parity_matrix
+ *   decode_matrix        matrix.hpp:440-467         pyrit_decode_matrix
+ *   sparse_transform     ring.hpp:77-90             pyrit_sparse_transform
+ *   compile_schedule     schedule.hpp:94-163        pyrit_plan_create (+ _encode/_decode)
+ *   schedule_stats       schedule.hpp:216-223       pyrit_plan_get_stats
+ *   replay / parallel_replay codec.hpp:375-450      pyrit_cu_apply
+ *   encode               codec.hpp:469-477          pyrit_cu_encode   (device buffers)
+ *                                                    pyrit_encode_host (host buffers)
+ *   decode               codec.hpp:498-541          pyrit_cu_decode   (device buffers)
+ *                                                    pyrit_decode_host (host buffers)
+ *   Errc / Error         errors.hpp:57-84           return codes, pyrit_strerror
+ *
+ * Symbols are bit-sliced exactly as SymbolBuffer stores them
+ * (codec.hpp:281-330): a symbol of symbol_size bytes is w contiguous strips
+ * of symbol_size / w bytes, strip i holding coefficient i of every bit
+ * column.  symbol_size must be a positive multiple of w and of 8
+ * (codec.hpp:285-287).
+ *
+ * Return codes: 0 ok; 1 + Errc (1..11, errors.hpp:57-69) for argument,
+ * shape and algebra errors; negative for device failures: -e for a
+ * cudaError_t e, -1000 - r for an nvrtcResult r, -2000 - r for a driver
+ * CUresult r.  Nothing throws across this boundary.
+ *
+ * Ownership: the caller owns every buffer; device entry points allocate
+ * nothing per call and run asynchronously on the given stream (a
+ * cudaStream_t passed as void*; NULL = legacy default stream).  Plans are
+ * immutable once created and may be used from any thread concurrently.
+ */
+#ifndef PYRIT_B200_H
+#define PYRIT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+/* field.hpp:116-137 (ring elements widened: n <= 32, any p | x^n + 1) */
+typedef struct pyrit_field {
+    uint32_t w;       /* extension degree, elements are w-bit (<= 16) */
+    uint32_t n;       /* ring length, w < n <= 32 */
+    uint32_t kind;    /* 0 = Aop, 1 = Esp (FieldKind, field.hpp:100-103) */
+    uint32_t s;       /* coefficient spacing */
+    uint32_t r_esp;   /* degree of the ESP base polynomial (w for AOP) */
+    uint32_t modulus; /* p(x), bit i = coefficient of x^i */
+} pyrit_field;
+
+/* matrix.hpp:263-270 */
+typedef struct pyrit_code {
+    uint32_t k;         /* data symbols */
+    uint32_t r;         /* parity symbols */
+    pyrit_field field;
+    uint32_t transform; /* 0 = Embedding, 1 = Parity (transform.hpp:142) */
+} pyrit_code;
+
+/* schedule.hpp:61-67 ScheduleStats, extended with the fused-program counts */
+typedef struct pyrit_plan_stats {
+    uint32_t rows, cols;       /* outputs x inputs */
+    uint64_t matrix_ones;      /* sum of representative weights x w (schedule.hpp:112) */
+    uint64_t ref_region_ops;   /* ops compile_schedule emits (pre+core+post), generalized fold */
+    uint64_t naive_xors;       /* 2-input XORs of the unshared ring program */
+    uint64_t xors;             /* 2-input XORs of the compiled program */
+    uint64_t loads, stores;    /* strip words read / written per column word */
+    uint32_t group;            /* input symbols whose strips are live together */
+} pyrit_plan_stats;
+
+typedef struct pyrit_plan pyrit_plan;
+
+/* ---- host algebra ---------------------------------------------------- */
+const char* pyrit_version(void);
+const char* pyrit_strerror(int code);
+
+/* FieldSpec::gf16_aop / gf64_esp (field.hpp:124-129) and the BASELINE fields */
+int pyrit_field_named(const char* name, pyrit_field* out); /* "gf16", "gf64", "gf256_r17", "gf1024", "gf4096" */
+int pyrit_field_validate(const pyrit_field* f);
+int pyrit_gf_mul(const pyrit_field* f, uint32_t a, uint32_t b, uint32_t* out);   /* field.hpp:154 */
+int pyrit_gf_inv(const pyrit_field* f, uint32_t a, uint32_t* out);               /* field.hpp:168 */
+int pyrit_sparse_transform(const pyrit_field* f, uint32_t u, uint32_t* rep);     /* ring.hpp:77 */
+int pyrit_fold_table(const pyrit_field* f, uint32_t* fold /* n - w entries */);  /* x^t mod p */
+/* out: r x k row-major (matrix.hpp:301) */
+int pyrit_cauchy_parity_matrix(const pyrit_code* code, uint16_t* out);
+/* out: (#erased data) x k rows of A^-1, survivors in given order (matrix.hpp:440) */
+int pyrit_decode_matrix(const pyrit_code* code, const uint32_t* survivors, uint16_t* out, uint32_t* rows);
+/* fused repair matrix: survivors (k, lowest index first), outputs (erased,
+ * data then parity, each ascending), matrix outputs x k */
+int pyrit_repair_matrix(const pyrit_code* code, const uint32_t* erased, uint32_t n_erased,
+                        uint32_t* survivors, uint32_t* outputs, uint16_t* matrix);
+
+/* ---- compiled plans (schedule.hpp:94 compile_schedule) ---------------- */
+/* rep: 0 = RingRep::Sparse (minimal weight), 1 = Dense (schedule.hpp:78);
+ * group: input symbols per register group, 0 = automatic */
+int pyrit_plan_create(const pyrit_field* f, uint32_t transform, const uint16_t* matrix, uint32_t rows,
+                      uint32_t cols, uint32_t rep, uint32_t group, pyrit_plan** out);
+int pyrit_plan_encode(const pyrit_code* code, pyrit_plan** out);
+int pyrit_plan_decode(const pyrit_code* code, const uint32_t* erased, uint32_t n_erased, pyrit_plan** out,
+                      uint32_t* survivors, uint32_t* outputs);
+int pyrit_plan_get_stats(const pyrit_plan* plan, pyrit_plan_stats* out);
+int pyrit_plan_reps(const pyrit_plan* plan, uint32_t* reps /* rows x cols */);
+/* generated CUDA source of the fused kernel; *len receives the full size */
+int pyrit_plan_source(const pyrit_plan* plan, uint32_t lanes, char* buf, size_t cap, size_t* len,
+                      char* name, size_t name_cap);
+/* verification aid: interprets the compiled program on HOST buffers (no
+ * device involved); used to test the compiler where no GPU exists */
+int pyrit_plan_interpret(const pyrit_plan* plan, const uint8_t* const* in, uint8_t* const* out,
+                         uint64_t strip_bytes, uint64_t off, uint64_t len);
+void pyrit_plan_destroy(pyrit_plan* plan);
+
+/* ---- device path ------------------------------------------------------ */
+/* replay (codec.hpp:375): window [off, off+len) of every strip; in[j] /
+ * out[i] are device base pointers of the input / output symbols */
+int pyrit_cu_apply(const pyrit_plan* plan, const uint8_t* const* in, uint8_t* const* out, uint64_t strip_bytes,
+                   uint64_t off, uint64_t len, void* stream);
+/* compile + load the plan's kernel for the current device (no launch) */
+int pyrit_cu_prepare(const pyrit_plan* plan);
+/* encode (codec.hpp:469): data[k], parity[r] device symbol pointers */
+int pyrit_cu_encode(const pyrit_code* code, const uint8_t* const* data, uint8_t* const* parity,
+                    uint64_t symbol_size, void* stream);
+/* decode (codec.hpp:498): symbols[k + r] device pointers, repaired in place */
+int pyrit_cu_decode(const pyrit_code* code, uint8_t* const* symbols, const uint32_t* erased, uint32_t n_erased,
+                    uint64_t symbol_size, void* stream);
+
+/* ---- host-buffer path (end to end: H2D, fused kernel, D2H, pipelined) -- */
+/* data: k * symbol_size contiguous host bytes (SymbolBuffer layout);
+ * parity: r * symbol_size host bytes.  Synchronous. Pinned buffers overlap. */
+int pyrit_encode_host(const pyrit_code* code, const uint8_t* data, uint8_t* parity, uint64_t symbol_size,
+                      int device);
+/* symbols: (k + r) * symbol_size host bytes, repaired in place.  Synchronous. */
+int pyrit_decode_host(const pyrit_code* code, uint8_t* symbols, const uint32_t* erased, uint32_t n_erased,
+                      uint64_t symbol_size, int device);
+/* bytes per strip per pipeline chunk (0 = automatic) */
+int pyrit_set_host_chunk(uint64_t strip_chunk_bytes);
+
+/* ---- synthetic inputs and verification digests ----------------------- */
+int pyrit_cu_fill(uint64_t seed, uint64_t frag, uint8_t* dst, uint64_t begin, uint64_t len, uint64_t valid,
+                  void* stream);
+/* *out (device uint64) += digest of src[0, len) whose first word has global
+ * index word_offset; src 8-byte aligned */
+int pyrit_cu_digest(const uint8_t* src, uint64_t len, uint64_t word_offset, uint64_t* out, void* stream);
+
+/* ---- runtime knobs and counters -------------------------------------- */
+int pyrit_set_lanes(uint32_t lanes); /* 32-bit words per thread per strip: 1, 2 or 4 */
+int pyrit_set_kernel_dir(const char* dir);
+uint64_t pyrit_jit_compiles(void);
+uint64_t pyrit_kernel_launches(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PYRIT_B200_H */

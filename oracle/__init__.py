@@ -1,0 +1,329 @@
+"""TEST INFRASTRUCTURE ONLY -- ctypes front end of the CPU checker.
+
+`liboracle.so` is the plain-C restatement (pyrit_oracle.c); `_ref/libpyrit_ref.so`
+is the unmodified reference compiled in place from /root/reference headers by
+oracle/Makefile.  Only tests/, __graft_entry__.smoke() and bench.py's CPU
+baseline / reference arm may import this package; the product never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(HERE, "liboracle.so")
+_REF = os.path.join(HERE, "_ref", "libpyrit_ref.so")
+
+u8p = C.POINTER(C.c_uint8)
+u16p = C.POINTER(C.c_uint16)
+u32p = C.POINTER(C.c_uint32)
+u64p = C.POINTER(C.c_uint64)
+
+
+@dataclass(frozen=True)
+class Field:
+    """FieldSpec (field.hpp:116-137), ring elements widened to 32 bits."""
+    w: int
+    n: int
+    kind: int  # 0 Aop, 1 Esp
+    s: int
+    r_esp: int
+    modulus: int
+
+
+GF16 = Field(4, 5, 0, 1, 4, 0x1F)        # FieldSpec::gf16_aop (field.hpp:124-126)
+GF64 = Field(6, 9, 1, 3, 2, 0x49)        # FieldSpec::gf64_esp (field.hpp:127-129)
+GF256_R17 = Field(8, 17, 0, 1, 8, 0x139)  # BASELINE configs 2 and 4
+GF1024 = Field(10, 11, 0, 1, 10, 0x7FF)   # BASELINE config 3
+GF4096 = Field(12, 13, 0, 1, 12, 0x1FFF)  # BASELINE config 5
+
+
+def build() -> None:
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def _load(path: str):
+    if not os.path.exists(path):
+        build()
+    return C.CDLL(path)
+
+
+_lib = None
+_ref = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = _load(_LIB)
+        _lib.or_gf_mul.restype = C.c_uint32
+        _lib.or_gf_inv.restype = C.c_uint32
+        _lib.or_sparse_transform.restype = C.c_uint32
+        _lib.or_ring_mul.restype = C.c_uint32
+        _lib.or_mix64.restype = C.c_uint64
+        _lib.or_mix64.argtypes = [C.c_uint64]
+        _lib.or_digest.restype = C.c_uint64
+        _lib.or_digest.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64]
+        _lib.or_poly_mod.restype = C.c_uint64
+        _lib.or_poly_mod.argtypes = [C.c_uint64, C.c_uint64]
+        _lib.or_clmul.restype = C.c_uint64
+        _lib.or_clmul.argtypes = [C.c_uint64, C.c_uint64]
+    return _lib
+
+
+def ref_available() -> bool:
+    return os.path.exists(_REF) or os.path.isdir("/root/reference/proj/include/pyrit")
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        if not os.path.exists(_REF):
+            build()
+        _ref = C.CDLL(_REF)
+        for name in ("ref_gf_mul", "ref_gf_inv", "ref_ring_mul", "ref_sparse_transform", "ref_phi_E_inv"):
+            getattr(_ref, name).restype = C.c_uint32
+        _ref.ref_plan_create.restype = C.c_void_p
+        _ref.ref_plan_create.argtypes = [C.c_uint] * 6 + [C.c_uint] * 3 + [C.c_uint64, u32p, C.c_uint]
+        _ref.ref_plan_symbol.restype = C.c_void_p
+        _ref.ref_plan_symbol.argtypes = [C.c_void_p, C.c_uint]
+        _ref.ref_plan_run.argtypes = [C.c_void_p, C.c_uint]
+        _ref.ref_plan_destroy.argtypes = [C.c_void_p]
+    return _ref
+
+
+def _fa(f: Field):
+    return (f.w, f.n, f.kind, f.s, f.r_esp, f.modulus)
+
+
+def _ptrs(arrs):
+    return (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+
+
+# ---------------------------------------------------------------- oracle (C)
+def gf_mul(a, b, f: Field) -> int:
+    return lib().or_gf_mul(a, b, f.modulus)
+
+
+def gf_inv(a, f: Field) -> int:
+    return lib().or_gf_inv(a, f.w, f.modulus)
+
+
+def ring_mul(a, b, f: Field) -> int:
+    return lib().or_ring_mul(a, b, f.n)
+
+
+def sparse_transform(u, f: Field) -> int:
+    return lib().or_sparse_transform(u, f.w, f.n, f.modulus)
+
+
+def fold_table(f: Field):
+    out = (C.c_uint32 * 32)()
+    lib().or_fold_table(f.w, f.n, f.modulus, out)
+    return list(out[: f.n - f.w])
+
+
+def cauchy(k, r, f: Field) -> np.ndarray:
+    out = np.zeros(max(r, 1) * k, dtype=np.uint16)
+    rc = lib().or_cauchy(k, r, f.w, f.modulus, out.ctypes.data_as(u16p))
+    if rc:
+        raise OracleError(rc)
+    return out[: r * k].reshape(r, k)
+
+
+def invert(m: np.ndarray, f: Field) -> np.ndarray:
+    m = np.ascontiguousarray(m, dtype=np.uint16)
+    out = np.zeros_like(m)
+    rc = lib().or_invert(m.shape[0], f.w, f.modulus, m.ctypes.data_as(u16p), out.ctypes.data_as(u16p))
+    if rc:
+        raise OracleError(rc)
+    return out
+
+
+def decode_matrix(k, r, f: Field, survivors) -> np.ndarray:
+    c = cauchy(k, r, f)
+    surv = np.asarray(survivors, dtype=np.uint32)
+    out = np.zeros(k * k, dtype=np.uint16)
+    rows = C.c_uint32(0)
+    rc = lib().or_decode_matrix(k, r, f.w, f.modulus, c.ctypes.data_as(u16p), surv.ctypes.data_as(u32p),
+                                out.ctypes.data_as(u16p), C.byref(rows))
+    if rc:
+        raise OracleError(rc)
+    return out[: rows.value * k].reshape(rows.value, k)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, rc):
+        super().__init__(f"oracle error {rc}")
+        self.rc = rc
+
+
+def _apply(fn, f: Field, kind, m, ins, outs, strip, off, len_, extra=()):
+    m = np.ascontiguousarray(m, dtype=np.uint16)
+    rows, cols = m.shape
+    rc = fn(f.w, f.n, f.s, f.modulus, kind, rows, cols, m.ctypes.data_as(u16p), _ptrs(ins), _ptrs(outs),
+            C.c_uint64(strip), C.c_uint64(off), C.c_uint64(len_), *extra)
+    if rc:
+        raise OracleError(rc)
+
+
+def apply_columns(f: Field, m, ins, strip, kind=0, off=0, length=None, outs=None):
+    """codec.hpp:444-469 oracle_apply restated; ins: list of uint8 arrays (w*strip each)."""
+    length = strip - off if length is None else length
+    if outs is None:
+        outs = [np.zeros(f.w * strip, dtype=np.uint8) for _ in range(np.asarray(m).shape[0])]
+    _apply(lib().or_apply_columns, f, kind, m, ins, outs, strip, off, length)
+    return outs
+
+
+def ring_replay(f: Field, m, ins, strip, kind=0, off=0, length=None, outs=None, want_ops=False):
+    """schedule.hpp:94-163 + codec.hpp:118-157 restated (ring schedule, generalized fold)."""
+    length = strip - off if length is None else length
+    if outs is None:
+        outs = [np.zeros(f.w * strip, dtype=np.uint8) for _ in range(np.asarray(m).shape[0])]
+    ops = C.c_uint64(0)
+    _apply(lib().or_ring_replay, f, kind, m, ins, outs, strip, off, length, extra=(C.byref(ops),))
+    return (outs, ops.value) if want_ops else outs
+
+
+def decode(k, r, f: Field, symbols, erased, strip, kind=0, off=0, length=None):
+    """codec.hpp:498-541 restated in place over k + r symbol arrays."""
+    length = strip - off if length is None else length
+    er = np.asarray(sorted(erased) if False else list(erased), dtype=np.uint32)
+    rc = lib().or_decode(k, r, f.w, f.n, f.s, f.modulus, kind, _ptrs(symbols), er.ctypes.data_as(u32p),
+                         len(er), C.c_uint64(strip), C.c_uint64(off), C.c_uint64(length))
+    if rc:
+        raise OracleError(rc)
+
+
+def fill(seed, frag, length, valid=None, begin=0) -> np.ndarray:
+    valid = begin + length if valid is None else valid
+    out = np.empty(length, dtype=np.uint8)
+    lib().or_fill(C.c_uint64(seed), C.c_uint64(frag), out.ctypes.data_as(u8p), C.c_uint64(begin),
+                  C.c_uint64(length), C.c_uint64(valid))
+    return out
+
+
+def digest(buf: np.ndarray, word_offset=0) -> int:
+    buf = np.ascontiguousarray(buf)
+    return lib().or_digest(buf.ctypes.data, buf.nbytes, word_offset)
+
+
+# ------------------------------------------------------- numpy restatements
+_M1, _M2, _GOLD, _DG = (np.uint64(0xBF58476D1CE4E5B9), np.uint64(0x94D049BB133111EB),
+                        np.uint64(0x9E3779B97F4A7C15), np.uint64(0xD6E8FEB86659FD93))
+
+
+def mix64_np(z: np.ndarray) -> np.ndarray:
+    z = z + _GOLD
+    z = (z ^ (z >> np.uint64(30))) * _M1
+    z = (z ^ (z >> np.uint64(27))) * _M2
+    return z ^ (z >> np.uint64(31))
+
+
+def fill_np(seed, frag, length, valid=None, begin=0) -> np.ndarray:
+    """Vectorised twin of or_fill (same bytes); begin and length multiples of 8."""
+    valid = begin + length if valid is None else valid
+    assert begin % 8 == 0 and length % 8 == 0
+    q = np.arange(begin // 8, (begin + length) // 8, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        words = mix64_np((np.uint64(seed) << np.uint64(48)) ^ (np.uint64(frag) << np.uint64(36)) ^ q)
+    out = words.view(np.uint8).copy()
+    if valid < begin + length:
+        out[max(valid - begin, 0):] = 0
+    return out
+
+
+def digest_np(buf: np.ndarray, word_offset=0) -> int:
+    b = np.ascontiguousarray(buf).view(np.uint8)
+    pad = (-b.nbytes) % 8
+    if pad:
+        b = np.concatenate([b, np.zeros(pad, np.uint8)])
+    words = b.view(np.uint64)
+    q = np.arange(word_offset, word_offset + words.size, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        return int(mix64_np(words ^ (q * _DG)).sum(dtype=np.uint64))
+
+
+# ----------------------------------------------------------- the reference
+def ref_cauchy(k, r, f: Field) -> np.ndarray:
+    out = np.zeros(max(r, 1) * k, dtype=np.uint16)
+    rc = ref().ref_cauchy(k, r, f.w, f.n, f.modulus, out.ctypes.data_as(u16p))
+    if rc:
+        raise OracleError(rc)
+    return out[: r * k].reshape(r, k)
+
+
+def ref_sparse_transform(u, f: Field) -> int:
+    return ref().ref_sparse_transform(u, *_fa(f))
+
+
+def ref_schedule_stats(f: Field, m, transform=0, crs=0, rep=0) -> dict:
+    m = np.ascontiguousarray(m, dtype=np.uint16)
+    st = (C.c_uint64 * 8)()
+    rc = ref().ref_schedule_stats(*_fa(f), m.shape[0], m.shape[1], m.ctypes.data_as(u16p), transform, crs,
+                                  rep, st)
+    if rc:
+        raise OracleError(rc)
+    keys = ("copy", "xor", "zero", "total", "matrix_ones", "pre", "core", "post")
+    return dict(zip(keys, list(st)))
+
+
+def ref_oracle_apply(f: Field, m, data: np.ndarray, symbol_size, transform=0) -> np.ndarray:
+    m = np.ascontiguousarray(m, dtype=np.uint16)
+    out = np.zeros(m.shape[0] * symbol_size, dtype=np.uint8)
+    rc = ref().ref_oracle_apply(*_fa(f), transform, m.shape[0], m.shape[1], m.ctypes.data_as(u16p),
+                                data.ctypes.data_as(u8p), C.c_uint64(symbol_size), out.ctypes.data_as(u8p))
+    if rc:
+        raise OracleError(rc)
+    return out
+
+
+def ref_encode(f: Field, k, r, data: np.ndarray, symbol_size, transform=0, crs=0, threads=1) -> np.ndarray:
+    out = np.zeros(r * symbol_size, dtype=np.uint8)
+    rc = ref().ref_encode(*_fa(f), k, r, transform, crs, data.ctypes.data_as(u8p), C.c_uint64(symbol_size),
+                          out.ctypes.data_as(u8p), threads)
+    if rc:
+        raise OracleError(rc)
+    return out
+
+
+def ref_decode(f: Field, k, r, symbols: np.ndarray, symbol_size, erased, transform=0, threads=1) -> None:
+    er = np.asarray(list(erased), dtype=np.uint32)
+    rc = ref().ref_decode(*_fa(f), k, r, transform, symbols.ctypes.data_as(u8p), C.c_uint64(symbol_size),
+                          er.ctypes.data_as(u32p), len(er), threads)
+    if rc:
+        raise OracleError(rc)
+
+
+class RefPlan:
+    """Precompiled reference schedule + preallocated SymbolBuffer (bench.hpp:146-208 method)."""
+
+    def __init__(self, f: Field, k, r, mode, symbol_size, erased=()):
+        er = np.asarray(list(erased) or [0], dtype=np.uint32)
+        self.k, self.r, self.symbol_size = k, r, symbol_size
+        self.h = ref().ref_plan_create(*_fa(f), k, r, mode, symbol_size, er.ctypes.data_as(u32p),
+                                       len(list(erased)))
+        if not self.h:
+            raise OracleError(-1)
+
+    def symbol(self, i) -> np.ndarray:
+        p = ref().ref_plan_symbol(self.h, i)
+        return np.ctypeslib.as_array(C.cast(p, u8p), shape=(self.symbol_size,))
+
+    def run(self, threads=1):
+        rc = ref().ref_plan_run(self.h, threads)
+        if rc:
+            raise OracleError(rc)
+
+    def close(self):
+        if self.h:
+            ref().ref_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()

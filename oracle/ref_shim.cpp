@@ -1,0 +1,264 @@
+// ref_shim.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// Exposes the UNMODIFIED reference library (header-only C++20, compiled in
+// place from /root/reference/proj/include by oracle/Makefile; nothing is
+// copied into this repository) through a small extern "C" surface so the
+// Python tests can pin the C oracle against it and bench.py can time the
+// reference's own CPU path.  Output: oracle/_ref/libpyrit_ref.so.
+//
+// Every function forwards to the reference symbol named in its comment;
+// pyrit::Error is mapped to 1 + Errc (errors.hpp:57-69).
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "pyrit/codec.hpp"
+#include "pyrit/matrix.hpp"
+#include "pyrit/schedule.hpp"
+
+using namespace pyrit;
+
+#define REF_EXPORT extern "C" __attribute__((visibility("default")))
+
+namespace {
+
+FieldSpec make_field(unsigned w, unsigned n, unsigned kind, unsigned s, unsigned r_esp,
+                     std::uint32_t modulus) {
+    return FieldSpec{w, n, kind ? FieldKind::Esp : FieldKind::Aop, s, r_esp, modulus};
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const Error& e) {
+        return 1 + static_cast<int>(e.code());
+    } catch (...) {
+        return 100;
+    }
+}
+
+FieldMatrix make_matrix(const FieldSpec& spec, unsigned rows, unsigned cols, const std::uint16_t* m) {
+    FieldMatrix fm(rows, cols, spec);
+    for (unsigned i = 0; i < rows * cols; ++i) fm.e[i] = m[i];
+    return fm;
+}
+
+} // namespace
+
+// field.hpp:154 gf_mul / :168 gf_inv
+REF_EXPORT std::uint32_t ref_gf_mul(std::uint32_t a, std::uint32_t b, unsigned w, unsigned n,
+                                    std::uint32_t modulus) {
+    return gf_mul(static_cast<FieldElem>(a), static_cast<FieldElem>(b),
+                  make_field(w, n, 0, 1, w, modulus));
+}
+REF_EXPORT std::uint32_t ref_gf_inv(std::uint32_t a, unsigned w, unsigned n, std::uint32_t modulus) {
+    std::uint32_t out = 0;
+    guarded([&] { out = gf_inv(static_cast<FieldElem>(a), make_field(w, n, 0, 1, w, modulus)); });
+    return out;
+}
+
+// ring.hpp:24 ring_mul, :77 sparse_transform, transform.hpp:157 phi_E_inv
+REF_EXPORT std::uint32_t ref_ring_mul(std::uint32_t a, std::uint32_t b, unsigned w, unsigned n,
+                                      std::uint32_t modulus) {
+    return ring_mul(static_cast<RingElem>(a), static_cast<RingElem>(b),
+                    make_field(w, n, 0, 1, w, modulus));
+}
+REF_EXPORT std::uint32_t ref_sparse_transform(std::uint32_t u, unsigned w, unsigned n, unsigned kind,
+                                              unsigned s, unsigned r_esp, std::uint32_t modulus) {
+    return sparse_transform(static_cast<FieldElem>(u), make_field(w, n, kind, s, r_esp, modulus));
+}
+REF_EXPORT std::uint32_t ref_phi_E_inv(std::uint32_t a, unsigned w, unsigned n, unsigned kind,
+                                       unsigned s, unsigned r_esp, std::uint32_t modulus) {
+    return phi_E_inv(static_cast<RingElem>(a), make_field(w, n, kind, s, r_esp, modulus));
+}
+
+// matrix.hpp:301 cauchy_parity_matrix
+REF_EXPORT int ref_cauchy(unsigned k, unsigned r, unsigned w, unsigned n, std::uint32_t modulus,
+                          std::uint16_t* out) {
+    return guarded([&] {
+        const FieldMatrix c = cauchy_parity_matrix(k, r, make_field(w, n, 0, 1, w, modulus));
+        std::memcpy(out, c.e.data(), c.e.size() * sizeof(std::uint16_t));
+    });
+}
+
+// matrix.hpp:343 invert
+REF_EXPORT int ref_invert(unsigned dim, unsigned w, unsigned n, std::uint32_t modulus,
+                          const std::uint16_t* in, std::uint16_t* out) {
+    return guarded([&] {
+        const FieldMatrix inv = invert(make_matrix(make_field(w, n, 0, 1, w, modulus), dim, dim, in));
+        std::memcpy(out, inv.e.data(), inv.e.size() * sizeof(std::uint16_t));
+    });
+}
+
+// matrix.hpp:440 decode_matrix
+REF_EXPORT int ref_decode_matrix(unsigned k, unsigned r, unsigned w, unsigned n, std::uint32_t modulus,
+                                 const std::uint32_t* survivors, std::uint16_t* out,
+                                 unsigned* rows_out) {
+    return guarded([&] {
+        const FieldSpec spec = make_field(w, n, 0, 1, w, modulus);
+        const CodeSpec code{k, r, spec, TransformKind::Embedding};
+        const FieldMatrix c = cauchy_parity_matrix(k, r, spec);
+        std::vector<unsigned> surv(survivors, survivors + k);
+        const FieldMatrix dm = decode_matrix(code, c, surv);
+        std::memcpy(out, dm.e.data(), dm.e.size() * sizeof(std::uint16_t));
+        *rows_out = static_cast<unsigned>(dm.rows);
+    });
+}
+
+// schedule.hpp:94 compile_schedule / :168 compile_crs_schedule + :216 schedule_stats
+// crs: 0 ring schedule (rep: 0 Sparse, 1 Dense), 1 CRS bitmatrix schedule.
+// stats: [copy, xor, zero, total, matrix_ones, pre, core, post]
+REF_EXPORT int ref_schedule_stats(unsigned w, unsigned n, unsigned kind, unsigned s, unsigned r_esp,
+                                  std::uint32_t modulus, unsigned rows, unsigned cols,
+                                  const std::uint16_t* m, unsigned transform, unsigned crs,
+                                  unsigned rep, std::uint64_t* stats) {
+    return guarded([&] {
+        const FieldMatrix fm = make_matrix(make_field(w, n, kind, s, r_esp, modulus), rows, cols, m);
+        const XorSchedule sched =
+            crs ? compile_crs_schedule(fm)
+                : compile_schedule(fm, static_cast<TransformKind>(transform),
+                                   rep ? RingRep::Dense : RingRep::Sparse);
+        const ScheduleStats st = schedule_stats(sched);
+        stats[0] = st.copy_ops;
+        stats[1] = st.xor_ops;
+        stats[2] = st.zero_ops;
+        stats[3] = st.total_region_ops;
+        stats[4] = st.matrix_ones;
+        stats[5] = sched.pre.size();
+        stats[6] = sched.core.size();
+        stats[7] = sched.post.size();
+    });
+}
+
+// codec.hpp:444 oracle_apply over whole symbols (data: cols symbols contiguous)
+REF_EXPORT int ref_oracle_apply(unsigned w, unsigned n, unsigned kind, unsigned s, unsigned r_esp,
+                                std::uint32_t modulus, unsigned transform, unsigned rows,
+                                unsigned cols, const std::uint16_t* m, const std::uint8_t* data,
+                                std::uint64_t symbol_size, std::uint8_t* out) {
+    return guarded([&] {
+        const FieldSpec spec = make_field(w, n, kind, s, r_esp, modulus);
+        SymbolBuffer in(cols, symbol_size, spec);
+        std::memcpy(in.symbol(0), data, cols * symbol_size);
+        const SymbolBuffer o = oracle_apply(make_matrix(spec, rows, cols, m),
+                                            static_cast<TransformKind>(transform), in);
+        std::memcpy(out, o.symbol(0), rows * symbol_size);
+    });
+}
+
+// codec.hpp:469 encode (ring) and :480 encode_crs, whole symbols
+REF_EXPORT int ref_encode(unsigned w, unsigned n, unsigned kind, unsigned s, unsigned r_esp,
+                          std::uint32_t modulus, unsigned k, unsigned r, unsigned transform,
+                          unsigned crs, const std::uint8_t* data, std::uint64_t symbol_size,
+                          std::uint8_t* parity, unsigned threads) {
+    return guarded([&] {
+        const FieldSpec spec = make_field(w, n, kind, s, r_esp, modulus);
+        const CodeSpec code{k, r, spec, static_cast<TransformKind>(transform)};
+        SymbolBuffer in(k, symbol_size, spec);
+        std::memcpy(in.symbol(0), data, k * symbol_size);
+        const SymbolBuffer p = crs ? encode_crs(in, code, threads) : encode(in, code, threads);
+        std::memcpy(parity, p.symbol(0), r * symbol_size);
+    });
+}
+
+// codec.hpp:498 decode, in place over k + r contiguous symbols
+REF_EXPORT int ref_decode(unsigned w, unsigned n, unsigned kind, unsigned s, unsigned r_esp,
+                          std::uint32_t modulus, unsigned k, unsigned r, unsigned transform,
+                          std::uint8_t* symbols, std::uint64_t symbol_size, const unsigned* erased,
+                          unsigned n_erased, unsigned threads) {
+    return guarded([&] {
+        const FieldSpec spec = make_field(w, n, kind, s, r_esp, modulus);
+        const CodeSpec code{k, r, spec, static_cast<TransformKind>(transform)};
+        SymbolBuffer buf(k + r, symbol_size, spec);
+        std::memcpy(buf.symbol(0), symbols, (k + r) * symbol_size);
+        decode(buf, std::vector<unsigned>(erased, erased + n_erased), code, threads);
+        std::memcpy(symbols, buf.symbol(0), (k + r) * symbol_size);
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Precompiled plans for timing the reference CPU path the way bench.hpp:146-208
+// does (schedule compiled once, buffers preallocated, parallel_replay timed).
+// mode 0: encode with the ring schedule (compile_schedule, schedule.hpp:94)
+// mode 1: encode with the CRS schedule  (compile_crs_schedule, schedule.hpp:168)
+// mode 2: decode (codec.hpp:498-541 restated with CRS schedules): erased data
+//         via decode_matrix, then erased parity re-encoded from data.
+// mode 3: decode, same two passes with ring schedules (the reference's own
+//         decode(); valid for the AOP/ESP fields only).
+struct RefPlan {
+    FieldSpec spec;
+    CodeSpec code;
+    unsigned mode;
+    std::unique_ptr<SymbolBuffer> symbols; // k data then r parity
+    XorSchedule sched_a, sched_b;
+    std::vector<unsigned> in_a, out_a, in_b, out_b;
+    bool has_a = false, has_b = false;
+};
+
+REF_EXPORT void* ref_plan_create(unsigned w, unsigned n, unsigned kind, unsigned s, unsigned r_esp,
+                                 std::uint32_t modulus, unsigned k, unsigned r, unsigned mode,
+                                 std::uint64_t symbol_size, const unsigned* erased,
+                                 unsigned n_erased) {
+    RefPlan* p = nullptr;
+    const int rc = guarded([&] {
+        auto plan = std::make_unique<RefPlan>(RefPlan{make_field(w, n, kind, s, r_esp, modulus),
+                                                      CodeSpec{}, mode, nullptr, {}, {}, {}, {},
+                                                      {}, {}, false, false});
+        plan->code = CodeSpec{k, r, plan->spec, TransformKind::Embedding};
+        plan->symbols = std::make_unique<SymbolBuffer>(k + r, symbol_size, plan->spec);
+        const FieldMatrix c = cauchy_parity_matrix(plan->code);
+        auto compile = [&](const FieldMatrix& m, bool crs) {
+            return crs ? compile_crs_schedule(m) : compile_schedule(m, TransformKind::Embedding);
+        };
+        if (mode <= 1) {
+            plan->sched_a = compile(c, mode == 1);
+            plan->in_a = detail::iota_map(k);
+            plan->out_a = detail::iota_map(r, k);
+            plan->has_a = true;
+        } else {
+            const bool crs = mode == 2;
+            std::vector<bool> gone(k + r, false);
+            for (unsigned i = 0; i < n_erased; ++i) gone[erased[i]] = true;
+            std::vector<unsigned> surv, ed, ep;
+            for (unsigned i = 0; i < k + r && surv.size() < k; ++i)
+                if (!gone[i]) surv.push_back(i);
+            for (unsigned i = 0; i < k + r; ++i)
+                if (gone[i]) (i < k ? ed : ep).push_back(i);
+            if (!ed.empty()) {
+                plan->sched_a = compile(decode_matrix(plan->code, c, surv), crs);
+                plan->in_a = surv;
+                plan->out_a = ed;
+                plan->has_a = true;
+            }
+            if (!ep.empty()) {
+                FieldMatrix rows(ep.size(), k, plan->spec);
+                for (std::size_t i = 0; i < ep.size(); ++i)
+                    for (unsigned j = 0; j < k; ++j) rows.at(i, j) = c.at(ep[i] - k, j);
+                plan->sched_b = compile(rows, crs);
+                plan->in_b = detail::iota_map(k);
+                plan->out_b = ep;
+                plan->has_b = true;
+            }
+        }
+        p = plan.release();
+    });
+    return rc == 0 ? p : nullptr;
+}
+
+REF_EXPORT std::uint8_t* ref_plan_symbol(void* plan, unsigned sym) {
+    return static_cast<RefPlan*>(plan)->symbols->symbol(sym);
+}
+
+REF_EXPORT int ref_plan_run(void* plan, unsigned threads) {
+    RefPlan* p = static_cast<RefPlan*>(plan);
+    return guarded([&] {
+        if (p->has_a)
+            parallel_replay(p->sched_a, *p->symbols, p->in_a, *p->symbols, p->out_a, threads);
+        if (p->has_b)
+            parallel_replay(p->sched_b, *p->symbols, p->in_b, *p->symbols, p->out_b, threads);
+    });
+}
+
+REF_EXPORT void ref_plan_destroy(void* plan) { delete static_cast<RefPlan*>(plan); }

@@ -1,0 +1,302 @@
+"""B200-native PYRIT ring codec -- Python mirror of the reference C++ API.
+
+Names, argument meaning and errors follow the reference library
+(/root/reference/proj/include/pyrit/, cited per function); the work is done
+by libpyrit_b200.so (C++ host algebra + generated sm_100a kernels) through the
+C ABI in include/pyrit_b200.h.  Device entry points take CUDA torch tensors;
+host entry points take numpy arrays laid out like SymbolBuffer
+(codec.hpp:281-330: symbols contiguous, each w strips of symbol_size/w bytes).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import _lib as L
+from ._lib import PyritError
+
+__all__ = [
+    "FieldSpec", "CodeSpec", "TransformKind", "RingRep", "PyritError", "Plan", "gf_mul", "gf_inv",
+    "sparse_transform", "fold_table", "cauchy_parity_matrix", "decode_matrix", "repair_matrix", "encode",
+    "decode", "encode_host", "decode_host", "fill", "digest", "choose_transform",
+]
+
+
+class TransformKind(enum.IntEnum):  # transform.hpp:142
+    Embedding = 0
+    Parity = 1
+
+
+class RingRep(enum.IntEnum):  # schedule.hpp:78
+    Sparse = 0
+    Dense = 1
+
+
+def choose_transform(k: int, r: int) -> TransformKind:  # schedule.hpp:71-73
+    return TransformKind.Embedding if k >= r else TransformKind.Parity
+
+
+@dataclass(frozen=True)
+class FieldSpec:
+    """field.hpp:116-137; ring elements are 32-bit so R_{2,17} is representable."""
+    w: int
+    n: int
+    kind: int = 0
+    s: int = 1
+    r_esp: int = 0
+    modulus: int = 0
+
+    @staticmethod
+    def gf16_aop() -> "FieldSpec":  # field.hpp:124-126
+        return FieldSpec(4, 5, 0, 1, 4, 0b11111)
+
+    @staticmethod
+    def gf64_esp() -> "FieldSpec":  # field.hpp:127-129
+        return FieldSpec(6, 9, 1, 3, 2, 0b001001001)
+
+    @staticmethod
+    def gf256_r17() -> "FieldSpec":  # BASELINE configs 2/4: p = x^8+x^5+x^4+x^3+1 | x^17+1
+        return FieldSpec(8, 17, 0, 1, 8, 0x139)
+
+    @staticmethod
+    def aop(w: int) -> "FieldSpec":  # all-one p of degree w in R_{2,w+1} (field.hpp:189-218)
+        return FieldSpec(w, w + 1, 0, 1, w, (1 << (w + 1)) - 1)
+
+    def c(self) -> L.pyrit_field:
+        return L.pyrit_field(self.w, self.n, self.kind, self.s, self.r_esp or self.w, self.modulus)
+
+    def field_size(self) -> int:
+        return 1 << self.w
+
+
+@dataclass(frozen=True)
+class CodeSpec:
+    """matrix.hpp:263-270."""
+    k: int
+    r: int
+    field: FieldSpec
+    transform: TransformKind = TransformKind.Embedding
+
+    def c(self) -> L.pyrit_code:
+        return L.pyrit_code(self.k, self.r, self.field.c(), int(self.transform))
+
+
+def _clib():
+    return L.load()
+
+
+def _u32(x) -> C.c_uint32:
+    return C.c_uint32(x)
+
+
+def gf_mul(a: int, b: int, f: FieldSpec) -> int:  # field.hpp:154
+    out = C.c_uint32()
+    L.check(_clib().pyrit_gf_mul(C.byref(f.c()), a, b, C.byref(out)))
+    return out.value
+
+
+def gf_inv(a: int, f: FieldSpec) -> int:  # field.hpp:168
+    out = C.c_uint32()
+    L.check(_clib().pyrit_gf_inv(C.byref(f.c()), a, C.byref(out)))
+    return out.value
+
+
+def sparse_transform(u: int, f: FieldSpec) -> int:  # ring.hpp:77
+    out = C.c_uint32()
+    L.check(_clib().pyrit_sparse_transform(C.byref(f.c()), u, C.byref(out)))
+    return out.value
+
+
+def fold_table(f: FieldSpec) -> list[int]:
+    out = (C.c_uint32 * 32)()
+    L.check(_clib().pyrit_fold_table(C.byref(f.c()), out))
+    return list(out[: f.n - f.w])
+
+
+def cauchy_parity_matrix(code: CodeSpec) -> np.ndarray:  # matrix.hpp:301-327
+    out = np.zeros(max(code.r * code.k, 1), dtype=np.uint16)
+    L.check(_clib().pyrit_cauchy_parity_matrix(C.byref(code.c()), out.ctypes.data))
+    return out[: code.r * code.k].reshape(code.r, code.k)
+
+
+def decode_matrix(code: CodeSpec, survivors: Sequence[int]) -> np.ndarray:  # matrix.hpp:440-467
+    surv = np.asarray(survivors, dtype=np.uint32)
+    if surv.size != code.k:
+        raise PyritError(11, "need exactly k survivors")
+    out = np.zeros(code.k * code.k, dtype=np.uint16)
+    rows = C.c_uint32()
+    L.check(_clib().pyrit_decode_matrix(C.byref(code.c()), surv.ctypes.data, out.ctypes.data, C.byref(rows)))
+    return out[: rows.value * code.k].reshape(rows.value, code.k)
+
+
+def repair_matrix(code: CodeSpec, erased: Iterable[int]):
+    """Fused one-pass repair: (survivors, outputs, matrix over survivors)."""
+    er = np.asarray(list(erased), dtype=np.uint32)
+    surv = np.zeros(code.k, dtype=np.uint32)
+    outs = np.zeros(max(er.size, 1), dtype=np.uint32)
+    m = np.zeros(max(er.size, 1) * code.k, dtype=np.uint16)
+    L.check(_clib().pyrit_repair_matrix(C.byref(code.c()), er.ctypes.data, er.size, surv.ctypes.data,
+                                       outs.ctypes.data, m.ctypes.data))
+    return surv, outs[: er.size], m[: er.size * code.k].reshape(er.size, code.k)
+
+
+def _ptr_array(ptrs):
+    return (C.c_void_p * max(len(ptrs), 1))(*ptrs)
+
+
+class Plan:
+    """A compiled ring program: the GPU counterpart of XorSchedule (schedule.hpp:50-59)."""
+
+    def __init__(self, handle: C.c_void_p, survivors=None, outputs=None):
+        self._h = handle
+        self.survivors = survivors
+        self.outputs = outputs
+
+    @classmethod
+    def create(cls, f: FieldSpec, matrix: np.ndarray, transform=TransformKind.Embedding, rep=RingRep.Sparse,
+               group: int = 0) -> "Plan":  # compile_schedule(m, kind, rep), schedule.hpp:94
+        m = np.ascontiguousarray(matrix, dtype=np.uint16)
+        h = C.c_void_p()
+        L.check(_clib().pyrit_plan_create(C.byref(f.c()), int(transform), m.ctypes.data, m.shape[0], m.shape[1],
+                                         int(rep), group, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def encode(cls, code: CodeSpec) -> "Plan":
+        h = C.c_void_p()
+        L.check(_clib().pyrit_plan_encode(C.byref(code.c()), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def decode(cls, code: CodeSpec, erased: Iterable[int]) -> "Plan":
+        er = np.asarray(list(erased), dtype=np.uint32)
+        surv = np.zeros(code.k, dtype=np.uint32)
+        outs = np.zeros(max(er.size, 1), dtype=np.uint32)
+        h = C.c_void_p()
+        L.check(_clib().pyrit_plan_decode(C.byref(code.c()), er.ctypes.data, er.size, C.byref(h), surv.ctypes.data,
+                                         outs.ctypes.data))
+        return cls(h, surv.tolist(), outs[: er.size].tolist())
+
+    def stats(self) -> dict:
+        st = L.pyrit_plan_stats()
+        L.check(_clib().pyrit_plan_get_stats(self._h, C.byref(st)))
+        return {k: getattr(st, k) for k, _ in L.pyrit_plan_stats._fields_}
+
+    def reps(self) -> np.ndarray:
+        st = self.stats()
+        out = np.zeros(st["rows"] * st["cols"], dtype=np.uint32)
+        L.check(_clib().pyrit_plan_reps(self._h, out.ctypes.data))
+        return out.reshape(st["rows"], st["cols"])
+
+    def source(self, lanes: int = 1) -> tuple[str, str]:
+        size = C.c_size_t()
+        name = C.create_string_buffer(128)
+        L.check(_clib().pyrit_plan_source(self._h, lanes, None, 0, C.byref(size), name, 128))
+        buf = C.create_string_buffer(size.value + 1)
+        L.check(_clib().pyrit_plan_source(self._h, lanes, buf, size.value + 1, None, None, 0))
+        return name.value.decode(), buf.value.decode()
+
+    def interpret(self, ins: Sequence[np.ndarray], strip: int, off: int = 0, length: int | None = None,
+                  outs: Sequence[np.ndarray] | None = None) -> list[np.ndarray]:
+        """Run the compiled program on host arrays (compiler verification only)."""
+        st = self.stats()
+        length = strip - off if length is None else length
+        if outs is None:
+            outs = [np.zeros(len(ins[0]), dtype=np.uint8) for _ in range(st["rows"])]
+        L.check(_clib().pyrit_plan_interpret(self._h, _ptr_array([a.ctypes.data for a in ins]),
+                                            _ptr_array([a.ctypes.data for a in outs]), strip, off, length))
+        return list(outs)
+
+    def apply(self, in_ptrs: Sequence[int], out_ptrs: Sequence[int], strip: int, off: int = 0,
+              length: int | None = None, stream: int | None = None) -> None:
+        """replay (codec.hpp:375) over device pointers, asynchronously on `stream`."""
+        length = strip - off if length is None else length
+        L.check(_clib().pyrit_cu_apply(self._h, _ptr_array(list(in_ptrs)), _ptr_array(list(out_ptrs)), strip, off,
+                                      length, stream))
+
+    def prepare(self) -> None:
+        L.check(_clib().pyrit_cu_prepare(self._h))
+
+    def close(self):
+        if self._h:
+            _clib().pyrit_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _stream_of(t):
+    import torch
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _rows(t) -> list[int]:
+    return [t[i].data_ptr() for i in range(t.shape[0])]
+
+
+def encode(data, code: CodeSpec):
+    """encode (codec.hpp:469-477): data is a (k, symbol_size) uint8 CUDA tensor; returns (r, symbol_size)."""
+    import torch
+    if data.dim() != 2 or data.shape[0] != code.k or data.dtype != torch.uint8 or not data.is_cuda:
+        raise PyritError(4, "data buffer does not match the code")
+    data = data.contiguous()
+    parity = torch.empty((code.r, data.shape[1]), dtype=torch.uint8, device=data.device)
+    L.check(_clib().pyrit_cu_encode(C.byref(code.c()), _ptr_array(_rows(data)), _ptr_array(_rows(parity)),
+                                   data.shape[1], _stream_of(data)))
+    return parity
+
+
+def decode(symbols, erased: Iterable[int], code: CodeSpec) -> None:
+    """decode (codec.hpp:498-541), in place on a (k + r, symbol_size) uint8 CUDA tensor."""
+    import torch
+    if symbols.dim() != 2 or symbols.shape[0] != code.k + code.r or symbols.dtype != torch.uint8:
+        raise PyritError(4, "symbol buffer does not match the code")
+    er = np.asarray(list(erased), dtype=np.uint32)
+    L.check(_clib().pyrit_cu_decode(C.byref(code.c()), _ptr_array(_rows(symbols)), er.ctypes.data, er.size,
+                                   symbols.shape[1], _stream_of(symbols)))
+
+
+def encode_host(data: np.ndarray, code: CodeSpec, device: int = 0, parity: np.ndarray | None = None) -> np.ndarray:
+    """encode with host buffers (H2D, fused kernel, D2H inside): data (k, symbol_size) uint8."""
+    data = np.ascontiguousarray(data, dtype=np.uint8)
+    if data.ndim != 2 or data.shape[0] != code.k:
+        raise PyritError(4, "data buffer does not match the code")
+    if parity is None:
+        parity = np.empty((code.r, data.shape[1]), dtype=np.uint8)
+    L.check(_clib().pyrit_encode_host(C.byref(code.c()), data.ctypes.data, parity.ctypes.data, data.shape[1], device))
+    return parity
+
+
+def decode_host(symbols: np.ndarray, erased: Iterable[int], code: CodeSpec, device: int = 0) -> None:
+    """decode with host buffers, in place on a (k + r, symbol_size) uint8 array."""
+    if symbols.ndim != 2 or symbols.shape[0] != code.k + code.r or not symbols.flags.c_contiguous:
+        raise PyritError(4, "symbol buffer does not match the code")
+    er = np.asarray(list(erased), dtype=np.uint32)
+    L.check(_clib().pyrit_decode_host(C.byref(code.c()), symbols.ctypes.data, er.ctypes.data, er.size,
+                                     symbols.shape[1], device))
+
+
+def fill(t, seed: int, frag: int, begin: int = 0, valid: int | None = None, stream: int | None = None) -> None:
+    """Seeded synthetic bytes (same definition as oracle/pyrit_oracle.c or_fill) into a CUDA tensor."""
+    n = t.numel()
+    valid = begin + n if valid is None else valid
+    L.check(_clib().pyrit_cu_fill(seed, frag, t.data_ptr(), begin, n, valid,
+                                 _stream_of(t) if stream is None else stream))
+
+
+def digest(t, word_offset: int = 0, out=None, stream: int | None = None):
+    """K3 slice digest: out (1-element uint64 CUDA tensor) += digest(t)."""
+    import torch
+    if out is None:
+        out = torch.zeros(1, dtype=torch.int64, device=t.device)
+    L.check(_clib().pyrit_cu_digest(t.data_ptr(), t.numel(), word_offset, out.data_ptr(),
+                                   _stream_of(t) if stream is None else stream))
+    return out

@@ -1,0 +1,140 @@
+"""Build libpyrit_b200.so in-tree (sm_100a) and prebuild the generated ring kernels.
+
+    python -m paper_1709_00178_b200.build [--force] [--no-prebuild]
+
+Steps
+  1. g++ (C++20) compiles the host algebra, program compiler, runtime, pipeline
+     and C ABI; nvcc compiles the ahead-of-time kernels (kernels.cu) with
+     -gencode arch=compute_100a,code=sm_100a -lineinfo; both link into
+     paper_1709_00178_b200/libpyrit_b200.so (static cudart, NVRTC, hidden internals).
+  2. For the BASELINE.json encode/decode programs, the library's own code
+     generator emits CUDA C which nvcc compiles to
+     paper_1709_00178_b200/kernels/<kernel>.cubin; the runtime loads those before
+     falling back to NVRTC, so no JIT happens for the benchmarked plans.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+BUILD = os.path.join(ROOT, "build")
+LIB = os.path.join(PKG, "libpyrit_b200.so")
+KDIR = os.path.join(PKG, "kernels")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA, "bin", "nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+HOST_SOURCES = ["algebra.cpp", "program.cpp", "runtime.cpp", "pipeline.cpp", "capi.cpp"]
+CUDA_SOURCES = ["kernels.cu"]
+HEADERS = ["algebra.hpp", "program.hpp", "runtime.hpp", "pipeline.hpp", "kernels.hpp"]
+
+
+def _run(cmd, **kw):
+    print("+", " ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True, **kw)
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_library(force=False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "pyrit_b200.h")]
+    objs = []
+    for src in HOST_SOURCES:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(BUILD, src + ".o")
+        if force or _stale(o, [s] + hdrs):
+            _run(["g++", "-std=c++20", "-O2", "-g", "-fPIC", "-fvisibility=hidden", "-Wall", "-Wextra",
+                  f"-I{CUDA}/include", "-c", s, "-o", o])
+        objs.append(o)
+    for src in CUDA_SOURCES:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(BUILD, src + ".o")
+        if force or _stale(o, [s] + hdrs):
+            _run([NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
+                  "-Xptxas", "-v", "-c", s, "-o", o])
+        objs.append(o)
+    if force or _stale(LIB, objs):
+        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static", f"-L{CUDA}/lib64", "-lnvrtc",
+              "-Xlinker", f"-rpath,{CUDA}/lib64", "-Xlinker", "--exclude-libs,ALL", "-ldl", "-lpthread", "-lrt"])
+    return LIB
+
+
+# (name, field, k, r, erased) -- the programs bench.py and the GPU tests run
+def baseline_programs():
+    gf16 = (4, 5, 0, 1, 4, 0x1F)
+    gf256 = (8, 17, 0, 1, 8, 0x139)
+    gf1024 = (10, 11, 0, 1, 10, 0x7FF)
+    gf4096 = (12, 13, 0, 1, 12, 0x1FFF)
+    return [
+        ("cfg1", gf16, 4, 2, None),
+        ("cfg2", gf256, 10, 4, None),
+        ("cfg3", gf1024, 12, 4, None),
+        ("cfg4-dec", gf256, 10, 4, (1, 6, 9, 10)),
+        ("cfg4-dec-data", gf256, 10, 4, (0, 1, 2, 3)),
+        ("cfg5", gf4096, 16, 4, None),
+    ]
+
+
+def prebuild_kernels(lanes=(1,), force=False) -> list[str]:
+    """Generate + nvcc-compile the BASELINE plans' kernels into kernels/*.cubin."""
+    sys.path.insert(0, ROOT)
+    from paper_1709_00178_b200 import _lib as L  # noqa: E402
+
+    lib = L.load()
+    os.makedirs(KDIR, exist_ok=True)
+    src_dir = os.path.join(BUILD, "generated")
+    os.makedirs(src_dir, exist_ok=True)
+    built = []
+    for tag, fld, k, r, erased in baseline_programs():
+        code = L.pyrit_code(k, r, L.pyrit_field(*fld), 0)
+        plan = C.c_void_p()
+        if erased is None:
+            L.check(lib.pyrit_plan_encode(C.byref(code), C.byref(plan)))
+        else:
+            er = (C.c_uint32 * len(erased))(*erased)
+            L.check(lib.pyrit_plan_decode(C.byref(code), er, len(erased), C.byref(plan), None, None))
+        try:
+            for ln in lanes:
+                size = C.c_size_t(0)
+                name = C.create_string_buffer(128)
+                L.check(lib.pyrit_plan_source(plan, ln, None, 0, C.byref(size), name, 128))
+                buf = C.create_string_buffer(size.value + 1)
+                L.check(lib.pyrit_plan_source(plan, ln, buf, size.value + 1, None, None, 0))
+                nm = name.value.decode()
+                cu = os.path.join(src_dir, nm + ".cu")
+                cubin = os.path.join(KDIR, nm + ".cubin")
+                with open(cu, "w") as f:
+                    f.write(buf.value.decode())
+                if force or not os.path.exists(cubin):
+                    _run([NVCC, "-cubin", *ARCH, "-lineinfo", "-O3", "-Xptxas", "-v", cu, "-o", cubin])
+                built.append(cubin)
+        finally:
+            lib.pyrit_plan_destroy(plan)
+    return built
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--no-prebuild", action="store_true")
+    ap.add_argument("--lanes", default="1")
+    a = ap.parse_args(argv)
+    build_library(a.force)
+    if not a.no_prebuild:
+        prebuild_kernels(tuple(int(x) for x in a.lanes.split(",")), a.force)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,453 @@
+// extern "C" boundary (include/pyrit_b200.h).  Every entry point catches
+// and maps errors to return codes; nothing throws across the ABI.
+#include "../../include/pyrit_b200.h"
+
+#include <cstring>
+#include <list>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <unordered_map>
+
+#include "algebra.hpp"
+#include "kernels.hpp"
+#include "pipeline.hpp"
+#include "program.hpp"
+#include "runtime.hpp"
+
+using namespace pyrit_b200;
+
+struct pyrit_plan {
+    Program prog;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return 1 + static_cast<int>(e.code());
+    } catch (const CudaFailure& e) {
+        g_last_error = e.what();
+        return e.code();
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of host memory";
+        return -2;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return -3;
+    }
+}
+
+Field to_field(const pyrit_field* f) {
+    if (!f) raise(Errc::InvalidArgument, "null field");
+    Field x;
+    x.w = f->w;
+    x.n = f->n;
+    x.kind = static_cast<FieldKind>(f->kind);
+    x.s = f->s;
+    x.r_esp = f->r_esp;
+    x.modulus = f->modulus;
+    validate_field(x);
+    return x;
+}
+
+void check_code(const pyrit_code* c) {
+    if (!c) raise(Errc::InvalidArgument, "null code");
+    if (c->k == 0) raise(Errc::InvalidArgument, "k must be at least 1");          // matrix.hpp:272-273
+    if (c->transform > 1) raise(Errc::InvalidArgument, "unknown transform");
+    const Field f = to_field(&c->field);
+    if (c->k + c->r > f.field_size()) raise(Errc::TooManySymbols, "k + r exceeds field size"); // :274-277
+}
+
+std::uint64_t strip_of(const pyrit_code* c, std::uint64_t symbol_size) {
+    // SymbolBuffer shape rule, codec.hpp:285-287
+    if (symbol_size == 0 || symbol_size % c->field.w != 0 || symbol_size % 8 != 0)
+        raise(Errc::BufferShape, "symbol size must be a positive multiple of w and of the word width");
+    return symbol_size / c->field.w;
+}
+
+// compiled programs for the top-level API, keyed by code (+ erasures)
+class PlanCache {
+public:
+    std::shared_ptr<const Program> get(const std::string& key) {
+        std::lock_guard<std::mutex> lk(mu_);
+        auto it = map_.find(key);
+        if (it == map_.end()) return nullptr;
+        lru_.splice(lru_.begin(), lru_, it->second.second);
+        return it->second.first;
+    }
+    void put(const std::string& key, std::shared_ptr<const Program> p) {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (map_.count(key)) return;
+        lru_.push_front(key);
+        map_[key] = {std::move(p), lru_.begin()};
+        while (map_.size() > 512) {
+            map_.erase(lru_.back());
+            lru_.pop_back();
+        }
+    }
+
+private:
+    std::mutex mu_;
+    std::list<std::string> lru_;
+    std::unordered_map<std::string, std::pair<std::shared_ptr<const Program>, std::list<std::string>::iterator>> map_;
+};
+
+PlanCache& cache() {
+    static PlanCache c;
+    return c;
+}
+
+std::string code_key(const pyrit_code* c) {
+    std::ostringstream s;
+    s << c->k << ',' << c->r << ',' << c->field.w << ',' << c->field.n << ',' << c->field.kind << ','
+      << c->field.s << ',' << c->field.r_esp << ',' << c->field.modulus << ',' << c->transform;
+    return s.str();
+}
+
+std::shared_ptr<const Program> encode_program(const pyrit_code* c) {
+    const std::string key = "E" + code_key(c);
+    if (auto p = cache().get(key)) return p;
+    const Field f = to_field(&c->field);
+    auto p = std::make_shared<const Program>(compile_program(
+        f, static_cast<TransformKind>(c->transform), cauchy_parity_matrix(c->k, c->r, f), CompileOptions{}));
+    cache().put(key, p);
+    return p;
+}
+
+struct DecodeProgram {
+    std::shared_ptr<const Program> prog;
+    RepairPlan repair;
+};
+
+DecodeProgram decode_program(const pyrit_code* c, const std::vector<std::uint32_t>& erased) {
+    const Field f = to_field(&c->field);
+    DecodeProgram d;
+    d.repair = repair_matrix(c->k, c->r, f, erased);
+    if (d.repair.outputs.empty()) return d;
+    std::ostringstream key;
+    key << "D" << code_key(c) << ':';
+    for (std::uint32_t o : d.repair.outputs) key << o << ',';
+    if (auto p = cache().get(key.str())) {
+        d.prog = p;
+        return d;
+    }
+    auto p = std::make_shared<const Program>(
+        compile_program(f, static_cast<TransformKind>(c->transform), d.repair.m, CompileOptions{}));
+    cache().put(key.str(), p);
+    d.prog = p;
+    return d;
+}
+
+} // namespace
+
+extern "C" {
+
+const char* pyrit_version(void) { return "pyrit_b200 0.1 (sm_100a, generated ring programs)"; }
+
+const char* pyrit_strerror(int code) {
+    static const char* errc[] = {"ok",
+                                 "ZeroInverse: multiplicative inverse of 0 requested",
+                                 "Singular: matrix inversion hit a zero pivot",
+                                 "TooManySymbols: k + r exceeds the field size",
+                                 "BufferShape: symbol buffer does not match the code geometry",
+                                 "TransformMismatch",
+                                 "InsufficientShards: fewer than k usable shards",
+                                 "HeaderMismatch",
+                                 "ChecksumError",
+                                 "BadHeader",
+                                 "IoError",
+                                 "InvalidArgument: bad API parameter"};
+    if (code >= 0 && code <= 11) return errc[code];
+    if (!g_last_error.empty()) return g_last_error.c_str();
+    if (code <= -2000) return "CUDA driver error";
+    if (code <= -1000) return "NVRTC error";
+    return "CUDA runtime error";
+}
+
+int pyrit_field_named(const char* name, pyrit_field* out) {
+    return guarded([&] {
+        if (!name || !out) raise(Errc::InvalidArgument, "null argument");
+        const std::string n = name;
+        if (n == "gf16") *out = pyrit_field{4, 5, 0, 1, 4, 0x1F};          // field.hpp:124-126
+        else if (n == "gf64") *out = pyrit_field{6, 9, 1, 3, 2, 0x49};     // field.hpp:127-129
+        else if (n == "gf256_r17") *out = pyrit_field{8, 17, 0, 1, 8, 0x139};
+        else if (n == "gf1024") *out = pyrit_field{10, 11, 0, 1, 10, 0x7FF};
+        else if (n == "gf4096") *out = pyrit_field{12, 13, 0, 1, 12, 0x1FFF};
+        else raise(Errc::InvalidArgument, "unknown field name " + n);
+    });
+}
+
+int pyrit_field_validate(const pyrit_field* f) {
+    return guarded([&] { to_field(f); });
+}
+
+int pyrit_gf_mul(const pyrit_field* f, uint32_t a, uint32_t b, uint32_t* out) {
+    return guarded([&] { *out = gf_mul(a, b, to_field(f)); });
+}
+
+int pyrit_gf_inv(const pyrit_field* f, uint32_t a, uint32_t* out) {
+    return guarded([&] { *out = gf_inv(a, to_field(f)); });
+}
+
+int pyrit_sparse_transform(const pyrit_field* f, uint32_t u, uint32_t* rep) {
+    return guarded([&] {
+        const Field x = to_field(f);
+        if (u >= x.field_size()) raise(Errc::InvalidArgument, "element outside the field");
+        *rep = sparse_transform(u, x);
+    });
+}
+
+int pyrit_fold_table(const pyrit_field* f, uint32_t* fold) {
+    return guarded([&] {
+        const auto t = fold_table(to_field(f));
+        std::memcpy(fold, t.data(), t.size() * sizeof(uint32_t));
+    });
+}
+
+int pyrit_cauchy_parity_matrix(const pyrit_code* code, uint16_t* out) {
+    return guarded([&] {
+        check_code(code);
+        const Matrix m = cauchy_parity_matrix(code->k, code->r, to_field(&code->field));
+        std::memcpy(out, m.e.data(), m.e.size() * sizeof(uint16_t));
+    });
+}
+
+int pyrit_decode_matrix(const pyrit_code* code, const uint32_t* survivors, uint16_t* out, uint32_t* rows) {
+    return guarded([&] {
+        check_code(code);
+        const Field f = to_field(&code->field);
+        const Matrix c = cauchy_parity_matrix(code->k, code->r, f);
+        const Matrix dm =
+            decode_matrix(code->k, code->r, f, c, std::vector<uint32_t>(survivors, survivors + code->k));
+        std::memcpy(out, dm.e.data(), dm.e.size() * sizeof(uint16_t));
+        *rows = dm.rows;
+    });
+}
+
+int pyrit_repair_matrix(const pyrit_code* code, const uint32_t* erased, uint32_t n_erased, uint32_t* survivors,
+                        uint32_t* outputs, uint16_t* matrix) {
+    return guarded([&] {
+        check_code(code);
+        const RepairPlan rp = repair_matrix(code->k, code->r, to_field(&code->field),
+                                            std::vector<uint32_t>(erased, erased + n_erased));
+        std::memcpy(survivors, rp.survivors.data(), rp.survivors.size() * sizeof(uint32_t));
+        std::memcpy(outputs, rp.outputs.data(), rp.outputs.size() * sizeof(uint32_t));
+        std::memcpy(matrix, rp.m.e.data(), rp.m.e.size() * sizeof(uint16_t));
+    });
+}
+
+int pyrit_plan_create(const pyrit_field* f, uint32_t transform, const uint16_t* matrix, uint32_t rows,
+                      uint32_t cols, uint32_t rep, uint32_t group, pyrit_plan** out) {
+    return guarded([&] {
+        if (!out || (!matrix && rows != 0 && cols != 0)) raise(Errc::InvalidArgument, "null argument");
+        if (transform > 1) raise(Errc::InvalidArgument, "unknown transform");
+        Matrix m(rows, cols);
+        std::memcpy(m.e.data(), matrix, std::size_t(rows) * cols * sizeof(uint16_t));
+        CompileOptions opt;
+        opt.group = group;
+        opt.dense = rep == 1;
+        auto plan = std::make_unique<pyrit_plan>();
+        plan->prog = compile_program(to_field(f), static_cast<TransformKind>(transform), m, opt);
+        *out = plan.release();
+    });
+}
+
+int pyrit_plan_encode(const pyrit_code* code, pyrit_plan** out) {
+    return guarded([&] {
+        check_code(code);
+        auto plan = std::make_unique<pyrit_plan>();
+        plan->prog = *encode_program(code);
+        *out = plan.release();
+    });
+}
+
+int pyrit_plan_decode(const pyrit_code* code, const uint32_t* erased, uint32_t n_erased, pyrit_plan** out,
+                      uint32_t* survivors, uint32_t* outputs) {
+    return guarded([&] {
+        check_code(code);
+        const DecodeProgram d = decode_program(code, std::vector<uint32_t>(erased, erased + n_erased));
+        if (!d.prog) raise(Errc::InvalidArgument, "nothing erased");
+        auto plan = std::make_unique<pyrit_plan>();
+        plan->prog = *d.prog;
+        if (survivors) std::memcpy(survivors, d.repair.survivors.data(), d.repair.survivors.size() * sizeof(uint32_t));
+        if (outputs) std::memcpy(outputs, d.repair.outputs.data(), d.repair.outputs.size() * sizeof(uint32_t));
+        *out = plan.release();
+    });
+}
+
+int pyrit_plan_get_stats(const pyrit_plan* plan, pyrit_plan_stats* out) {
+    return guarded([&] {
+        if (!plan || !out) raise(Errc::InvalidArgument, "null argument");
+        const auto& s = plan->prog.stats;
+        out->rows = plan->prog.rows;
+        out->cols = plan->prog.cols;
+        out->matrix_ones = s.matrix_ones;
+        out->ref_region_ops = s.ref_region_ops;
+        out->naive_xors = s.naive_xors;
+        out->xors = s.xors;
+        out->loads = s.loads;
+        out->stores = s.stores;
+        out->group = plan->prog.group;
+    });
+}
+
+int pyrit_plan_reps(const pyrit_plan* plan, uint32_t* reps) {
+    return guarded([&] {
+        if (!plan || !reps) raise(Errc::InvalidArgument, "null argument");
+        std::memcpy(reps, plan->prog.reps.data(), plan->prog.reps.size() * sizeof(uint32_t));
+    });
+}
+
+int pyrit_plan_source(const pyrit_plan* plan, uint32_t lanes, char* buf, size_t cap, size_t* len, char* name,
+                      size_t name_cap) {
+    return guarded([&] {
+        if (!plan) raise(Errc::InvalidArgument, "null plan");
+        if (lanes != 0 && lanes != 1 && lanes != 2 && lanes != 4) raise(Errc::InvalidArgument, "bad lanes");
+        const KernelShape ks = shape_for(lanes);
+        const std::string src = generate_cuda(plan->prog, ks);
+        const std::string nm = kernel_name(plan->prog, ks);
+        if (len) *len = src.size();
+        if (buf && cap) {
+            const size_t n = std::min(cap - 1, src.size());
+            std::memcpy(buf, src.data(), n);
+            buf[n] = 0;
+        }
+        if (name && name_cap) {
+            const size_t n = std::min(name_cap - 1, nm.size());
+            std::memcpy(name, nm.data(), n);
+            name[n] = 0;
+        }
+    });
+}
+
+int pyrit_plan_interpret(const pyrit_plan* plan, const uint8_t* const* in, uint8_t* const* out,
+                         uint64_t strip_bytes, uint64_t off, uint64_t len) {
+    return guarded([&] {
+        if (!plan || !in || !out) raise(Errc::InvalidArgument, "null argument");
+        if (off + len > strip_bytes) raise(Errc::BufferShape, "column window out of range");
+        interpret_program(plan->prog, in, out, strip_bytes, off, len);
+    });
+}
+
+void pyrit_plan_destroy(pyrit_plan* plan) { delete plan; }
+
+int pyrit_cu_apply(const pyrit_plan* plan, const uint8_t* const* in, uint8_t* const* out, uint64_t strip_bytes,
+                   uint64_t off, uint64_t len, void* stream) {
+    return guarded([&] {
+        if (!plan || !in || !out) raise(Errc::InvalidArgument, "null argument");
+        launch_program(plan->prog, in, out, strip_bytes, off, len, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int pyrit_cu_prepare(const pyrit_plan* plan) {
+    return guarded([&] {
+        if (!plan) raise(Errc::InvalidArgument, "null plan");
+        prepare_program(plan->prog, preferred_lanes());
+    });
+}
+
+int pyrit_cu_encode(const pyrit_code* code, const uint8_t* const* data, uint8_t* const* parity,
+                    uint64_t symbol_size, void* stream) {
+    return guarded([&] {
+        check_code(code);
+        const std::uint64_t strip = strip_of(code, symbol_size);
+        if (!data || (!parity && code->r)) raise(Errc::InvalidArgument, "null symbol array");
+        if (code->r == 0) return;
+        auto p = encode_program(code);
+        launch_program(*p, data, parity, strip, 0, strip, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int pyrit_cu_decode(const pyrit_code* code, uint8_t* const* symbols, const uint32_t* erased, uint32_t n_erased,
+                    uint64_t symbol_size, void* stream) {
+    return guarded([&] {
+        check_code(code);
+        const std::uint64_t strip = strip_of(code, symbol_size);
+        if (!symbols || (!erased && n_erased)) raise(Errc::InvalidArgument, "null argument");
+        const DecodeProgram d = decode_program(code, std::vector<uint32_t>(erased, erased + n_erased));
+        if (!d.prog) return;
+        std::vector<const uint8_t*> in;
+        std::vector<uint8_t*> out;
+        for (uint32_t s : d.repair.survivors) in.push_back(symbols[s]);
+        for (uint32_t o : d.repair.outputs) out.push_back(symbols[o]);
+        launch_program(*d.prog, in.data(), out.data(), strip, 0, strip, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int pyrit_encode_host(const pyrit_code* code, const uint8_t* data, uint8_t* parity, uint64_t symbol_size,
+                      int device) {
+    return guarded([&] {
+        check_code(code);
+        const std::uint64_t strip = strip_of(code, symbol_size);
+        if (!data || (!parity && code->r)) raise(Errc::InvalidArgument, "null buffer");
+        if (code->r == 0) return;
+        auto p = encode_program(code);
+        std::vector<const uint8_t*> in;
+        std::vector<uint8_t*> out;
+        for (uint32_t j = 0; j < code->k; ++j) in.push_back(data + std::uint64_t(j) * symbol_size);
+        for (uint32_t i = 0; i < code->r; ++i) out.push_back(parity + std::uint64_t(i) * symbol_size);
+        run_host(*p, in, out, strip, device);
+    });
+}
+
+int pyrit_decode_host(const pyrit_code* code, uint8_t* symbols, const uint32_t* erased, uint32_t n_erased,
+                      uint64_t symbol_size, int device) {
+    return guarded([&] {
+        check_code(code);
+        const std::uint64_t strip = strip_of(code, symbol_size);
+        if (!symbols || (!erased && n_erased)) raise(Errc::InvalidArgument, "null argument");
+        const DecodeProgram d = decode_program(code, std::vector<uint32_t>(erased, erased + n_erased));
+        if (!d.prog) return;
+        std::vector<const uint8_t*> in;
+        std::vector<uint8_t*> out;
+        for (uint32_t s : d.repair.survivors) in.push_back(symbols + std::uint64_t(s) * symbol_size);
+        for (uint32_t o : d.repair.outputs) out.push_back(symbols + std::uint64_t(o) * symbol_size);
+        run_host(*d.prog, in, out, strip, device);
+    });
+}
+
+int pyrit_set_host_chunk(uint64_t strip_chunk_bytes) {
+    return guarded([&] {
+        if (strip_chunk_bytes % 16) raise(Errc::InvalidArgument, "chunk must be a multiple of 16 bytes");
+        set_host_chunk(strip_chunk_bytes);
+    });
+}
+
+int pyrit_cu_fill(uint64_t seed, uint64_t frag, uint8_t* dst, uint64_t begin, uint64_t len, uint64_t valid,
+                  void* stream) {
+    return guarded([&] {
+        if (!dst && len) raise(Errc::InvalidArgument, "null buffer");
+        if (begin % 8 || reinterpret_cast<std::uintptr_t>(dst) % 8)
+            raise(Errc::InvalidArgument, "fill needs 8-byte aligned begin and destination");
+        check_cuda(launch_fill(seed, frag, dst, begin, len, valid, static_cast<cudaStream_t>(stream)), "fill");
+    });
+}
+
+int pyrit_cu_digest(const uint8_t* src, uint64_t len, uint64_t word_offset, uint64_t* out, void* stream) {
+    return guarded([&] {
+        if ((!src && len) || !out) raise(Errc::InvalidArgument, "null buffer");
+        if (reinterpret_cast<std::uintptr_t>(src) % 8) raise(Errc::InvalidArgument, "digest needs 8-byte alignment");
+        check_cuda(launch_digest(src, len, word_offset, out, static_cast<cudaStream_t>(stream)), "digest");
+    });
+}
+
+int pyrit_set_lanes(uint32_t lanes) {
+    return guarded([&] { set_preferred_lanes(lanes); });
+}
+
+int pyrit_set_kernel_dir(const char* dir) {
+    return guarded([&] { set_kernel_dir(dir ? dir : ""); });
+}
+
+uint64_t pyrit_jit_compiles(void) { return jit_compiles(); }
+uint64_t pyrit_kernel_launches(void) { return kernel_launches(); }
+
+} // extern "C"

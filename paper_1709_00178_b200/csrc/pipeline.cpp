@@ -1,0 +1,99 @@
+// Host-buffer path: the end-to-end encode()/decode() a reference user calls
+// with SymbolBuffer-resident bytes (codec.hpp:469, :498).  Strips are moved
+// in column chunks through a ring of device staging slots, one stream per
+// slot, so the H2D copy of chunk c+1, the fused kernel of chunk c and the
+// D2H copy of chunk c-1 overlap on the two copy engines and the SMs.
+#include "pipeline.hpp"
+
+#include <algorithm>
+#include <map>
+#include <memory>
+#include <mutex>
+
+namespace pyrit_b200 {
+
+namespace {
+
+constexpr int kSlots = 3;
+
+struct Slot {
+    cudaStream_t stream = nullptr;
+    std::uint8_t* buf = nullptr;
+    std::size_t bytes = 0;
+};
+
+struct DeviceCtx {
+    std::mutex mu;
+    int device = 0;
+    Slot slots[kSlots];
+};
+
+std::mutex g_ctx_mu;
+std::map<int, std::unique_ptr<DeviceCtx>> g_ctx;
+std::uint64_t g_chunk = 0;
+
+DeviceCtx& ctx_for(int device) {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    auto& c = g_ctx[device];
+    if (!c) {
+        c = std::make_unique<DeviceCtx>();
+        c->device = device;
+    }
+    return *c;
+}
+
+} // namespace
+
+void set_host_chunk(std::uint64_t bytes) { g_chunk = bytes; }
+
+void run_host(const Program& p, const std::vector<const std::uint8_t*>& host_in,
+              const std::vector<std::uint8_t*>& host_out, std::uint64_t strip, int device) {
+    const std::uint32_t w = p.field.w;
+    if (host_in.size() != p.cols || host_out.size() != p.rows) raise(Errc::BufferShape, "symbol count mismatch");
+    if (p.rows == 0 || strip == 0) return;
+    DeviceCtx& ctx = ctx_for(device);
+    std::lock_guard<std::mutex> lk(ctx.mu);
+    check_cuda(cudaSetDevice(device), "cudaSetDevice");
+
+    const std::uint64_t strips = std::uint64_t(p.cols + p.rows) * w;
+    std::uint64_t chunk = g_chunk;
+    if (chunk == 0) chunk = (std::uint64_t(96) << 20) / strips; // ~96 MiB of staging per slot
+    chunk = std::max<std::uint64_t>(chunk, 64 * 1024) & ~std::uint64_t(4095);
+    if (strip % 16 == 0) chunk = std::min(chunk, strip);
+    else chunk = std::min(chunk, strip & ~std::uint64_t(15)); // tail chunk handled in byte mode
+    if (chunk == 0) chunk = strip;
+    const std::size_t need = static_cast<std::size_t>(strips * chunk);
+    for (Slot& s : ctx.slots) {
+        if (!s.stream) check_cuda(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "stream");
+        if (s.bytes < need) {
+            if (s.buf) check_cuda(cudaFree(s.buf), "cudaFree");
+            s.buf = nullptr;
+            s.bytes = 0;
+            check_cuda(cudaMalloc(&s.buf, need), "cudaMalloc staging");
+            s.bytes = need;
+        }
+    }
+    std::vector<const std::uint8_t*> din(p.cols);
+    std::vector<std::uint8_t*> dout(p.rows);
+    std::uint64_t c0 = 0;
+    for (int c = 0; c0 < strip; ++c) {
+        const std::uint64_t len = std::min(chunk, strip - c0);
+        Slot& s = ctx.slots[c % kSlots];
+        for (std::uint32_t j = 0; j < p.cols; ++j) {
+            std::uint8_t* d = s.buf + std::uint64_t(j) * w * chunk;
+            check_cuda(cudaMemcpy2DAsync(d, chunk, host_in[j] + c0, strip, len, w, cudaMemcpyHostToDevice, s.stream),
+                       "H2D");
+            din[j] = d;
+        }
+        for (std::uint32_t i = 0; i < p.rows; ++i) dout[i] = s.buf + std::uint64_t(p.cols + i) * w * chunk;
+        launch_program(p, din.data(), dout.data(), chunk, 0, len, s.stream);
+        for (std::uint32_t i = 0; i < p.rows; ++i)
+            check_cuda(cudaMemcpy2DAsync(host_out[i] + c0, strip, dout[i], chunk, len, w, cudaMemcpyDeviceToHost,
+                                         s.stream),
+                       "D2H");
+        c0 += len;
+    }
+    for (Slot& s : ctx.slots) check_cuda(cudaStreamSynchronize(s.stream), "cudaStreamSynchronize");
+}
+
+} // namespace pyrit_b200

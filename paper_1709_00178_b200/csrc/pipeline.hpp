@@ -1,0 +1,18 @@
+// Host-buffer (end-to-end) encode/decode pipeline.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "runtime.hpp"
+
+namespace pyrit_b200 {
+
+// Apply `p` to host symbols: host_in[j] / host_out[i] point at symbols of
+// w strips of `strip` bytes.  Synchronous on return.
+void run_host(const Program& p, const std::vector<const std::uint8_t*>& host_in,
+              const std::vector<std::uint8_t*>& host_out, std::uint64_t strip, int device);
+
+void set_host_chunk(std::uint64_t bytes);
+
+} // namespace pyrit_b200

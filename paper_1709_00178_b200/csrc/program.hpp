@@ -1,0 +1,83 @@
+// Ring program compiler: the B200 replacement for compile_schedule
+// (schedule.hpp:94-163).
+//
+// The reference compiles a generator matrix into a flat list of
+// whole-strip region ops (Copy/Xor/Zero) that replay() streams through
+// memory one op at a time (codec.hpp:118-157).  Here the same ring
+// semantics -- output ring row t of output i accumulates input strip
+// (t - sh) mod n for every shift sh of the entry's minimal-weight
+// representative, strips >= w of an embedded input are identically zero,
+// and the top rows are folded back by x^t mod p -- are compiled into a
+// straight-line SSA program over per-thread registers, which the code
+// generator turns into one fused CUDA kernel: every input byte is read
+// from HBM once and every output byte written once.
+//
+// XOR is associative and commutative, so the compiler is free to share
+// common pairs between ring rows (greedy pair elimination inside a group
+// of fragments whose strips are live in registers at the same time); the
+// bytes are identical to the reference's op-by-op replay.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "algebra.hpp"
+
+namespace pyrit_b200 {
+
+struct Instr {
+    enum Op : std::uint8_t { Load, Xor, Store } op;
+    std::uint32_t dst = 0;            // Load/Xor: defined variable
+    std::uint32_t sym = 0, strip = 0; // Load: input fragment/strip; Store: output fragment/strip
+    std::vector<std::uint32_t> src;   // Xor/Store: XOR of these variables (Store: empty = zero)
+};
+
+struct ProgramStats {
+    std::uint64_t matrix_ones = 0;   // sum of representative weights x w (schedule.hpp:112)
+    std::uint64_t ref_region_ops = 0; // what compile_schedule would emit (pre + core + post)
+    std::uint64_t naive_xors = 0;    // 2-input XORs of the ring program without sharing
+    std::uint64_t xors = 0;          // 2-input XORs after pair elimination
+    std::uint64_t loads = 0, stores = 0, vars = 0;
+};
+
+struct Program {
+    Field field;
+    TransformKind kind = TransformKind::Embedding;
+    std::uint32_t rows = 0, cols = 0; // outputs x inputs
+    std::uint32_t group = 1;          // input fragments whose strips are live together
+    std::vector<std::uint32_t> reps;  // rows x cols ring representatives (n-bit masks)
+    std::vector<std::uint32_t> fold;  // fold[t - w] = x^t mod p
+    std::vector<Instr> code;
+    std::uint32_t nvars = 0;
+    ProgramStats stats;
+};
+
+struct CompileOptions {
+    std::uint32_t group = 0;   // 0: choose automatically
+    bool cse = true;           // greedy pair elimination
+    bool dense = false;        // RingRep::Dense (plain phi1) instead of Sparse (schedule.hpp:78)
+};
+
+// compile_schedule analogue: matrix (rows x cols, GF(2^w) entries) -> program
+Program compile_program(const Field& f, TransformKind kind, const Matrix& m, const CompileOptions& opt);
+
+// Host interpreter of a compiled program (verification of the compiler on
+// machines without a GPU; never used by the device path).  Window
+// [off, off+len) of every strip; strip i of symbol j is in[j] + i*strip.
+void interpret_program(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
+                       std::uint64_t strip, std::uint64_t off, std::uint64_t len);
+
+// CUDA C source of the fused kernel for this program.
+//   lanes: 32-bit words per thread per strip (1, 2 or 4); 0 = byte mode
+struct KernelShape {
+    std::uint32_t lanes = 1;
+    std::uint32_t threads = 256;
+    std::uint32_t min_blocks = 2;
+};
+std::string kernel_name(const Program& p, const KernelShape& ks);
+std::string generate_cuda(const Program& p, const KernelShape& ks);
+
+std::uint64_t fnv1a(const std::string& s);
+
+} // namespace pyrit_b200

@@ -1,0 +1,244 @@
+#include "runtime.hpp"
+
+#include <cuda.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <atomic>
+#include <cstdlib>
+#include <fstream>
+#include <iterator>
+#include <mutex>
+#include <unordered_map>
+#include <vector>
+
+namespace pyrit_b200 {
+
+void check_cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw CudaFailure(-static_cast<int>(e), std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+// Driver entry points, resolved through the runtime so the library loads
+// on machines without a driver (the build container).
+struct Driver {
+    CUresult (*moduleLoadData)(CUmodule*, const void*) = nullptr;
+    CUresult (*moduleGetFunction)(CUfunction*, CUmodule, const char*) = nullptr;
+    CUresult (*launchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                             CUstream, void**, void**) = nullptr;
+    CUresult (*occupancy)(int*, CUfunction, int, size_t) = nullptr;
+    CUresult (*getErrorString)(CUresult, const char**) = nullptr;
+};
+
+template <class F>
+void resolve(const char* sym, F& fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    check_cuda(cudaGetDriverEntryPoint(sym, &p, cudaEnableDefault, &q), sym);
+    if (!p || q != cudaDriverEntryPointSuccess) throw CudaFailure(-1, std::string("driver symbol missing: ") + sym);
+    fn = reinterpret_cast<F>(p);
+}
+
+const Driver& driver() {
+    static std::once_flag once;
+    static Driver d;
+    std::call_once(once, [] {
+        resolve("cuModuleLoadData", d.moduleLoadData);
+        resolve("cuModuleGetFunction", d.moduleGetFunction);
+        resolve("cuLaunchKernel", d.launchKernel);
+        resolve("cuOccupancyMaxActiveBlocksPerMultiprocessor", d.occupancy);
+        resolve("cuGetErrorString", d.getErrorString);
+    });
+    return d;
+}
+
+void check_cu(CUresult r, const char* what) {
+    if (r == CUDA_SUCCESS) return;
+    const char* msg = "unknown";
+    if (driver().getErrorString) driver().getErrorString(r, &msg);
+    throw CudaFailure(-2000 - static_cast<int>(r), std::string(what) + ": " + msg);
+}
+
+struct LoadedKernel {
+    CUfunction fn = nullptr;
+    int blocks_per_sm = 1;
+    int sms = 148;
+};
+
+std::mutex g_mu;
+std::unordered_map<std::string, LoadedKernel> g_kernels; // name@device
+std::unordered_map<std::string, CUmodule> g_modules;
+std::atomic<std::uint64_t> g_jit{0}, g_launches{0};
+std::atomic<std::uint32_t> g_lanes{0};
+std::string g_kernel_dir;
+
+std::string default_kernel_dir() {
+    Dl_info info{};
+    if (dladdr(reinterpret_cast<void*>(&default_kernel_dir), &info) && info.dli_fname) {
+        std::string so = info.dli_fname;
+        const auto slash = so.rfind('/');
+        return (slash == std::string::npos ? std::string(".") : so.substr(0, slash)) + "/kernels";
+    }
+    return "kernels";
+}
+
+std::vector<char> read_file(const std::string& path) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) return {};
+    return std::vector<char>(std::istreambuf_iterator<char>(f), {});
+}
+
+std::vector<char> nvrtc_compile(const std::string& src, const std::string& name) {
+    nvrtcProgram prog;
+    auto chk = [&](nvrtcResult r, const char* what) {
+        if (r != NVRTC_SUCCESS)
+            throw CudaFailure(-1000 - static_cast<int>(r), std::string(what) + ": " + nvrtcGetErrorString(r));
+    };
+    chk(nvrtcCreateProgram(&prog, src.c_str(), (name + ".cu").c_str(), 0, nullptr, nullptr), "nvrtcCreateProgram");
+    const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "-DNDEBUG"};
+    const nvrtcResult rc = nvrtcCompileProgram(prog, 4, opts);
+    if (rc != NVRTC_SUCCESS) {
+        size_t n = 0;
+        nvrtcGetProgramLogSize(prog, &n);
+        std::string log(n, '\0');
+        nvrtcGetProgramLog(prog, log.data());
+        nvrtcDestroyProgram(&prog);
+        throw CudaFailure(-1000 - static_cast<int>(rc), "NVRTC failed for " + name + ":\n" + log);
+    }
+    size_t n = 0;
+    chk(nvrtcGetCUBINSize(prog, &n), "nvrtcGetCUBINSize");
+    std::vector<char> cubin(n);
+    chk(nvrtcGetCUBIN(prog, cubin.data()), "nvrtcGetCUBIN");
+    nvrtcDestroyProgram(&prog);
+    ++g_jit;
+    return cubin;
+}
+
+LoadedKernel load_kernel(const Program& p, const KernelShape& ks, int device) {
+    const std::string name = kernel_name(p, ks);
+    const std::string key = name + "@" + std::to_string(device);
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = g_kernels.find(key);
+        if (it != g_kernels.end()) return it->second;
+    }
+    std::vector<char> cubin = read_file(kernel_dir() + "/" + name + ".cubin");
+    if (cubin.empty()) cubin = nvrtc_compile(generate_cuda(p, ks), name);
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_kernels.find(key);
+    if (it != g_kernels.end()) return it->second;
+    check_cuda(cudaSetDevice(device), "cudaSetDevice");
+    CUmodule mod = nullptr;
+    check_cu(driver().moduleLoadData(&mod, cubin.data()), "cuModuleLoadData");
+    LoadedKernel k;
+    check_cu(driver().moduleGetFunction(&k.fn, mod, name.c_str()), "cuModuleGetFunction");
+    check_cu(driver().occupancy(&k.blocks_per_sm, k.fn, static_cast<int>(ks.threads), 0), "occupancy");
+    if (k.blocks_per_sm < 1) k.blocks_per_sm = 1;
+    check_cuda(cudaDeviceGetAttribute(&k.sms, cudaDevAttrMultiProcessorCount, device), "sm count");
+    g_modules[key] = mod;
+    g_kernels[key] = k;
+    return k;
+}
+
+bool aligned(const void* p, std::uint64_t v) { return reinterpret_cast<std::uintptr_t>(p) % v == 0; }
+
+} // namespace
+
+std::uint32_t preferred_lanes() {
+    std::uint32_t l = g_lanes.load();
+    if (l == 0) {
+        const char* env = std::getenv("PYRIT_B200_LANES");
+        l = env ? static_cast<std::uint32_t>(std::atoi(env)) : 1;
+        if (l != 1 && l != 2 && l != 4) l = 1;
+        g_lanes = l;
+    }
+    return l;
+}
+
+void set_preferred_lanes(std::uint32_t lanes) {
+    if (lanes != 1 && lanes != 2 && lanes != 4) raise(Errc::InvalidArgument, "lanes must be 1, 2 or 4");
+    g_lanes = lanes;
+}
+
+void set_kernel_dir(const std::string& dir) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_kernel_dir = dir;
+}
+
+std::string kernel_dir() {
+    if (g_kernel_dir.empty()) {
+        const char* env = std::getenv("PYRIT_B200_KERNEL_DIR");
+        g_kernel_dir = env ? env : default_kernel_dir();
+    }
+    return g_kernel_dir;
+}
+
+std::uint64_t jit_compiles() { return g_jit.load(); }
+std::uint64_t kernel_launches() { return g_launches.load(); }
+
+KernelShape shape_for(std::uint32_t lanes) {
+    KernelShape ks;
+    ks.lanes = lanes;
+    ks.threads = 256;
+    // one block per SM guaranteed: lets ptxas keep the larger ring programs
+    // (up to ~240 live words) spill-free; occupancy follows actual usage
+    ks.min_blocks = 1;
+    return ks;
+}
+
+std::string prepare_program(const Program& p, std::uint32_t lanes) {
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    const KernelShape ks = shape_for(lanes);
+    load_kernel(p, ks, dev);
+    return kernel_name(p, ks);
+}
+
+LaunchInfo launch_program(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
+                          std::uint64_t strip, std::uint64_t off, std::uint64_t len, cudaStream_t stream) {
+    LaunchInfo info;
+    if (off + len > strip) raise(Errc::BufferShape, "column window out of range");
+    if (len == 0) return info;
+    // widest vector the alignment of every pointer, the strip pitch and the
+    // window allows; byte mode otherwise
+    std::uint32_t lanes = 0;
+    for (std::uint32_t l = preferred_lanes(); l >= 1; l /= 2) {
+        const std::uint64_t v = 4ull * l;
+        bool ok = strip % v == 0 && off % v == 0 && len % v == 0;
+        for (std::uint32_t j = 0; ok && j < p.cols; ++j) ok = aligned(in[j], v);
+        for (std::uint32_t i = 0; ok && i < p.rows; ++i) ok = aligned(out[i], v);
+        if (ok) {
+            lanes = l;
+            break;
+        }
+    }
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    const KernelShape ks = shape_for(lanes);
+    const LoadedKernel k = load_kernel(p, ks, dev);
+    const std::uint64_t vbytes = lanes ? 4ull * lanes : 1ull;
+    const std::uint64_t nwords = len / vbytes;
+    std::vector<std::uint64_t> args(std::size_t(p.cols) + p.rows + 3);
+    for (std::uint32_t j = 0; j < p.cols; ++j) args[j] = reinterpret_cast<std::uint64_t>(in[j]);
+    for (std::uint32_t i = 0; i < p.rows; ++i) args[p.cols + i] = reinterpret_cast<std::uint64_t>(out[i]);
+    args[p.cols + p.rows] = strip;
+    args[p.cols + p.rows + 1] = off;
+    args[p.cols + p.rows + 2] = nwords;
+    const std::uint64_t want = (nwords + ks.threads - 1) / ks.threads;
+    const std::uint64_t cap = std::uint64_t(k.sms) * std::uint64_t(k.blocks_per_sm);
+    const unsigned blocks = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min(want, cap)));
+    void* params[] = {args.data()};
+    check_cu(driver().launchKernel(k.fn, blocks, 1, 1, ks.threads, 1, 1, 0, reinterpret_cast<CUstream>(stream),
+                                   params, nullptr),
+             "cuLaunchKernel");
+    ++g_launches;
+    info.lanes = lanes;
+    info.threads = ks.threads;
+    info.blocks = blocks;
+    info.kernel = kernel_name(p, ks);
+    return info;
+}
+
+} // namespace pyrit_b200

@@ -1,0 +1,54 @@
+// Device runtime: compiles generated ring programs for sm_100a (prebuilt
+// cubins shipped next to the library, else NVRTC at first use), caches the
+// loaded modules per device, and launches them.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "program.hpp"
+
+namespace pyrit_b200 {
+
+// CUDA-side failure: carries a negative C-ABI code (see pyrit_b200.h)
+class CudaFailure : public std::runtime_error {
+public:
+    CudaFailure(int code, const std::string& what) : std::runtime_error(what), code_(code) {}
+    int code() const noexcept { return code_; }
+
+private:
+    int code_;
+};
+
+void check_cuda(cudaError_t e, const char* what);
+
+struct LaunchInfo {
+    std::uint32_t lanes = 1, threads = 0, blocks = 0;
+    std::string kernel;
+};
+
+// Apply the program to the byte window [off, off+len) of every strip.
+// in[j] / out[i] are device base pointers of input / output symbols; strip
+// s of a symbol starts at base + s * strip.  Asynchronous on `stream`.
+LaunchInfo launch_program(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
+                          std::uint64_t strip, std::uint64_t off, std::uint64_t len, cudaStream_t stream);
+
+// Force compilation/loading for the current device (no launch).
+std::string prepare_program(const Program& p, std::uint32_t lanes);
+
+// Lanes (32-bit words per thread per strip) preferred when alignment allows.
+std::uint32_t preferred_lanes();
+void set_preferred_lanes(std::uint32_t lanes);
+
+// Directory searched for prebuilt <kernel>.cubin files.
+void set_kernel_dir(const std::string& dir);
+std::string kernel_dir();
+
+std::uint64_t jit_compiles(); // number of NVRTC compilations performed so far
+std::uint64_t kernel_launches(); // number of generated-kernel launches so far
+
+KernelShape shape_for(std::uint32_t lanes);
+
+} // namespace pyrit_b200

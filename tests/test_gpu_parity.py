@@ -1,0 +1,226 @@
+"""GPU parity: the fused sm_100a kernels vs the CPU oracle, bit for bit.
+
+Every call goes through libpyrit_b200.so (C ABI): device buffers are torch CUDA
+tensors, results are copied back and compared with oracle/ (the plain-C
+restatement, itself pinned against the reference in test_oracle.py).
+"""
+from __future__ import annotations
+
+import itertools
+import random
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1709_00178_b200 as P
+from paper_1709_00178_b200 import _lib as L
+from paper_1709_00178_b200.workloads import WORKLOADS, shard
+from tests.helpers import G16, G64, G256, G1024, G4096, oracle_encode, oracle_ring, rand_symbols, seeded_symbols
+
+pytestmark = pytest.mark.gpu
+
+
+def dev_encode(cuda, code, data: np.ndarray) -> np.ndarray:
+    import torch
+    d = torch.from_numpy(data).to(cuda)
+    out = P.encode(d, code)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def dev_decode(cuda, code, symbols: np.ndarray, erased) -> np.ndarray:
+    import torch
+    d = torch.from_numpy(symbols).to(cuda)
+    P.decode(d, erased, code)
+    torch.cuda.synchronize()
+    return d.cpu().numpy()
+
+
+def test_library_is_the_native_one(cuda):
+    lib = L.load()
+    assert b"sm_100a" in lib.pyrit_version()
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 5])
+def test_baseline_encode_small(cuda, cfg):
+    """BASELINE configs at a reduced fragment size: GPU == ring oracle == field oracle."""
+    wl = WORKLOADS[cfg]
+    f = wl.fld
+    ss = f.w * 4096
+    data = seeded_symbols(wl.k, ss, f.w, wl.seed)
+    C = P.cauchy_parity_matrix(wl.code)
+    got = dev_encode(cuda, wl.code, data)
+    want = oracle_ring(f, C, data)
+    np.testing.assert_array_equal(got, want)
+    # field oracle (codec.hpp:444) on a window of every strip
+    strip = ss // f.w
+    outs = O.apply_columns(O.Field(f.w, f.n, f.kind, f.s, f.r_esp, f.modulus), C, list(data), strip, off=512,
+                           length=256)
+    for i in range(wl.m):
+        for s in range(f.w):
+            np.testing.assert_array_equal(got[i][s * strip + 512: s * strip + 768],
+                                          outs[i][s * strip + 512: s * strip + 768])
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_baseline_encode_full_size(cuda, cfg):
+    """Configs 1 and 2 at their full BASELINE size, every byte against the ring oracle."""
+    wl = WORKLOADS[cfg]
+    data = seeded_symbols(wl.k, wl.frag, wl.fld.w, wl.seed, valid=wl.valid)
+    got = dev_encode(cuda, wl.code, data)
+    want = oracle_ring(wl.fld, P.cauchy_parity_matrix(wl.code), data)
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("erased", [(1, 6, 9, 10), (0, 1, 2, 3), (10, 11, 12, 13), (2,), (0, 13)])
+def test_config4_decode(cuda, erased):
+    """Config 4 geometry (GF(2^8) in R_{2,17}, k=10, m=4): repair bit-exact, parity included."""
+    wl = WORKLOADS[4]
+    ss = wl.fld.w * 8192
+    data = seeded_symbols(wl.k, ss, wl.fld.w, wl.seed)
+    parity = oracle_ring(wl.fld, P.cauchy_parity_matrix(wl.code), data)
+    full = np.concatenate([data, parity])
+    work = full.copy()
+    work[list(erased)] = 0xAA
+    got = dev_decode(cuda, wl.code, work, erased)
+    np.testing.assert_array_equal(got, full)
+    # and the C oracle's decode (codec.hpp:498 restated) agrees on a window
+    work2 = full.copy()
+    work2[list(erased)] = 0x55
+    syms = [work2[i] for i in range(len(work2))]
+    strip = ss // wl.fld.w
+    O.decode(wl.k, wl.m, O.Field(8, 17, 0, 1, 8, 0x139), syms, erased, strip, off=0, length=strip)
+    np.testing.assert_array_equal(np.stack(syms), full)
+
+
+@pytest.mark.parametrize("spec", [G16, G64])
+@pytest.mark.parametrize("kind", [0, 1])
+def test_all_small_codes_match_oracle(cuda, spec, kind):
+    """test_codec.cpp:53-80 / test_schedule.cpp:104-136 grid: k, r in [1,5], both transforms."""
+    rng = random.Random(101 + kind)
+    for k in range(1, 6):
+        for r in range(1, 6):
+            code = P.CodeSpec(k, r, spec, P.TransformKind(kind))
+            ss = int(np.lcm(spec.w, 8)) * (1 + rng.randrange(3)) * 8
+            data = rand_symbols(k, ss, rng.randrange(1 << 30))
+            C = P.cauchy_parity_matrix(code)
+            got = dev_encode(cuda, code, data)
+            want = oracle_encode(spec, C, data, kind=kind)
+            np.testing.assert_array_equal(got, want, err_msg=f"k={k} r={r} kind={kind}")
+
+
+@pytest.mark.parametrize("grid", [(4, 2, G16), (6, 3, G16), (6, 3, G64)])
+@pytest.mark.parametrize("kind", [0, 1])
+def test_decode_erasure_patterns(cuda, grid, kind):
+    """test_codec.cpp:108-143: erasure patterns of weight <= r repair bit-exact (sampled on GPU;
+    every pattern is covered through the program interpreter in test_compiler.py)."""
+    k, r, spec = grid
+    code = P.CodeSpec(k, r, spec, P.TransformKind(kind))
+    ss = int(np.lcm(spec.w, 8)) * 16
+    data = rand_symbols(k, ss, 911)
+    full = np.concatenate([data, oracle_encode(spec, P.cauchy_parity_matrix(code), data, kind=kind)])
+    pats = [c for wgt in range(1, r + 1) for c in itertools.combinations(range(k + r), wgt)]
+    rng = random.Random(7)
+    for erased in rng.sample(pats, min(len(pats), 24)):
+        work = full.copy()
+        work[list(erased)] = 0xAA
+        np.testing.assert_array_equal(dev_decode(cuda, code, work, erased), full, err_msg=str(erased))
+
+
+def test_odd_strip_sizes_byte_mode(cuda):
+    """Strips that are not word multiples (SymbolBuffer allows any multiple of lcm(w, 8))."""
+    for spec, k, r in [(G16, 4, 2), (G64, 5, 3), (G256, 10, 4), (G4096, 16, 4)]:
+        code = P.CodeSpec(k, r, spec)
+        ss = int(np.lcm(spec.w, 8)) * 3  # strip of 6, 12, 3, 6 bytes
+        data = rand_symbols(k, ss, 5)
+        np.testing.assert_array_equal(dev_encode(cuda, code, data),
+                                      oracle_encode(spec, P.cauchy_parity_matrix(code), data))
+
+
+def test_empty_and_degenerate(cuda):
+    import torch
+    # r = 0: nothing to compute; decode with nothing erased is a no-op
+    code = P.CodeSpec(4, 0, G16)
+    d = torch.zeros((4, 16), dtype=torch.uint8, device=cuda)
+    assert P.encode(d, code).shape == (0, 16)
+    code = P.CodeSpec(4, 2, G16)
+    s = torch.arange(6 * 16, dtype=torch.int32, device=cuda).to(torch.uint8).view(6, 16)
+    before = s.clone()
+    P.decode(s, [], code)
+    assert torch.equal(s, before)
+    # too many erasures / bad shapes raise like the reference
+    with pytest.raises(P.PyritError) as e:
+        P.decode(s, [0, 1, 2], code)
+    assert e.value.code == "InsufficientShards"
+    with pytest.raises(P.PyritError):
+        P.encode(torch.zeros((4, 12), dtype=torch.uint8, device=cuda), code)  # 12 % 8 != 0
+
+
+def test_fill_and_digest_kernels(cuda):
+    import torch
+    t = torch.empty(1 << 20, dtype=torch.uint8, device=cuda)
+    P.fill(t, 4, 7, begin=8 * 1000, valid=8 * 1000 + 700_001)
+    want = O.fill_np(4, 7, 1 << 20, valid=8 * 1000 + 700_001, begin=8 * 1000)
+    np.testing.assert_array_equal(t.cpu().numpy(), want)
+    d = P.digest(t, word_offset=123)
+    torch.cuda.synchronize()
+    assert (int(d.item()) & (2**64 - 1)) == O.digest_np(want, 123)
+    # additivity over disjoint word ranges (the sharded "checksum of checksums")
+    a = P.digest(t[: 1 << 19], word_offset=123)
+    P.digest(t[1 << 19:], word_offset=123 + (1 << 16), out=a)
+    assert int(a.item()) == int(d.item())
+
+
+def test_shard_invariance_windows(cuda):
+    """Encoding byte-offset shards separately == one encode (test_codec.cpp:199-212 analogue)."""
+    import torch
+    wl = WORKLOADS[5]
+    ss = wl.fld.w * (1 << 16)
+    strip = ss // wl.fld.w
+    data = torch.from_numpy(seeded_symbols(wl.k, ss, wl.fld.w, 4)).to(cuda)
+    whole = P.encode(data, wl.code)
+    plan = P.Plan.encode(wl.code)
+    for world in (2, 4, 8):
+        out = torch.zeros_like(whole)
+        for rank in range(world):
+            lo, hi = shard(strip, rank, world)
+            plan.apply([data[j].data_ptr() for j in range(wl.k)], [out[i].data_ptr() for i in range(wl.m)], strip,
+                       lo, hi - lo, stream=torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert torch.equal(out, whole), world
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_host_buffer_path(cuda, cfg):
+    """pyrit_encode_host / pyrit_decode_host (H2D + kernel + D2H pipeline) == device path."""
+    wl = WORKLOADS[cfg]
+    ss = wl.fld.w * (1 << 18)
+    data = seeded_symbols(wl.k, ss, wl.fld.w, wl.seed)
+    L.check(L.load().pyrit_set_host_chunk(1 << 16))  # force several chunks through the slot ring
+    try:
+        parity = P.encode_host(data, wl.code)
+        np.testing.assert_array_equal(parity, dev_encode(cuda, wl.code, data))
+        if wl.op == "decode":
+            full = np.concatenate([data, parity])
+            work = full.copy()
+            work[list(wl.erased)] = 0
+            P.decode_host(work, wl.erased, wl.code)
+            np.testing.assert_array_equal(work, full)
+    finally:
+        L.check(L.load().pyrit_set_host_chunk(0))
+
+
+@pytest.mark.parametrize("lanes", [1, 2, 4])
+def test_vector_widths(cuda, lanes):
+    """The 4/8/16-byte-per-thread variants of the generated kernel agree."""
+    lib = L.load()
+    L.check(lib.pyrit_set_lanes(lanes))
+    try:
+        wl = WORKLOADS[3]
+        ss = wl.fld.w * 4096
+        data = seeded_symbols(wl.k, ss, wl.fld.w, 2)
+        np.testing.assert_array_equal(dev_encode(cuda, wl.code, data),
+                                      oracle_ring(wl.fld, P.cauchy_parity_matrix(wl.code), data))
+    finally:
+        L.check(lib.pyrit_set_lanes(1))
