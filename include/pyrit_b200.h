@@ -110,7 +110,10 @@ int pyrit_plan_decode(const pyrit_code* code, const uint32_t* erased, uint32_t n
                       uint32_t* survivors, uint32_t* outputs);
 int pyrit_plan_get_stats(const pyrit_plan* plan, pyrit_plan_stats* out);
 int pyrit_plan_reps(const pyrit_plan* plan, uint32_t* reps /* rows x cols */);
-/* generated CUDA source of the fused kernel; *len receives the full size */
+/* generated CUDA source of the fused kernel; *len receives the full size.
+ * lanes: 1/2/4 = direct LDG kernel with that many 32-bit words per thread per
+ * strip, 0 = byte mode, PYRIT_SOURCE_STAGED = the TMA-staged kernel */
+#define PYRIT_SOURCE_STAGED 100u
 int pyrit_plan_source(const pyrit_plan* plan, uint32_t lanes, char* buf, size_t cap, size_t* len,
                       char* name, size_t name_cap);
 /* verification aid: interprets the compiled program on HOST buffers (no
@@ -153,6 +156,10 @@ int pyrit_cu_digest(const uint8_t* src, uint64_t len, uint64_t word_offset, uint
 
 /* ---- runtime knobs and counters -------------------------------------- */
 int pyrit_set_lanes(uint32_t lanes); /* 32-bit words per thread per strip: 1, 2 or 4 */
+/* 0 = auto (TMA-staged kernel whenever pointers/pitch/window are 16-byte
+ * aligned and the tiles fit in shared memory), 1 = direct kernel only,
+ * 2 = staged whenever possible */
+int pyrit_set_kernel_mode(int mode);
 int pyrit_set_kernel_dir(const char* dir);
 uint64_t pyrit_jit_compiles(void);
 uint64_t pyrit_kernel_launches(void);

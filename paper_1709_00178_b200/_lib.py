@@ -30,6 +30,9 @@ class pyrit_plan_stats(C.Structure):
                 ("loads", C.c_uint64), ("stores", C.c_uint64), ("group", C.c_uint32)]
 
 
+SOURCE_STAGED = 100
+
+
 class PyritError(RuntimeError):
     """Mirror of pyrit::Error (errors.hpp:71-80): carries the Errc name/code."""
 
@@ -47,7 +50,7 @@ EXPORTS = (
     "pyrit_repair_matrix", "pyrit_plan_create", "pyrit_plan_encode", "pyrit_plan_decode", "pyrit_plan_get_stats",
     "pyrit_plan_reps", "pyrit_plan_source", "pyrit_plan_interpret", "pyrit_plan_destroy", "pyrit_cu_apply",
     "pyrit_cu_prepare", "pyrit_cu_encode", "pyrit_cu_decode", "pyrit_encode_host", "pyrit_decode_host",
-    "pyrit_set_host_chunk", "pyrit_cu_fill", "pyrit_cu_digest", "pyrit_set_lanes", "pyrit_set_kernel_dir",
+    "pyrit_set_host_chunk", "pyrit_cu_fill", "pyrit_cu_digest", "pyrit_set_lanes", "pyrit_set_kernel_mode", "pyrit_set_kernel_dir",
     "pyrit_jit_compiles", "pyrit_kernel_launches",
 )
 
@@ -86,6 +89,7 @@ def load():
     lib.pyrit_cu_digest.argtypes = [vp, u64, u64, vp, vp]
     lib.pyrit_set_lanes.argtypes = [u32]
     lib.pyrit_set_kernel_dir.argtypes = [C.c_char_p]
+    lib.pyrit_set_kernel_mode.argtypes = [i32]
     lib.pyrit_jit_compiles.restype = u64
     lib.pyrit_kernel_launches.restype = u64
     lib.pyrit_field_named.argtypes = [C.c_char_p, P(pyrit_field)]

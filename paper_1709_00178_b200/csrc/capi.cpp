@@ -310,8 +310,13 @@ int pyrit_plan_source(const pyrit_plan* plan, uint32_t lanes, char* buf, size_t 
                       size_t name_cap) {
     return guarded([&] {
         if (!plan) raise(Errc::InvalidArgument, "null plan");
-        if (lanes != 0 && lanes != 1 && lanes != 2 && lanes != 4) raise(Errc::InvalidArgument, "bad lanes");
-        const KernelShape ks = shape_for(lanes);
+        if (lanes != 0 && lanes != 1 && lanes != 2 && lanes != 4 && lanes != PYRIT_SOURCE_STAGED)
+            raise(Errc::InvalidArgument, "bad lanes");
+        KernelShape ks = shape_for(lanes == PYRIT_SOURCE_STAGED ? 1 : lanes);
+        if (lanes == PYRIT_SOURCE_STAGED) {
+            ks = staged_shape(plan->prog, 227 * 1024);
+            if (!ks.staged) raise(Errc::BufferShape, "program tiles do not fit in shared memory");
+        }
         const std::string src = generate_cuda(plan->prog, ks);
         const std::string nm = kernel_name(plan->prog, ks);
         if (len) *len = src.size();
@@ -441,6 +446,10 @@ int pyrit_cu_digest(const uint8_t* src, uint64_t len, uint64_t word_offset, uint
 
 int pyrit_set_lanes(uint32_t lanes) {
     return guarded([&] { set_preferred_lanes(lanes); });
+}
+
+int pyrit_set_kernel_mode(int mode) {
+    return guarded([&] { set_kernel_mode(mode); });
 }
 
 int pyrit_set_kernel_dir(const char* dir) {

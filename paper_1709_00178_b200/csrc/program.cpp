@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <bit>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
@@ -70,6 +71,40 @@ void toggle(std::vector<std::uint32_t>& set, std::uint32_t x) {
     auto it = std::find(set.begin(), set.end(), x);
     if (it == set.end()) set.push_back(x);
     else set.erase(it);
+}
+
+// Reorder so that every pair temporary (the first `ntemps` instructions,
+// as emitted by share_pairs) is defined right before its first use; keeps
+// the live range of shared sub-sums short.
+void lazy_order(std::vector<Instr>& code, std::size_t ntemps) {
+    std::vector<Instr> out;
+    out.reserve(code.size());
+    std::vector<std::size_t> def_of;
+    std::uint32_t lo = 0xFFFFFFFFu, hi = 0;
+    for (std::size_t i = 0; i < ntemps; ++i) {
+        lo = std::min(lo, code[i].dst);
+        hi = std::max(hi, code[i].dst + 1);
+    }
+    if (ntemps) def_of.assign(hi - lo, SIZE_MAX);
+    for (std::size_t i = 0; i < ntemps; ++i) def_of[code[i].dst - lo] = i;
+    std::vector<bool> done(ntemps, false);
+    std::vector<std::size_t> stack;
+    auto emit_deps = [&](const Instr& ins, auto&& self) -> void {
+        for (std::uint32_t v : ins.src)
+            if (ntemps && v >= lo && v < hi && def_of[v - lo] != SIZE_MAX && !done[def_of[v - lo]]) {
+                const std::size_t d = def_of[v - lo];
+                done[d] = true;
+                self(code[d], self);
+                out.push_back(code[d]);
+            }
+    };
+    for (std::size_t i = ntemps; i < code.size(); ++i) {
+        emit_deps(code[i], emit_deps);
+        out.push_back(code[i]);
+    }
+    for (std::size_t i = 0; i < ntemps; ++i)
+        if (!done[i]) out.push_back(code[i]);
+    code.swap(out);
 }
 
 } // namespace
@@ -154,6 +189,7 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
                 p.stats.naive_xors += tg.size(); // one XOR per term into the row...
             }
         if (opt.cse) share_pairs(targets, nvars, cp);
+        const std::size_t ntemps = cp.size();
         for (std::size_t r = 0; r < targets.size(); ++r) {
             auto& tg = targets[r];
             if (tg.empty()) continue;
@@ -167,6 +203,7 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
             acc[r] = x.dst;
             cp.push_back(std::move(x));
         }
+        lazy_order(cp, ntemps);
         loads.push_back(std::move(ld));
         compute.push_back(std::move(cp));
     }
@@ -177,6 +214,7 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
     // order: prefetch group g+1's strips before computing group g
     for (std::size_t g = 0; g < loads.size(); ++g) {
         if (g == 0) p.code.insert(p.code.end(), loads[0].begin(), loads[0].end());
+        // (direct mode) issue the next group's HBM loads before this group's XORs
         if (g + 1 < loads.size()) p.code.insert(p.code.end(), loads[g + 1].begin(), loads[g + 1].end());
         p.code.insert(p.code.end(), compute[g].begin(), compute[g].end());
     }
@@ -194,9 +232,16 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
                     }
             if (!targets[b].empty() && acc[i * out_rows + b] == kNone) --p.stats.naive_xors;
         }
-        if (opt.cse) share_pairs(targets, nvars, p.code);
-        for (std::uint32_t b = 0; b < w; ++b) p.code.push_back(Instr{Instr::Store, 0, i, b, targets[b]});
+        std::vector<Instr> fold;
+        if (opt.cse) share_pairs(targets, nvars, fold);
+        const std::size_t ntemps = fold.size();
+        for (std::uint32_t b = 0; b < w; ++b) fold.push_back(Instr{Instr::Store, 0, i, b, targets[b]});
+        lazy_order(fold, ntemps);
+        p.code.insert(p.code.end(), fold.begin(), fold.end());
+        p.tail.insert(p.tail.end(), fold.begin(), fold.end());
     }
+    p.group_loads = std::move(loads);
+    p.group_compute = std::move(compute);
     p.nvars = nvars;
     for (const Instr& in : p.code) {
         if (in.op == Instr::Load) ++p.stats.loads;
@@ -204,6 +249,42 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
         if (in.op != Instr::Load && in.src.size() > 1) p.stats.xors += in.src.size() - 1;
     }
     p.stats.vars = nvars;
+
+    // output parts for the staged kernel (see KernelShape): keep each part's
+    // ring accumulators (rows x out_rows words) near 40 registers
+    if (opt.parts != 1 && e > 0) {
+        // parts: the smallest power of two that keeps each part's program
+        // near 450 two-input XORs (about 200 live registers under ptxas)
+        std::uint32_t R = opt.parts;
+        if (!R) {
+            const char* env = std::getenv("PYRIT_B200_PARTS");
+            R = env ? static_cast<std::uint32_t>(std::atoi(env)) : 0;
+        }
+        if (!R) {
+            const std::uint64_t want = (p.stats.xors + 449) / 450;
+            R = 1;
+            while (R < want && R < 8) R *= 2;
+        }
+        R = std::max<std::uint32_t>(1, std::min(R, e));
+        std::uint32_t pg = opt.part_group;
+        if (!pg) {
+            const char* env = std::getenv("PYRIT_B200_PART_GROUP");
+            pg = env ? static_cast<std::uint32_t>(std::atoi(env)) : 8;
+        }
+        pg = std::max<std::uint32_t>(1, std::min(pg, k));
+        for (std::uint32_t r = 0, row0 = 0; r < R; ++r) {
+            const std::uint32_t nrows = e / R + (r < e % R ? 1 : 0);
+            Matrix sub(nrows, k);
+            for (std::uint32_t i = 0; i < nrows; ++i)
+                for (std::uint32_t j = 0; j < k; ++j) sub.at(i, j) = m.at(row0 + i, j);
+            CompileOptions o2 = opt;
+            o2.parts = 1;
+            o2.group = pg;
+            p.parts.push_back(compile_program(f, kind, sub, o2));
+            p.part_row0.push_back(row0);
+            row0 += nrows;
+        }
+    }
     return p;
 }
 
@@ -238,15 +319,205 @@ void interpret_program(const Program& p, const std::uint8_t* const* in, std::uin
 std::string kernel_name(const Program& p, const KernelShape& ks) {
     std::ostringstream fp;
     fp << p.field.w << ',' << p.field.n << ',' << p.field.modulus << ',' << int(p.kind) << ',' << p.rows << ','
-       << p.cols << ',' << p.group << ',' << ks.lanes << ',' << ks.threads << ',' << ks.min_blocks << ':';
+       << p.cols << ',' << p.group << ',' << ks.lanes << ',' << ks.threads << ',' << ks.min_blocks << ','
+       << ks.staged << ',' << ks.tile << ',' << ks.stages << ',' << ks.bar_bytes << ',' << p.parts.size() << ','
+       << (p.parts.empty() ? 0u : p.parts[0].group) << ':';
     for (std::uint32_t r : p.reps) fp << r << ',';
-    char name[96];
-    std::snprintf(name, sizeof name, "pyrit_ring_k%u_e%u_w%u_n%u_L%u_%016llx", p.cols, p.rows, p.field.w,
-                  p.field.n, ks.lanes, static_cast<unsigned long long>(fnv1a(fp.str())));
+    char name[112];
+    if (ks.staged)
+        std::snprintf(name, sizeof name, "pyrit_ring_k%u_e%u_w%u_n%u_tma%ux%u_%016llx", p.cols, p.rows, p.field.w,
+                      p.field.n, ks.tile, ks.stages, static_cast<unsigned long long>(fnv1a(fp.str())));
+    else
+        std::snprintf(name, sizeof name, "pyrit_ring_k%u_e%u_w%u_n%u_L%u_%016llx", p.cols, p.rows, p.field.w,
+                      p.field.n, ks.lanes, static_cast<unsigned long long>(fnv1a(fp.str())));
     return name;
 }
 
+KernelShape staged_shape(const Program& p, std::uint32_t smem_limit) {
+    KernelShape ks;
+    ks.lanes = 1;
+    ks.min_blocks = 1;
+    if (p.parts.empty()) {
+        ks.staged = false;
+        return ks;
+    }
+    const std::uint32_t nin = p.cols * p.field.w;
+    const std::uint32_t G = p.parts[0].group;
+    const std::uint32_t groups = (p.cols + G - 1) / G;
+    const std::uint32_t R = static_cast<std::uint32_t>(p.parts.size());
+    // 8 warps per CTA (two per SM sub-partition keeps the 255-register cap);
+    // part r owns 256/R consumer threads, one 4-byte column word each, so a
+    // strip tile is 1024/R bytes; fall back to 4 warps if 2 stages do not fit
+    for (std::uint32_t threads : {256u, 128u}) {
+        if (threads % R) continue;
+        const std::uint32_t tile = 4 * (threads / R);
+        if (tile < 64) continue;
+        const std::uint64_t stage = std::uint64_t(nin) * tile;
+        for (std::uint32_t stages = 8; stages >= 2; --stages) {
+            const std::uint32_t bar = (8 * stages * (groups + 1) + 127) / 128 * 128;
+            if (bar + stages * stage > smem_limit) continue;
+            ks.staged = true;
+            ks.tile = tile;
+            ks.stages = stages;
+            ks.bar_bytes = bar;
+            ks.threads = threads;
+            ks.smem_bytes = static_cast<std::uint32_t>(bar + stages * stage);
+            return ks;
+        }
+    }
+    ks.staged = false;
+    return ks;
+}
+
+namespace {
+
+void emit_xor_list(std::ostringstream& o, const std::vector<std::uint32_t>& src,
+                   const std::string& prefix) {
+    if (src.empty()) o << "0u";
+    for (std::size_t s = 0; s < src.size(); ++s) o << (s ? " ^ " : "") << prefix << src[s];
+}
+
+std::string generate_staged(const Program& p, const KernelShape& ks) {
+    const std::uint32_t w = p.field.w, k = p.cols, G = p.parts[0].group;
+    const std::uint32_t nin = k * w, groups = (k + G - 1) / G, TILE = ks.tile, ST = ks.stages;
+    const std::uint32_t R = static_cast<std::uint32_t>(p.parts.size());
+    const std::uint32_t cols_per_part = TILE / 4, consumers = R * cols_per_part;
+    std::uint64_t part_xors = 0;
+    for (const Program& q : p.parts) part_xors += q.stats.xors;
+    std::ostringstream o;
+    o << "// generated by pyrit_b200 program compiler (TMA-staged): field w=" << w << " n=" << p.field.n << " p=0x"
+      << std::hex << p.field.modulus << std::dec << ", " << p.rows << "x" << k << " ring matrix in " << R
+      << " output part(s), " << part_xors << " XORs per column word (naive ring program " << p.stats.naive_xors
+      << ", reference schedule " << p.stats.ref_region_ops << " region ops); tile " << TILE << " B/strip x " << nin
+      << " strips, " << ST << " stages, " << groups << " barrier group(s)\n";
+    o << "typedef unsigned int u32; typedef unsigned long long u64; typedef unsigned char u8;\n";
+    o << "struct Args { const u8* in[" << k << "]; u8* out[" << p.rows << "]; u64 S; u64 off; u64 len; };\n";
+    o << R"(static __device__ __forceinline__ u32 smem_u32(const void* p) {
+  u32 r; asm("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(r) : "l"(p)); return r; }
+static __device__ __forceinline__ void mbar_init(u32 bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory"); }
+static __device__ __forceinline__ void mbar_expect_tx(u32 bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory"); }
+static __device__ __forceinline__ void mbar_arrive(u32 bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory"); }
+static __device__ __forceinline__ void mbar_wait(u32 bar, u32 parity) {
+  asm volatile("{\n .reg .pred P1;\n WAIT:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n @P1 bra DONE;\n bra WAIT;\n DONE:\n}"
+               :: "r"(bar), "r"(parity) : "memory"); }
+static __device__ __forceinline__ void bulk_g2s(u32 dst, const void* src, u32 bytes, u32 bar, u64 pol) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+               :: "r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory"); }
+static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
+  asm volatile("st.global.cs.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory"); }
+)";
+    const std::string name = kernel_name(p, ks);
+    o << "#define TILE " << TILE << "u\n#define NIN " << nin << "u\n#define STAGES " << ST << "u\n#define NG " << groups
+      << "u\n#define BAR_BYTES " << ks.bar_bytes << "u\n";
+    o << "#define FULL(st, g) (sbase + 8u * ((st) * NG + (g)))\n#define EMPTY(st) (sbase + 8u * (STAGES * NG + (st)))\n";
+    o << "extern \"C\" __global__ void __launch_bounds__(" << ks.threads << ", 1) " << name
+      << "(const __grid_constant__ Args a)\n{\n";
+    o << "  extern __shared__ __align__(1024) u8 sm[];\n";
+    o << "  const u32 sbase = smem_u32(sm);\n";
+    o << "  const u64 end = a.off + a.len;\n";
+    o << "  const u32 ntiles = (u32)((a.len + TILE - 1) / TILE);\n";
+    o << "  if (threadIdx.x == 0) {\n";
+    o << "    for (u32 i = 0; i < STAGES * NG; ++i) mbar_init(sbase + 8u * i, 1u);\n";
+    o << "    for (u32 s = 0; s < STAGES; ++s) mbar_init(EMPTY(s), " << consumers << "u);\n";
+    o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n  }\n";
+    o << "  __syncthreads();\n";
+    // producer duty (warp 0, interleaved with its consumer work so that all
+    // warps are consumers): the 32 lanes stream the stage's strip tiles with
+    // cp.async.bulk, STAGES-1 tiles ahead of the tile being consumed
+    o << "  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;\n";
+    o << "  u64 pol = 0;\n";
+    o << "  if (warp == 0) asm volatile(\"createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\" : \"=l\"(pol));\n";
+    o << "  auto produce = [&](u32 it2) {\n";
+    o << "    const u32 t2 = blockIdx.x + it2 * gridDim.x;\n";
+    o << "    if (t2 >= ntiles) return;\n";
+    o << "    const u32 st = it2 % STAGES, ph = (it2 / STAGES) & 1u;\n";
+    o << "    mbar_wait(EMPTY(st), ph ^ 1u);\n";
+    o << "    const u64 o = a.off + (u64)t2 * TILE;\n";
+    o << "    const u32 bytes = (u32)(end - o < TILE ? end - o : TILE);\n";
+    o << "    const u32 dst = sbase + BAR_BYTES + st * (NIN * TILE);\n";
+    o << "    if (lane == 0) {\n";
+    for (std::uint32_t g = 0; g < groups; ++g) {
+        const std::uint32_t j0 = g * G, j1 = std::min(k, j0 + G);
+        o << "      mbar_expect_tx(FULL(st, " << g << "u), bytes * " << (j1 - j0) * w << "u);\n";
+    }
+    o << "    }\n    __syncwarp();\n";
+    o << "#pragma unroll 1\n";
+    o << "    for (u32 idx = lane; idx < NIN; idx += 32u) {\n";
+    o << "      const u32 j = idx / " << w << "u, s = idx - j * " << w << "u;\n";
+    o << "      bulk_g2s(dst + idx * TILE, a.in[j] + s * a.S + o, bytes, FULL(st, j / " << G << "u), pol);\n";
+    o << "    }\n";
+    o << "  };\n";
+    o << "  if (warp == 0)\n    for (u32 i = 0; i + 1 < STAGES; ++i) produce(i);\n";
+    // consumers: part r computes output rows [row0_r, row0_r + rows_r) for column word `col`
+    o << "  const u32 ctid = threadIdx.x;\n";
+    o << "  const u32 part = ctid / " << cols_per_part << "u, col = ctid % " << cols_per_part << "u;\n";
+    o << "  const u64 S = a.S;\n";
+    // one tile loop per output part: each is its own register-allocation region
+    for (std::uint32_t r = 0; r < R; ++r) {
+        const Program& q = p.parts[r];
+        const std::uint32_t row0 = p.part_row0[r];
+        o << "  " << (r ? "else if" : "if") << " (part == " << r << "u) {\n";
+        o << "   u32 it = 0;\n";
+        o << "   for (u32 t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {\n";
+        if (r == 0) {
+            o << "    if (warp == 0) produce(it + STAGES - 1u);\n";
+        }
+        o << "    const u32 st = it % STAGES, ph = (it / STAGES) & 1u;\n";
+        o << "    const u64 o = a.off + (u64)t * TILE + 4u * col;\n";
+        o << "    const bool live = o < end;\n";
+        o << "    const u32* sp = reinterpret_cast<const u32*>(sm + BAR_BYTES + st * (NIN * TILE)) + col;\n";
+        // group g's shared-memory loads (after its mbarrier) then its XORs;
+        // shared memory is close, so no cross-group prefetch
+        std::vector<const Instr*> order;
+        for (std::size_t g = 0; g < q.group_loads.size(); ++g) {
+            for (const Instr& x : q.group_loads[g]) order.push_back(&x);
+            for (const Instr& x : q.group_compute[g]) order.push_back(&x);
+        }
+        for (const Instr& x : q.tail) order.push_back(&x);
+        std::size_t last_load = 0;
+        for (std::size_t i = 0; i < order.size(); ++i)
+            if (order[i]->op == Instr::Load) last_load = i;
+        std::vector<bool> waited(groups, false), out_ptr(q.rows, false);
+        for (std::size_t idx = 0; idx < order.size(); ++idx) {
+            const Instr& ins = *order[idx];
+            if (ins.op == Instr::Load) {
+                const std::uint32_t g = ins.sym / G;
+                if (!waited[g]) {
+                    o << "      mbar_wait(FULL(st, " << g << "u), ph);\n";
+                    waited[g] = true;
+                }
+                o << "      const u32 v" << ins.dst << " = sp[" << (ins.sym * w + ins.strip) * (TILE / 4) << "];\n";
+                if (idx == last_load) o << "      mbar_arrive(EMPTY(st));\n";
+            } else if (ins.op == Instr::Xor) {
+                o << "      const u32 v" << ins.dst << " = ";
+                emit_xor_list(o, ins.src, "v");
+                o << ";\n";
+            } else {
+                const std::uint32_t row = row0 + ins.sym;
+                if (!out_ptr[ins.sym]) {
+                    o << "      u8* q" << row << " = a.out[" << row << "] + o;\n";
+                    out_ptr[ins.sym] = true;
+                }
+                o << "      if (live) st_cs(q" << row;
+                if (ins.strip) o << " + " << ins.strip << "u * S";
+                o << ", ";
+                emit_xor_list(o, ins.src, "v");
+                o << ");\n";
+            }
+        }
+        o << "   }\n  }\n";
+    }
+    o << "}\n";
+    return o.str();
+}
+
+} // namespace
+
 std::string generate_cuda(const Program& p, const KernelShape& ks) {
+    if (ks.staged) return generate_staged(p, ks);
     const std::uint32_t L = ks.lanes == 0 ? 1 : ks.lanes;
     const bool bytes = ks.lanes == 0;
     const std::uint32_t V = bytes ? 1 : 4 * L; // bytes per thread per strip

@@ -48,8 +48,14 @@ struct Program {
     std::uint32_t group = 1;          // input fragments whose strips are live together
     std::vector<std::uint32_t> reps;  // rows x cols ring representatives (n-bit masks)
     std::vector<std::uint32_t> fold;  // fold[t - w] = x^t mod p
-    std::vector<Instr> code;
+    std::vector<Instr> code;          // canonical order (next group's loads before this group's XORs)
+    std::vector<std::vector<Instr>> group_loads, group_compute; // per fragment group
+    std::vector<Instr> tail;          // inverse transform + stores
     std::uint32_t nvars = 0;
+    // staged kernels split the outputs across consumer warp groups: part r
+    // computes rows [part_row0[r], part_row0[r] + parts[r].rows)
+    std::vector<Program> parts;
+    std::vector<std::uint32_t> part_row0;
     ProgramStats stats;
 };
 
@@ -57,6 +63,8 @@ struct CompileOptions {
     std::uint32_t group = 0;   // 0: choose automatically
     bool cse = true;           // greedy pair elimination
     bool dense = false;        // RingRep::Dense (plain phi1) instead of Sparse (schedule.hpp:78)
+    std::uint32_t parts = 0;   // output parts for the staged kernel: 0 auto, 1 = do not split
+    std::uint32_t part_group = 0; // fragment group of the parts: 0 auto
 };
 
 // compile_schedule analogue: matrix (rows x cols, GF(2^w) entries) -> program
@@ -69,14 +77,31 @@ void interpret_program(const Program& p, const std::uint8_t* const* in, std::uin
                        std::uint64_t strip, std::uint64_t off, std::uint64_t len);
 
 // CUDA C source of the fused kernel for this program.
-//   lanes: 32-bit words per thread per strip (1, 2 or 4); 0 = byte mode
+//
+// Direct mode: every thread streams its column word of every strip with
+//   vector LDG (lanes 32-bit words per thread per strip; 0 = byte mode),
+//   grid-stride over the window.
+// Staged mode (the sm_100a main path): a persistent CTA per SM; warp 0 is a
+//   TMA producer that moves [k*w strips x tile] tiles of the window into a
+//   ring of shared-memory stages with cp.async.bulk, completion tracked by
+//   one mbarrier per (stage, fragment group); the consumer warps evaluate the
+//   ring program reading their 4-byte column word of each strip from shared
+//   memory and store the folded outputs straight to HBM.  Needs 16-byte
+//   aligned pointers, strip pitch, window offset and length.
 struct KernelShape {
     std::uint32_t lanes = 1;
     std::uint32_t threads = 256;
     std::uint32_t min_blocks = 2;
+    bool staged = false;
+    std::uint32_t tile = 512;       // staged: bytes per strip per tile (= 4 x consumer threads)
+    std::uint32_t stages = 2;       // staged: shared-memory ring depth
+    std::uint32_t bar_bytes = 128;  // staged: mbarrier area at the start of shared memory
+    std::uint32_t smem_bytes = 0;   // staged: dynamic shared memory per CTA
 };
 std::string kernel_name(const Program& p, const KernelShape& ks);
 std::string generate_cuda(const Program& p, const KernelShape& ks);
+// Staged-mode shape for this program, or staged=false if the tiles do not fit.
+KernelShape staged_shape(const Program& p, std::uint32_t smem_limit);
 
 std::uint64_t fnv1a(const std::string& s);
 

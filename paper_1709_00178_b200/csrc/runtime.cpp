@@ -30,6 +30,7 @@ struct Driver {
                              CUstream, void**, void**) = nullptr;
     CUresult (*occupancy)(int*, CUfunction, int, size_t) = nullptr;
     CUresult (*getErrorString)(CUresult, const char**) = nullptr;
+    CUresult (*funcSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
 };
 
 template <class F>
@@ -50,6 +51,7 @@ const Driver& driver() {
         resolve("cuLaunchKernel", d.launchKernel);
         resolve("cuOccupancyMaxActiveBlocksPerMultiprocessor", d.occupancy);
         resolve("cuGetErrorString", d.getErrorString);
+        resolve("cuFuncSetAttribute", d.funcSetAttribute);
     });
     return d;
 }
@@ -134,7 +136,11 @@ LoadedKernel load_kernel(const Program& p, const KernelShape& ks, int device) {
     check_cu(driver().moduleLoadData(&mod, cubin.data()), "cuModuleLoadData");
     LoadedKernel k;
     check_cu(driver().moduleGetFunction(&k.fn, mod, name.c_str()), "cuModuleGetFunction");
-    check_cu(driver().occupancy(&k.blocks_per_sm, k.fn, static_cast<int>(ks.threads), 0), "occupancy");
+    if (ks.smem_bytes > 48 * 1024)
+        check_cu(driver().funcSetAttribute(k.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                                           static_cast<int>(ks.smem_bytes)),
+                 "cuFuncSetAttribute(max dynamic smem)");
+    check_cu(driver().occupancy(&k.blocks_per_sm, k.fn, static_cast<int>(ks.threads), ks.smem_bytes), "occupancy");
     if (k.blocks_per_sm < 1) k.blocks_per_sm = 1;
     check_cuda(cudaDeviceGetAttribute(&k.sms, cudaDevAttrMultiProcessorCount, device), "sm count");
     g_modules[key] = mod;
@@ -188,10 +194,79 @@ KernelShape shape_for(std::uint32_t lanes) {
     return ks;
 }
 
+namespace {
+
+std::atomic<int> g_mode{-1};
+
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+}
+
+// staged shape for p (optionally overridden by PYRIT_B200_TILE / _STAGES for tuning)
+KernelShape staged_for(const Program& p) {
+    KernelShape ks = staged_shape(p, 227 * 1024);
+    const int tile = env_int("PYRIT_B200_TILE", 0), stages = env_int("PYRIT_B200_STAGES", 0);
+    if (ks.staged && (tile || stages)) {
+        if (tile == 256 || tile == 512 || tile == 1024) ks.tile = static_cast<std::uint32_t>(tile);
+        if (stages >= 1 && stages <= 8) ks.stages = static_cast<std::uint32_t>(stages);
+        ks.threads = 32 + ks.tile / 4;
+        const std::uint32_t groups = (p.cols + p.group - 1) / p.group;
+        ks.bar_bytes = (8 * ks.stages * (groups + 1) + 127) / 128 * 128;
+        ks.smem_bytes = ks.bar_bytes + ks.stages * p.cols * p.field.w * ks.tile;
+        if (ks.smem_bytes > 227 * 1024) ks.staged = false;
+    }
+    return ks;
+}
+
+} // namespace
+
+int kernel_mode() {
+    int m = g_mode.load();
+    if (m < 0) {
+        m = env_int("PYRIT_B200_MODE", 0);
+        if (m < 0 || m > 2) m = 0;
+        g_mode = m;
+    }
+    return m;
+}
+
+void set_kernel_mode(int mode) {
+    if (mode < 0 || mode > 2) raise(Errc::InvalidArgument, "mode must be 0 (auto), 1 (direct) or 2 (staged)");
+    g_mode = mode;
+}
+
+KernelShape choose_shape(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
+                         std::uint64_t strip, std::uint64_t off, std::uint64_t len) {
+    const auto all_aligned = [&](std::uint64_t v) {
+        bool ok = strip % v == 0 && off % v == 0 && len % v == 0;
+        for (std::uint32_t j = 0; ok && j < p.cols; ++j) ok = aligned(in[j], v);
+        for (std::uint32_t i = 0; ok && i < p.rows; ++i) ok = aligned(out[i], v);
+        return ok;
+    };
+    if (kernel_mode() != 1 && all_aligned(16)) {
+        const KernelShape ks = staged_for(p);
+        if (ks.staged) return ks;
+    }
+    // direct mode: widest vector the alignment of every pointer, the strip
+    // pitch and the window allows; byte mode otherwise
+    std::uint32_t lanes = 0;
+    for (std::uint32_t l = preferred_lanes(); l >= 1; l /= 2)
+        if (all_aligned(4ull * l)) {
+            lanes = l;
+            break;
+        }
+    return shape_for(lanes);
+}
+
 std::string prepare_program(const Program& p, std::uint32_t lanes) {
     int dev = 0;
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
-    const KernelShape ks = shape_for(lanes);
+    KernelShape ks = shape_for(lanes);
+    if (kernel_mode() != 1) {
+        const KernelShape st = staged_for(p);
+        if (st.staged) ks = st;
+    }
     load_kernel(p, ks, dev);
     return kernel_name(p, ks);
 }
@@ -201,42 +276,36 @@ LaunchInfo launch_program(const Program& p, const std::uint8_t* const* in, std::
     LaunchInfo info;
     if (off + len > strip) raise(Errc::BufferShape, "column window out of range");
     if (len == 0) return info;
-    // widest vector the alignment of every pointer, the strip pitch and the
-    // window allows; byte mode otherwise
-    std::uint32_t lanes = 0;
-    for (std::uint32_t l = preferred_lanes(); l >= 1; l /= 2) {
-        const std::uint64_t v = 4ull * l;
-        bool ok = strip % v == 0 && off % v == 0 && len % v == 0;
-        for (std::uint32_t j = 0; ok && j < p.cols; ++j) ok = aligned(in[j], v);
-        for (std::uint32_t i = 0; ok && i < p.rows; ++i) ok = aligned(out[i], v);
-        if (ok) {
-            lanes = l;
-            break;
-        }
-    }
     int dev = 0;
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
-    const KernelShape ks = shape_for(lanes);
+    const KernelShape ks = choose_shape(p, in, out, strip, off, len);
     const LoadedKernel k = load_kernel(p, ks, dev);
-    const std::uint64_t vbytes = lanes ? 4ull * lanes : 1ull;
-    const std::uint64_t nwords = len / vbytes;
     std::vector<std::uint64_t> args(std::size_t(p.cols) + p.rows + 3);
     for (std::uint32_t j = 0; j < p.cols; ++j) args[j] = reinterpret_cast<std::uint64_t>(in[j]);
     for (std::uint32_t i = 0; i < p.rows; ++i) args[p.cols + i] = reinterpret_cast<std::uint64_t>(out[i]);
     args[p.cols + p.rows] = strip;
     args[p.cols + p.rows + 1] = off;
-    args[p.cols + p.rows + 2] = nwords;
-    const std::uint64_t want = (nwords + ks.threads - 1) / ks.threads;
+    std::uint64_t want;
+    if (ks.staged) {
+        args[p.cols + p.rows + 2] = len; // bytes; tiles of ks.tile bytes per strip
+        want = (len + ks.tile - 1) / ks.tile;
+    } else {
+        const std::uint64_t vbytes = ks.lanes ? 4ull * ks.lanes : 1ull;
+        const std::uint64_t nwords = len / vbytes;
+        args[p.cols + p.rows + 2] = nwords;
+        want = (nwords + ks.threads - 1) / ks.threads;
+    }
     const std::uint64_t cap = std::uint64_t(k.sms) * std::uint64_t(k.blocks_per_sm);
     const unsigned blocks = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min(want, cap)));
     void* params[] = {args.data()};
-    check_cu(driver().launchKernel(k.fn, blocks, 1, 1, ks.threads, 1, 1, 0, reinterpret_cast<CUstream>(stream),
-                                   params, nullptr),
+    check_cu(driver().launchKernel(k.fn, blocks, 1, 1, ks.threads, 1, 1, ks.staged ? ks.smem_bytes : 0,
+                                   reinterpret_cast<CUstream>(stream), params, nullptr),
              "cuLaunchKernel");
     ++g_launches;
-    info.lanes = lanes;
+    info.lanes = ks.lanes;
     info.threads = ks.threads;
     info.blocks = blocks;
+    info.staged = ks.staged;
     info.kernel = kernel_name(p, ks);
     return info;
 }

@@ -26,6 +26,7 @@ void check_cuda(cudaError_t e, const char* what);
 
 struct LaunchInfo {
     std::uint32_t lanes = 1, threads = 0, blocks = 0;
+    bool staged = false;
     std::string kernel;
 };
 
@@ -50,5 +51,12 @@ std::uint64_t jit_compiles(); // number of NVRTC compilations performed so far
 std::uint64_t kernel_launches(); // number of generated-kernel launches so far
 
 KernelShape shape_for(std::uint32_t lanes);
+
+// 0 = auto (TMA-staged whenever alignment allows), 1 = direct LDG only, 2 = staged
+int kernel_mode();
+void set_kernel_mode(int mode);
+// the kernel shape a launch with these arguments uses
+KernelShape choose_shape(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
+                         std::uint64_t strip, std::uint64_t off, std::uint64_t len);
 
 } // namespace pyrit_b200
