@@ -260,6 +260,7 @@ def main(argv=None):
         e1.record(stream)
         torch.cuda.synchronize(dev)
     launches = lib.pyrit_kernel_launches() - launches0
+    launch = P.Plan.last_launch()
     ms = e0.elapsed_time(e1) / args.steps
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -303,7 +304,8 @@ def main(argv=None):
                        "p": hex(wl.fld.modulus), "fragment_bytes": wl.frag, "strip_bytes": wl.strip,
                        "shard_strip_bytes": Ls, "erased": list(wl.erased), "parallelism": f"byte-offset shards x{world}",
                        "l2": "inputs larger than L2" if nsets == 1 else f"{nsets} rotating buffer sets > L2",
-                       "kernel": plan.source(1)[0], "xors_per_column_word": st["xors"],
+                       "kernel": launch["kernel"], "grid": [launch["blocks"], launch["threads"]],
+                       "xors_per_column_word": st["xors"],
                        "reference_region_ops": st["ref_region_ops"]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,

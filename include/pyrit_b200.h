@@ -161,6 +161,8 @@ int pyrit_set_lanes(uint32_t lanes); /* 32-bit words per thread per strip: 1, 2 
  * 2 = staged whenever possible */
 int pyrit_set_kernel_mode(int mode);
 int pyrit_set_kernel_dir(const char* dir);
+/* name and geometry of this thread's most recent generated-kernel launch */
+int pyrit_cu_last_launch(char* kernel, size_t cap, uint32_t* blocks, uint32_t* threads);
 uint64_t pyrit_jit_compiles(void);
 uint64_t pyrit_kernel_launches(void);
 

@@ -218,6 +218,14 @@ class Plan:
         L.check(_clib().pyrit_cu_apply(self._h, _ptr_array(list(in_ptrs)), _ptr_array(list(out_ptrs)), strip, off,
                                       length, stream))
 
+    @staticmethod
+    def last_launch() -> dict:
+        """Kernel name / grid of this thread's most recent launch through the C ABI."""
+        name = C.create_string_buffer(128)
+        blocks, threads = C.c_uint32(), C.c_uint32()
+        L.check(_clib().pyrit_cu_last_launch(name, 128, C.byref(blocks), C.byref(threads)))
+        return {"kernel": name.value.decode(), "blocks": blocks.value, "threads": threads.value}
+
     def prepare(self) -> None:
         L.check(_clib().pyrit_cu_prepare(self._h))
 

@@ -51,7 +51,7 @@ EXPORTS = (
     "pyrit_plan_reps", "pyrit_plan_source", "pyrit_plan_interpret", "pyrit_plan_destroy", "pyrit_cu_apply",
     "pyrit_cu_prepare", "pyrit_cu_encode", "pyrit_cu_decode", "pyrit_encode_host", "pyrit_decode_host",
     "pyrit_set_host_chunk", "pyrit_cu_fill", "pyrit_cu_digest", "pyrit_set_lanes", "pyrit_set_kernel_mode", "pyrit_set_kernel_dir",
-    "pyrit_jit_compiles", "pyrit_kernel_launches",
+    "pyrit_cu_last_launch", "pyrit_jit_compiles", "pyrit_kernel_launches",
 )
 
 
@@ -90,6 +90,7 @@ def load():
     lib.pyrit_set_lanes.argtypes = [u32]
     lib.pyrit_set_kernel_dir.argtypes = [C.c_char_p]
     lib.pyrit_set_kernel_mode.argtypes = [i32]
+    lib.pyrit_cu_last_launch.argtypes = [vp, C.c_size_t, vp, vp]
     lib.pyrit_jit_compiles.restype = u64
     lib.pyrit_kernel_launches.restype = u64
     lib.pyrit_field_named.argtypes = [C.c_char_p, P(pyrit_field)]

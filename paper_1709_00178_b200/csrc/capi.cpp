@@ -456,6 +456,19 @@ int pyrit_set_kernel_dir(const char* dir) {
     return guarded([&] { set_kernel_dir(dir ? dir : ""); });
 }
 
+int pyrit_cu_last_launch(char* kernel, size_t cap, uint32_t* blocks, uint32_t* threads) {
+    return guarded([&] {
+        const LaunchInfo li = last_launch();
+        if (kernel && cap) {
+            const size_t n = std::min(cap - 1, li.kernel.size());
+            std::memcpy(kernel, li.kernel.data(), n);
+            kernel[n] = 0;
+        }
+        if (blocks) *blocks = li.blocks;
+        if (threads) *threads = li.threads;
+    });
+}
+
 uint64_t pyrit_jit_compiles(void) { return jit_compiles(); }
 uint64_t pyrit_kernel_launches(void) { return kernel_launches(); }
 

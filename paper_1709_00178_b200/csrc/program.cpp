@@ -321,12 +321,13 @@ std::string kernel_name(const Program& p, const KernelShape& ks) {
     fp << p.field.w << ',' << p.field.n << ',' << p.field.modulus << ',' << int(p.kind) << ',' << p.rows << ','
        << p.cols << ',' << p.group << ',' << ks.lanes << ',' << ks.threads << ',' << ks.min_blocks << ','
        << ks.staged << ',' << ks.tile << ',' << ks.stages << ',' << ks.bar_bytes << ',' << p.parts.size() << ','
-       << (p.parts.empty() ? 0u : p.parts[0].group) << ':';
+       << (p.parts.empty() ? 0u : p.parts[0].group) << ',' << ks.copy << ':';
     for (std::uint32_t r : p.reps) fp << r << ',';
     char name[112];
     if (ks.staged)
-        std::snprintf(name, sizeof name, "pyrit_ring_k%u_e%u_w%u_n%u_tma%ux%u_%016llx", p.cols, p.rows, p.field.w,
-                      p.field.n, ks.tile, ks.stages, static_cast<unsigned long long>(fnv1a(fp.str())));
+        std::snprintf(name, sizeof name, "pyrit_ring_k%u_e%u_w%u_n%u_%s%ux%u_%016llx", p.cols, p.rows, p.field.w,
+                      p.field.n, ks.copy ? "cpa" : "tma", ks.tile, ks.stages,
+                      static_cast<unsigned long long>(fnv1a(fp.str())));
     else
         std::snprintf(name, sizeof name, "pyrit_ring_k%u_e%u_w%u_n%u_L%u_%016llx", p.cols, p.rows, p.field.w,
                       p.field.n, ks.lanes, static_cast<unsigned long long>(fnv1a(fp.str())));
@@ -406,6 +407,10 @@ static __device__ __forceinline__ void mbar_wait(u32 bar, u32 parity) {
 static __device__ __forceinline__ void bulk_g2s(u32 dst, const void* src, u32 bytes, u32 bar, u64 pol) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
                :: "r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory"); }
+static __device__ __forceinline__ void cpa16(u32 dst, const void* src, u32 n) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(dst), "l"(src), "r"(n) : "memory"); }
+static __device__ __forceinline__ void cpa_arrive(u32 bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(bar) : "memory"); }
 static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
   asm volatile("st.global.cs.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory"); }
 )";
@@ -420,7 +425,8 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
     o << "  const u64 end = a.off + a.len;\n";
     o << "  const u32 ntiles = (u32)((a.len + TILE - 1) / TILE);\n";
     o << "  if (threadIdx.x == 0) {\n";
-    o << "    for (u32 i = 0; i < STAGES * NG; ++i) mbar_init(sbase + 8u * i, 1u);\n";
+    o << "    for (u32 i = 0; i < STAGES * NG; ++i) mbar_init(sbase + 8u * i, " << (ks.copy ? consumers : 1u)
+      << "u);\n";
     o << "    for (u32 s = 0; s < STAGES; ++s) mbar_init(EMPTY(s), " << consumers << "u);\n";
     o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n  }\n";
     o << "  __syncthreads();\n";
@@ -430,27 +436,55 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
     o << "  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;\n";
     o << "  u64 pol = 0;\n";
     o << "  if (warp == 0) asm volatile(\"createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\" : \"=l\"(pol));\n";
+    if (ks.copy == 0) {
     o << "  auto produce = [&](u32 it2) {\n";
-    o << "    const u32 t2 = blockIdx.x + it2 * gridDim.x;\n";
-    o << "    if (t2 >= ntiles) return;\n";
-    o << "    const u32 st = it2 % STAGES, ph = (it2 / STAGES) & 1u;\n";
-    o << "    mbar_wait(EMPTY(st), ph ^ 1u);\n";
-    o << "    const u64 o = a.off + (u64)t2 * TILE;\n";
-    o << "    const u32 bytes = (u32)(end - o < TILE ? end - o : TILE);\n";
-    o << "    const u32 dst = sbase + BAR_BYTES + st * (NIN * TILE);\n";
-    o << "    if (lane == 0) {\n";
-    for (std::uint32_t g = 0; g < groups; ++g) {
-        const std::uint32_t j0 = g * G, j1 = std::min(k, j0 + G);
+        o << "    const u32 t2 = blockIdx.x + it2 * gridDim.x;\n";
+        o << "    if (t2 >= ntiles) return;\n";
+        o << "    const u32 st = it2 % STAGES, ph = (it2 / STAGES) & 1u;\n";
+        o << "    mbar_wait(EMPTY(st), ph ^ 1u);\n";
+        o << "    const u64 o = a.off + (u64)t2 * TILE;\n";
+        o << "    const u32 bytes = (u32)(end - o < TILE ? end - o : TILE);\n";
+        o << "    const u32 dst = sbase + BAR_BYTES + st * (NIN * TILE);\n";
+        o << "    if (lane == 0) {\n";
+        for (std::uint32_t g = 0; g < groups; ++g) {
+            const std::uint32_t j0 = g * G, j1 = std::min(k, j0 + G);
         o << "      mbar_expect_tx(FULL(st, " << g << "u), bytes * " << (j1 - j0) * w << "u);\n";
     }
-    o << "    }\n    __syncwarp();\n";
-    o << "#pragma unroll 1\n";
-    o << "    for (u32 idx = lane; idx < NIN; idx += 32u) {\n";
-    o << "      const u32 j = idx / " << w << "u, s = idx - j * " << w << "u;\n";
-    o << "      bulk_g2s(dst + idx * TILE, a.in[j] + s * a.S + o, bytes, FULL(st, j / " << G << "u), pol);\n";
-    o << "    }\n";
-    o << "  };\n";
-    o << "  if (warp == 0)\n    for (u32 i = 0; i + 1 < STAGES; ++i) produce(i);\n";
+        o << "    }\n    __syncwarp();\n";
+        o << "#pragma unroll 1\n";
+        o << "    for (u32 idx = lane; idx < NIN; idx += 32u) {\n";
+        o << "      const u32 j = idx / " << w << "u, s = idx - j * " << w << "u;\n";
+        o << "      bulk_g2s(dst + idx * TILE, a.in[j] + s * a.S + o, bytes, FULL(st, j / " << G << "u), pol);\n";
+        o << "    }\n";
+        o << "  };\n";
+        o << "  if (warp == 0)\n    for (u32 i = 0; i + 1 < STAGES; ++i) produce(i);\n";
+    } else {
+        // every thread copies 16-byte chunks of the stage (strip tiles are
+        // TILE/16 consecutive chunks: coalesced), then arrives on the
+        // group's FULL barrier when its copies land (cp.async.mbarrier.arrive)
+        const std::uint32_t cps = TILE / 16; // chunks per strip tile
+        o << "  auto produce = [&](u32 it2) {\n";
+        o << "    const u32 t2 = blockIdx.x + it2 * gridDim.x;\n";
+        o << "    if (t2 >= ntiles) return;\n";
+        o << "    const u32 st = it2 % STAGES, ph = (it2 / STAGES) & 1u;\n";
+        o << "    mbar_wait(EMPTY(st), ph ^ 1u);\n";
+        o << "    const u64 o = a.off + (u64)t2 * TILE;\n";
+        o << "    const u32 dst = sbase + BAR_BYTES + st * (NIN * TILE);\n";
+        for (std::uint32_t g = 0; g < groups; ++g) {
+            const std::uint32_t j0 = g * G, j1 = std::min(k, j0 + G);
+            const std::uint32_t nchunks = (j1 - j0) * w * cps;
+            o << "#pragma unroll 4\n";
+            o << "    for (u32 c = threadIdx.x; c < " << nchunks << "u; c += " << consumers << "u) {\n";
+            o << "      const u32 sl = c / " << cps << "u, q = c - sl * " << cps << "u;\n";
+            o << "      const u32 idx = " << j0 * w << "u + sl, j = idx / " << w << "u, s = idx - j * " << w << "u;\n";
+            o << "      const u64 off = o + 16u * q;\n";
+            o << "      cpa16(dst + idx * TILE + 16u * q, a.in[j] + s * a.S + (off < end ? off : a.off), off < end ? 16u : 0u);\n";
+            o << "    }\n";
+            o << "    cpa_arrive(FULL(st, " << g << "u));\n";
+        }
+        o << "  };\n";
+        o << "  for (u32 i = 0; i + 1 < STAGES; ++i) produce(i);\n";
+    }
     // consumers: part r computes output rows [row0_r, row0_r + rows_r) for column word `col`
     o << "  const u32 ctid = threadIdx.x;\n";
     o << "  const u32 part = ctid / " << cols_per_part << "u, col = ctid % " << cols_per_part << "u;\n";
@@ -462,9 +496,8 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
         o << "  " << (r ? "else if" : "if") << " (part == " << r << "u) {\n";
         o << "   u32 it = 0;\n";
         o << "   for (u32 t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {\n";
-        if (r == 0) {
-            o << "    if (warp == 0) produce(it + STAGES - 1u);\n";
-        }
+        if (ks.copy) o << "    produce(it + STAGES - 1u);\n";
+        else if (r == 0) o << "    if (warp == 0) produce(it + STAGES - 1u);\n";
         o << "    const u32 st = it % STAGES, ph = (it / STAGES) & 1u;\n";
         o << "    const u64 o = a.off + (u64)t * TILE + 4u * col;\n";
         o << "    const bool live = o < end;\n";

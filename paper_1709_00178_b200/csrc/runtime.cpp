@@ -197,6 +197,7 @@ KernelShape shape_for(std::uint32_t lanes) {
 namespace {
 
 std::atomic<int> g_mode{-1};
+thread_local LaunchInfo g_last;
 
 int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
@@ -206,6 +207,7 @@ int env_int(const char* name, int dflt) {
 // staged shape for p (optionally overridden by PYRIT_B200_TILE / _STAGES for tuning)
 KernelShape staged_for(const Program& p) {
     KernelShape ks = staged_shape(p, 227 * 1024);
+    ks.copy = env_int("PYRIT_B200_COPY", static_cast<int>(ks.copy)) ? 1u : 0u;
     const int tile = env_int("PYRIT_B200_TILE", 0), stages = env_int("PYRIT_B200_STAGES", 0);
     if (ks.staged && (tile || stages)) {
         if (tile == 256 || tile == 512 || tile == 1024) ks.tile = static_cast<std::uint32_t>(tile);
@@ -307,7 +309,10 @@ LaunchInfo launch_program(const Program& p, const std::uint8_t* const* in, std::
     info.blocks = blocks;
     info.staged = ks.staged;
     info.kernel = kernel_name(p, ks);
+    g_last = info;
     return info;
 }
+
+LaunchInfo last_launch() { return g_last; }
 
 } // namespace pyrit_b200

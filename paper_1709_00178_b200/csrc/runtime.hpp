@@ -47,6 +47,7 @@ void set_preferred_lanes(std::uint32_t lanes);
 void set_kernel_dir(const std::string& dir);
 std::string kernel_dir();
 
+LaunchInfo last_launch(); // this thread's most recent launch_program
 std::uint64_t jit_compiles(); // number of NVRTC compilations performed so far
 std::uint64_t kernel_launches(); // number of generated-kernel launches so far
 
