@@ -120,6 +120,7 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
     const std::uint32_t w = f.w, n = f.n, k = m.cols, e = m.rows;
     p.group = opt.group ? opt.group : std::max<std::uint32_t>(1, 24 / w);
     p.group = std::min(p.group, k);
+    p.cse = opt.cse;
     p.fold = fold_table(f);
     p.reps.resize(std::size_t(e) * k);
     for (std::size_t i = 0; i < p.reps.size(); ++i) {
@@ -280,6 +281,7 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
             CompileOptions o2 = opt;
             o2.parts = 1;
             o2.group = pg;
+            if (const char* env = std::getenv("PYRIT_B200_PART_CSE")) o2.cse = std::atoi(env) != 0;
             p.parts.push_back(compile_program(f, kind, sub, o2));
             p.part_row0.push_back(row0);
             row0 += nrows;
@@ -321,7 +323,9 @@ std::string kernel_name(const Program& p, const KernelShape& ks) {
     fp << p.field.w << ',' << p.field.n << ',' << p.field.modulus << ',' << int(p.kind) << ',' << p.rows << ','
        << p.cols << ',' << p.group << ',' << ks.lanes << ',' << ks.threads << ',' << ks.min_blocks << ','
        << ks.staged << ',' << ks.tile << ',' << ks.stages << ',' << ks.bar_bytes << ',' << p.parts.size() << ','
-       << (p.parts.empty() ? 0u : p.parts[0].group) << ',' << ks.copy << ':';
+       << (p.parts.empty() ? 0u : p.parts[0].group) << ',' << ks.copy << ',' << p.cse << ',';
+    for (const Program& q : p.parts) fp << q.rows << '/' << q.cse << '/' << q.stats.xors << ',';
+    fp << ':';
     for (std::uint32_t r : p.reps) fp << r << ',';
     char name[112];
     if (ks.staged)
@@ -342,29 +346,34 @@ KernelShape staged_shape(const Program& p, std::uint32_t smem_limit) {
         ks.staged = false;
         return ks;
     }
-    const std::uint32_t nin = p.cols * p.field.w;
-    const std::uint32_t G = p.parts[0].group;
-    const std::uint32_t groups = (p.cols + G - 1) / G;
+    const std::uint32_t w = p.field.w, k = p.cols, G = p.parts[0].group;
     const std::uint32_t R = static_cast<std::uint32_t>(p.parts.size());
-    // 8 warps per CTA (two per SM sub-partition keeps the 255-register cap);
-    // part r owns 256/R consumer threads, one 4-byte column word each, so a
-    // strip tile is 1024/R bytes; fall back to 4 warps if 2 stages do not fit
+    // 8 warps per CTA (two per SM sub-partition keeps ptxas's 255-register
+    // cap); part r owns 256/R consumer threads, one 4-byte column word each,
+    // so a strip tile is 1024/R bytes.  The shared-memory ring holds one
+    // fragment group of one tile per slot.
     for (std::uint32_t threads : {256u, 128u}) {
         if (threads % R) continue;
         const std::uint32_t tile = 4 * (threads / R);
         if (tile < 64) continue;
-        const std::uint64_t stage = std::uint64_t(nin) * tile;
-        for (std::uint32_t stages = 8; stages >= 2; --stages) {
-            const std::uint32_t bar = (8 * stages * (groups + 1) + 127) / 128 * 128;
-            if (bar + stages * stage > smem_limit) continue;
-            ks.staged = true;
-            ks.tile = tile;
-            ks.stages = stages;
-            ks.bar_bytes = bar;
-            ks.threads = threads;
-            ks.smem_bytes = static_cast<std::uint32_t>(bar + stages * stage);
-            return ks;
+        const std::uint64_t slot = std::uint64_t(G) * w * tile;
+        std::uint32_t slots = 0, bar = 0;
+        for (std::uint32_t n = 32; n >= 2; --n) {
+            bar = (16 * n + 127) / 128 * 128;
+            if (bar + n * slot <= smem_limit) {
+                slots = n;
+                break;
+            }
         }
+        if (slots < 2) continue;
+        ks.staged = true;
+        ks.tile = tile;
+        ks.stages = slots;
+        ks.bar_bytes = bar;
+        ks.threads = threads;
+        ks.smem_bytes = static_cast<std::uint32_t>(bar + slots * slot);
+        (void)k;
+        return ks;
     }
     ks.staged = false;
     return ks;
@@ -372,25 +381,26 @@ KernelShape staged_shape(const Program& p, std::uint32_t smem_limit) {
 
 namespace {
 
-void emit_xor_list(std::ostringstream& o, const std::vector<std::uint32_t>& src,
-                   const std::string& prefix) {
+void emit_xor_list(std::ostringstream& o, const std::vector<std::uint32_t>& src, const std::string& prefix) {
     if (src.empty()) o << "0u";
     for (std::size_t s = 0; s < src.size(); ++s) o << (s ? " ^ " : "") << prefix << src[s];
 }
 
 std::string generate_staged(const Program& p, const KernelShape& ks) {
     const std::uint32_t w = p.field.w, k = p.cols, G = p.parts[0].group;
-    const std::uint32_t nin = k * w, groups = (k + G - 1) / G, TILE = ks.tile, ST = ks.stages;
+    const std::uint32_t groups = (k + G - 1) / G, TILE = ks.tile, NSLOT = ks.stages, T = ks.threads;
     const std::uint32_t R = static_cast<std::uint32_t>(p.parts.size());
-    const std::uint32_t cols_per_part = TILE / 4, consumers = R * cols_per_part;
+    const std::uint32_t cols_per_part = T / R;
+    const std::uint32_t slot_bytes = G * w * TILE;
     std::uint64_t part_xors = 0;
     for (const Program& q : p.parts) part_xors += q.stats.xors;
     std::ostringstream o;
-    o << "// generated by pyrit_b200 program compiler (TMA-staged): field w=" << w << " n=" << p.field.n << " p=0x"
-      << std::hex << p.field.modulus << std::dec << ", " << p.rows << "x" << k << " ring matrix in " << R
-      << " output part(s), " << part_xors << " XORs per column word (naive ring program " << p.stats.naive_xors
-      << ", reference schedule " << p.stats.ref_region_ops << " region ops); tile " << TILE << " B/strip x " << nin
-      << " strips, " << ST << " stages, " << groups << " barrier group(s)\n";
+    o << "// generated by pyrit_b200 program compiler (staged, " << (ks.copy ? "cp.async" : "TMA cp.async.bulk")
+      << "): field w=" << w << " n=" << p.field.n << " p=0x" << std::hex << p.field.modulus << std::dec << ", "
+      << p.rows << "x" << k << " ring matrix in " << R << " output part(s), " << part_xors
+      << " XORs per column word (naive ring program " << p.stats.naive_xors << ", reference schedule "
+      << p.stats.ref_region_ops << " region ops); " << T << " threads, tile " << TILE << " B/strip, ring of "
+      << NSLOT << " slots x " << G << " fragment(s)\n";
     o << "typedef unsigned int u32; typedef unsigned long long u64; typedef unsigned char u8;\n";
     o << "struct Args { const u8* in[" << k << "]; u8* out[" << p.rows << "]; u64 S; u64 off; u64 len; };\n";
     o << R"(static __device__ __forceinline__ u32 smem_u32(const void* p) {
@@ -415,79 +425,63 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
   asm volatile("st.global.cs.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory"); }
 )";
     const std::string name = kernel_name(p, ks);
-    o << "#define TILE " << TILE << "u\n#define NIN " << nin << "u\n#define STAGES " << ST << "u\n#define NG " << groups
-      << "u\n#define BAR_BYTES " << ks.bar_bytes << "u\n";
-    o << "#define FULL(st, g) (sbase + 8u * ((st) * NG + (g)))\n#define EMPTY(st) (sbase + 8u * (STAGES * NG + (st)))\n";
-    o << "extern \"C\" __global__ void __launch_bounds__(" << ks.threads << ", 1) " << name
+    o << "#define TILE " << TILE << "u\n#define NSLOT " << NSLOT << "u\n#define SLOT_BYTES " << slot_bytes
+      << "u\n#define NG " << groups << "u\n#define BAR_BYTES " << ks.bar_bytes << "u\n";
+    o << "#define FULL(s) (sbase + 8u * (s))\n#define EMPTY(s) (sbase + 8u * (NSLOT + (s)))\n";
+    o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", 1) " << name
       << "(const __grid_constant__ Args a)\n{\n";
     o << "  extern __shared__ __align__(1024) u8 sm[];\n";
     o << "  const u32 sbase = smem_u32(sm);\n";
     o << "  const u64 end = a.off + a.len;\n";
     o << "  const u32 ntiles = (u32)((a.len + TILE - 1) / TILE);\n";
     o << "  if (threadIdx.x == 0) {\n";
-    o << "    for (u32 i = 0; i < STAGES * NG; ++i) mbar_init(sbase + 8u * i, " << (ks.copy ? consumers : 1u)
-      << "u);\n";
-    o << "    for (u32 s = 0; s < STAGES; ++s) mbar_init(EMPTY(s), " << consumers << "u);\n";
+    o << "    for (u32 s = 0; s < NSLOT; ++s) { mbar_init(FULL(s), " << (ks.copy ? T : 1u) << "u); mbar_init(EMPTY(s), "
+      << T << "u); }\n";
     o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n  }\n";
     o << "  __syncthreads();\n";
-    // producer duty (warp 0, interleaved with its consumer work so that all
-    // warps are consumers): the 32 lanes stream the stage's strip tiles with
-    // cp.async.bulk, STAGES-1 tiles ahead of the tile being consumed
     o << "  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;\n";
+    // produce(u2): fill the slot of pipeline unit u2 = (tile it2, fragment group g2)
     o << "  u64 pol = 0;\n";
-    o << "  if (warp == 0) asm volatile(\"createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\" : \"=l\"(pol));\n";
-    if (ks.copy == 0) {
-    o << "  auto produce = [&](u32 it2) {\n";
-        o << "    const u32 t2 = blockIdx.x + it2 * gridDim.x;\n";
-        o << "    if (t2 >= ntiles) return;\n";
-        o << "    const u32 st = it2 % STAGES, ph = (it2 / STAGES) & 1u;\n";
-        o << "    mbar_wait(EMPTY(st), ph ^ 1u);\n";
-        o << "    const u64 o = a.off + (u64)t2 * TILE;\n";
-        o << "    const u32 bytes = (u32)(end - o < TILE ? end - o : TILE);\n";
-        o << "    const u32 dst = sbase + BAR_BYTES + st * (NIN * TILE);\n";
-        o << "    if (lane == 0) {\n";
-        for (std::uint32_t g = 0; g < groups; ++g) {
-            const std::uint32_t j0 = g * G, j1 = std::min(k, j0 + G);
-        o << "      mbar_expect_tx(FULL(st, " << g << "u), bytes * " << (j1 - j0) * w << "u);\n";
-    }
-        o << "    }\n    __syncwarp();\n";
-        o << "#pragma unroll 1\n";
-        o << "    for (u32 idx = lane; idx < NIN; idx += 32u) {\n";
-        o << "      const u32 j = idx / " << w << "u, s = idx - j * " << w << "u;\n";
-        o << "      bulk_g2s(dst + idx * TILE, a.in[j] + s * a.S + o, bytes, FULL(st, j / " << G << "u), pol);\n";
+    if (!ks.copy) o << "  if (warp == 0) asm volatile(\"createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\" : \"=l\"(pol));\n";
+    o << "  auto produce = [&](u32 u2) {\n";
+    o << "    const u32 it2 = u2 / NG, g2 = u2 - it2 * NG;\n";
+    o << "    const u32 t2 = blockIdx.x + it2 * gridDim.x;\n";
+    o << "    if (t2 >= ntiles) return;\n";
+    o << "    const u32 sl = u2 % NSLOT, ph = (u2 / NSLOT) & 1u;\n";
+    o << "    mbar_wait(EMPTY(sl), ph ^ 1u);\n";
+    o << "    const u64 o = a.off + (u64)t2 * TILE;\n";
+    o << "    const u32 dst = sbase + BAR_BYTES + sl * SLOT_BYTES;\n";
+    o << "    const u32 j0 = g2 * " << G << "u;\n";
+    o << "    const u32 nstr = (g2 + 1u == NG ? " << k << "u - j0 : " << G << "u) * " << w << "u;\n";
+    if (ks.copy) {
+        // every thread copies 16-byte chunks (a strip tile is TILE/16
+        // consecutive chunks: coalesced) and arrives on the slot's FULL
+        // barrier once its copies have landed
+        const std::uint32_t cps = TILE / 16;
+        o << "#pragma unroll 2\n";
+        o << "    for (u32 c = threadIdx.x; c < nstr * " << cps << "u; c += " << T << "u) {\n";
+        o << "      const u32 l = c / " << cps << "u, q = c - l * " << cps << "u;\n";
+        o << "      const u32 idx = j0 * " << w << "u + l, j = idx / " << w << "u, s = idx - j * " << w << "u;\n";
+        o << "      const u64 off = o + 16u * q;\n";
+        o << "      cpa16(dst + l * TILE + 16u * q, a.in[j] + s * a.S + (off < end ? off : a.off), off < end ? 16u : 0u);\n";
         o << "    }\n";
-        o << "  };\n";
-        o << "  if (warp == 0)\n    for (u32 i = 0; i + 1 < STAGES; ++i) produce(i);\n";
+        o << "    cpa_arrive(FULL(sl));\n";
     } else {
-        // every thread copies 16-byte chunks of the stage (strip tiles are
-        // TILE/16 consecutive chunks: coalesced), then arrives on the
-        // group's FULL barrier when its copies land (cp.async.mbarrier.arrive)
-        const std::uint32_t cps = TILE / 16; // chunks per strip tile
-        o << "  auto produce = [&](u32 it2) {\n";
-        o << "    const u32 t2 = blockIdx.x + it2 * gridDim.x;\n";
-        o << "    if (t2 >= ntiles) return;\n";
-        o << "    const u32 st = it2 % STAGES, ph = (it2 / STAGES) & 1u;\n";
-        o << "    mbar_wait(EMPTY(st), ph ^ 1u);\n";
-        o << "    const u64 o = a.off + (u64)t2 * TILE;\n";
-        o << "    const u32 dst = sbase + BAR_BYTES + st * (NIN * TILE);\n";
-        for (std::uint32_t g = 0; g < groups; ++g) {
-            const std::uint32_t j0 = g * G, j1 = std::min(k, j0 + G);
-            const std::uint32_t nchunks = (j1 - j0) * w * cps;
-            o << "#pragma unroll 4\n";
-            o << "    for (u32 c = threadIdx.x; c < " << nchunks << "u; c += " << consumers << "u) {\n";
-            o << "      const u32 sl = c / " << cps << "u, q = c - sl * " << cps << "u;\n";
-            o << "      const u32 idx = " << j0 * w << "u + sl, j = idx / " << w << "u, s = idx - j * " << w << "u;\n";
-            o << "      const u64 off = o + 16u * q;\n";
-            o << "      cpa16(dst + idx * TILE + 16u * q, a.in[j] + s * a.S + (off < end ? off : a.off), off < end ? 16u : 0u);\n";
-            o << "    }\n";
-            o << "    cpa_arrive(FULL(st, " << g << "u));\n";
-        }
-        o << "  };\n";
-        o << "  for (u32 i = 0; i + 1 < STAGES; ++i) produce(i);\n";
+        // warp 0: lane 0 posts the byte count, the lanes issue one
+        // cp.async.bulk per strip tile
+        o << "    const u32 bytes = (u32)(end - o < TILE ? end - o : TILE);\n";
+        o << "    if (lane == 0) mbar_expect_tx(FULL(sl), bytes * nstr);\n";
+        o << "    __syncwarp();\n";
+        o << "#pragma unroll 1\n";
+        o << "    for (u32 l = lane; l < nstr; l += 32u) {\n";
+        o << "      const u32 idx = j0 * " << w << "u + l, j = idx / " << w << "u, s = idx - j * " << w << "u;\n";
+        o << "      bulk_g2s(dst + l * TILE, a.in[j] + s * a.S + o, bytes, FULL(sl), pol);\n";
+        o << "    }\n";
     }
-    // consumers: part r computes output rows [row0_r, row0_r + rows_r) for column word `col`
-    o << "  const u32 ctid = threadIdx.x;\n";
-    o << "  const u32 part = ctid / " << cols_per_part << "u, col = ctid % " << cols_per_part << "u;\n";
+    o << "  };\n";
+    const std::string who = ks.copy ? "" : "if (warp == 0) ";
+    o << "  " << who << "for (u32 u = 0; u + 1 < NSLOT; ++u) produce(u);\n";
+    o << "  const u32 part = threadIdx.x / " << cols_per_part << "u, col = threadIdx.x % " << cols_per_part << "u;\n";
     o << "  const u64 S = a.S;\n";
     // one tile loop per output part: each is its own register-allocation region
     for (std::uint32_t r = 0; r < R; ++r) {
@@ -496,51 +490,48 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
         o << "  " << (r ? "else if" : "if") << " (part == " << r << "u) {\n";
         o << "   u32 it = 0;\n";
         o << "   for (u32 t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {\n";
-        if (ks.copy) o << "    produce(it + STAGES - 1u);\n";
-        else if (r == 0) o << "    if (warp == 0) produce(it + STAGES - 1u);\n";
-        o << "    const u32 st = it % STAGES, ph = (it / STAGES) & 1u;\n";
         o << "    const u64 o = a.off + (u64)t * TILE + 4u * col;\n";
         o << "    const bool live = o < end;\n";
-        o << "    const u32* sp = reinterpret_cast<const u32*>(sm + BAR_BYTES + st * (NIN * TILE)) + col;\n";
-        // group g's shared-memory loads (after its mbarrier) then its XORs;
-        // shared memory is close, so no cross-group prefetch
-        std::vector<const Instr*> order;
-        for (std::size_t g = 0; g < q.group_loads.size(); ++g) {
-            for (const Instr& x : q.group_loads[g]) order.push_back(&x);
-            for (const Instr& x : q.group_compute[g]) order.push_back(&x);
-        }
-        for (const Instr& x : q.tail) order.push_back(&x);
-        std::size_t last_load = 0;
-        for (std::size_t i = 0; i < order.size(); ++i)
-            if (order[i]->op == Instr::Load) last_load = i;
-        std::vector<bool> waited(groups, false), out_ptr(q.rows, false);
-        for (std::size_t idx = 0; idx < order.size(); ++idx) {
-            const Instr& ins = *order[idx];
+        std::vector<bool> out_ptr(q.rows, false);
+        std::string cur_sp;
+        auto emit = [&](const Instr& ins) {
             if (ins.op == Instr::Load) {
-                const std::uint32_t g = ins.sym / G;
-                if (!waited[g]) {
-                    o << "      mbar_wait(FULL(st, " << g << "u), ph);\n";
-                    waited[g] = true;
-                }
-                o << "      const u32 v" << ins.dst << " = sp[" << (ins.sym * w + ins.strip) * (TILE / 4) << "];\n";
-                if (idx == last_load) o << "      mbar_arrive(EMPTY(st));\n";
+                const std::uint32_t local = (ins.sym - (ins.sym / G) * G) * w + ins.strip;
+                o << "    const u32 v" << ins.dst << " = " << cur_sp << "[" << local * (TILE / 4) << "];\n";
             } else if (ins.op == Instr::Xor) {
-                o << "      const u32 v" << ins.dst << " = ";
+                o << "    const u32 v" << ins.dst << " = ";
                 emit_xor_list(o, ins.src, "v");
                 o << ";\n";
             } else {
                 const std::uint32_t row = row0 + ins.sym;
                 if (!out_ptr[ins.sym]) {
-                    o << "      u8* q" << row << " = a.out[" << row << "] + o;\n";
+                    o << "    u8* q" << row << " = a.out[" << row << "] + o;\n";
                     out_ptr[ins.sym] = true;
                 }
-                o << "      if (live) st_cs(q" << row;
+                o << "    if (live) st_cs(q" << row;
                 if (ins.strip) o << " + " << ins.strip << "u * S";
                 o << ", ";
                 emit_xor_list(o, ins.src, "v");
                 o << ");\n";
             }
+        };
+        for (std::uint32_t g = 0; g < groups; ++g) {
+            // unit (it, g): keep NSLOT-1 units in flight, wait for this one,
+            // read its strips from shared memory, release the slot, XOR
+            const std::string gs = std::to_string(g);
+            o << "    const u32 un" << gs << " = it * NG + " << g << "u;\n";
+            if (ks.copy) o << "    produce(un" << gs << " + NSLOT - 1u);\n";
+            else if (r == 0) o << "    if (warp == 0) produce(un" << gs << " + NSLOT - 1u);\n";
+            o << "    const u32 sl" << gs << " = un" << gs << " % NSLOT;\n";
+            o << "    mbar_wait(FULL(sl" << gs << "), (un" << gs << " / NSLOT) & 1u);\n";
+            o << "    const u32* sp" << gs << " = reinterpret_cast<const u32*>(sm + BAR_BYTES + sl" << gs
+              << " * SLOT_BYTES) + col;\n";
+            cur_sp = "sp" + gs;
+            for (const Instr& x : q.group_loads[g]) emit(x);
+            o << "    mbar_arrive(EMPTY(sl" << gs << "));\n";
+            for (const Instr& x : q.group_compute[g]) emit(x);
         }
+        for (const Instr& x : q.tail) emit(x);
         o << "   }\n  }\n";
     }
     o << "}\n";

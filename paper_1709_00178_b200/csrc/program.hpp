@@ -46,6 +46,7 @@ struct Program {
     TransformKind kind = TransformKind::Embedding;
     std::uint32_t rows = 0, cols = 0; // outputs x inputs
     std::uint32_t group = 1;          // input fragments whose strips are live together
+    bool cse = true;                  // pair sharing applied
     std::vector<std::uint32_t> reps;  // rows x cols ring representatives (n-bit masks)
     std::vector<std::uint32_t> fold;  // fold[t - w] = x^t mod p
     std::vector<Instr> code;          // canonical order (next group's loads before this group's XORs)

@@ -1,0 +1,100 @@
+#!/usr/bin/env python
+"""Kernel-variant sweep on one GPU (tuning aid, not the benchmark).
+
+    python tools/tune.py --config 5 --variants "PARTS=1,PART_GROUP=2,PART_CSE=0;MODE=1"
+
+Each variant is a set of PYRIT_B200_* knobs applied before the plan is compiled
+(parts / part group / pair sharing / copy engine / tile) or the launch (mode).
+Inputs are generated once on the device; every variant is timed with CUDA
+events over --steps launches after --warmup launches and checked against the
+first variant's output digest.  Prints one JSON line per variant.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--variants", required=True)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--scale", type=int, default=1, help="divide the fragment size by this")
+    a = ap.parse_args()
+
+    import torch
+
+    import paper_1709_00178_b200 as P
+    from paper_1709_00178_b200 import _lib as L
+    from paper_1709_00178_b200.workloads import WORKLOADS
+
+    lib = L.load()
+    dev = torch.device("cuda", 0)
+    wl = WORKLOADS[a.config]
+    w = wl.fld.w
+    S = wl.strip // a.scale // 16 * 16
+    sym = w * S
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    full = torch.empty((wl.k + wl.m, sym), dtype=torch.uint8, device=dev)
+    for j in range(wl.k):
+        for s in range(w):
+            P.fill(full[j, s * S:(s + 1) * S], wl.seed, j, begin=s * wl.strip, valid=wl.valid)
+    C = P.cauchy_parity_matrix(wl.code)
+    enc = P.Plan.create(wl.fld, C)
+    enc.apply([full[j].data_ptr() for j in range(wl.k)], [full[wl.k + i].data_ptr() for i in range(wl.m)], S,
+              stream=stream)
+    if wl.op == "encode":
+        ins = [full[j].data_ptr() for j in range(wl.k)]
+        out = torch.empty((wl.m, sym), dtype=torch.uint8, device=dev)
+        outs = [out[i].data_ptr() for i in range(wl.m)]
+        m = C
+    else:
+        surv, order, m = P.repair_matrix(wl.code, wl.erased)
+        ins = [full[s].data_ptr() for s in surv]
+        out = torch.empty((len(order), sym), dtype=torch.uint8, device=dev)
+        outs = [out[i].data_ptr() for i in range(len(order))]
+    moved = (len(ins) + len(outs)) * sym
+    ref = None
+    knobs = ("MODE", "COPY", "PARTS", "PART_GROUP", "PART_CSE", "TILE", "STAGES", "LANES")
+    for spec in a.variants.split(";"):
+        env = dict(kv.split("=") for kv in spec.split(",") if kv)
+        for k in knobs:
+            os.environ.pop("PYRIT_B200_" + k, None)
+        for k, v in env.items():
+            os.environ["PYRIT_B200_" + k] = v
+        L.check(lib.pyrit_set_kernel_mode(int(env.get("MODE", 0))))
+        L.check(lib.pyrit_set_lanes(int(env.get("LANES", 1))))
+        plan = P.Plan.create(wl.fld, m)
+        out.zero_()
+        try:
+            for _ in range(a.warmup):
+                plan.apply(ins, outs, S, stream=stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(a.steps):
+                plan.apply(ins, outs, S, stream=stream)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / a.steps
+            dg = int(P.digest(out).item())
+            if ref is None:
+                ref = dg
+            info = P.Plan.last_launch()
+            print(json.dumps({"variant": spec, "kernel": info["kernel"], "grid": [info["blocks"], info["threads"]],
+                              "ms": ms, "moved_GBps": moved / ms / 1e6,
+                              "source_GBps": wl.k * sym / ms / 1e6, "frac_of_6452.8": moved / ms / 1e6 / 6452.8,
+                              "matches_first": dg == ref}), flush=True)
+        except Exception as e:  # keep sweeping
+            print(json.dumps({"variant": spec, "error": str(e)[:300]}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
