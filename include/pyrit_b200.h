@@ -110,6 +110,8 @@ int pyrit_plan_decode(const pyrit_code* code, const uint32_t* erased, uint32_t n
                       uint32_t* survivors, uint32_t* outputs);
 int pyrit_plan_get_stats(const pyrit_plan* plan, pyrit_plan_stats* out);
 int pyrit_plan_reps(const pyrit_plan* plan, uint32_t* reps /* rows x cols */);
+/* key of the plan in the staged-kernel tuning table (tuned.tsv next to the library) */
+int pyrit_plan_key(const pyrit_plan* plan, char* buf, size_t cap);
 /* generated CUDA source of the fused kernel; *len receives the full size.
  * lanes: 1/2/4 = direct LDG kernel with that many 32-bit words per thread per
  * strip, 0 = byte mode, PYRIT_SOURCE_STAGED = the TMA-staged kernel */

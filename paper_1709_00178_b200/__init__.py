@@ -186,6 +186,12 @@ class Plan:
         L.check(_clib().pyrit_plan_get_stats(self._h, C.byref(st)))
         return {k: getattr(st, k) for k, _ in L.pyrit_plan_stats._fields_}
 
+    def key(self) -> str:
+        """Tuning-table key (field, transform, ring representatives)."""
+        buf = C.create_string_buffer(96)
+        L.check(_clib().pyrit_plan_key(self._h, buf, 96))
+        return buf.value.decode()
+
     def reps(self) -> np.ndarray:
         st = self.stats()
         out = np.zeros(st["rows"] * st["cols"], dtype=np.uint32)

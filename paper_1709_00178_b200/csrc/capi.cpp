@@ -299,6 +299,16 @@ int pyrit_plan_get_stats(const pyrit_plan* plan, pyrit_plan_stats* out) {
     });
 }
 
+int pyrit_plan_key(const pyrit_plan* plan, char* buf, size_t cap) {
+    return guarded([&] {
+        if (!plan || !buf || !cap) raise(Errc::InvalidArgument, "null argument");
+        const std::string k = plan_key(plan->prog);
+        const size_t n = std::min(cap - 1, k.size());
+        std::memcpy(buf, k.data(), n);
+        buf[n] = 0;
+    });
+}
+
 int pyrit_plan_reps(const pyrit_plan* plan, uint32_t* reps) {
     return guarded([&] {
         if (!plan || !reps) raise(Errc::InvalidArgument, "null argument");

@@ -3,8 +3,11 @@
 #include <algorithm>
 #include <bit>
 #include <cstdio>
+#include <dlfcn.h>
+
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <sstream>
 
 namespace pyrit_b200 {
@@ -108,6 +111,67 @@ void lazy_order(std::vector<Instr>& code, std::size_t ntemps) {
 }
 
 } // namespace
+
+std::string plan_key(const Program& p) {
+    std::ostringstream fp;
+    fp << p.field.w << ',' << p.field.n << ',' << p.field.modulus << ',' << int(p.kind) << ',' << p.rows << ','
+       << p.cols << ':';
+    for (std::uint32_t r : p.reps) fp << r << ',';
+    char key[64];
+    std::snprintf(key, sizeof key, "w%un%u_%ux%u_%016llx", p.field.w, p.field.n, p.rows, p.cols,
+                  static_cast<unsigned long long>(fnv1a(fp.str())));
+    return key;
+}
+
+namespace {
+std::mutex g_tuned_mu;
+std::string g_tuned_path;
+std::vector<TunedEntry> g_tuned;
+bool g_tuned_loaded = false;
+
+std::string library_dir() {
+    Dl_info info{};
+    if (dladdr(reinterpret_cast<void*>(&library_dir), &info) && info.dli_fname) {
+        std::string so = info.dli_fname;
+        const auto slash = so.rfind('/');
+        return slash == std::string::npos ? std::string(".") : so.substr(0, slash);
+    }
+    return ".";
+}
+} // namespace
+
+void set_tuned_path(const std::string& path) {
+    std::lock_guard<std::mutex> lk(g_tuned_mu);
+    g_tuned_path = path;
+    g_tuned_loaded = false;
+}
+
+const TunedEntry* find_tuned(const std::string& key) {
+    std::lock_guard<std::mutex> lk(g_tuned_mu);
+    if (!g_tuned_loaded) {
+        g_tuned_loaded = true;
+        g_tuned.clear();
+        std::string path = g_tuned_path.empty() ? library_dir() + "/tuned.tsv" : g_tuned_path;
+        if (const char* env = std::getenv("PYRIT_B200_TUNED")) path = env;
+        if (!path.empty())
+            if (FILE* fh = std::fopen(path.c_str(), "r")) {
+                char line[512];
+                while (std::fgets(line, sizeof line, fh)) {
+                    if (line[0] == '#' || line[0] == '\n') continue;
+                    char k[128];
+                    unsigned parts = 0, pg = 0;
+                    int cse = -1;
+                    if (std::sscanf(line, "%127s %u %u %d", k, &parts, &pg, &cse) == 4)
+                        g_tuned.push_back(TunedEntry{k, parts, pg, cse});
+                }
+                std::fclose(fh);
+            }
+    }
+    // the table is only written at load time; later lookups are read-only
+    for (const TunedEntry& t : g_tuned)
+        if (t.key == key) return &t;
+    return nullptr;
+}
 
 Program compile_program(const Field& f, TransformKind kind, const Matrix& m, const CompileOptions& opt) {
     validate_field(f);
@@ -251,40 +315,54 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
     }
     p.stats.vars = nvars;
 
-    // output parts for the staged kernel (see KernelShape): keep each part's
-    // ring accumulators (rows x out_rows words) near 40 registers
+    // Output parts of the staged kernel (see KernelShape).  Knobs, in order
+    // of precedence: CompileOptions, PYRIT_B200_PARTS / _PART_GROUP /
+    // _PART_CSE, the measured tuning table (tuned.tsv next to the library),
+    // and the heuristic: one part; fragment groups of about 48 strips; pair
+    // sharing only while the shared program stays small enough (<= 1000
+    // XORs per column word) for ptxas to keep it spill-free in 255 registers.
     if (opt.parts != 1 && e > 0) {
-        // parts: the smallest power of two that keeps each part's program
-        // near 450 two-input XORs (about 200 live registers under ptxas)
+        const auto env_u = [](const char* name) -> int {
+            const char* v = std::getenv(name);
+            return v ? std::atoi(v) : -1;
+        };
+        const TunedEntry* tuned = find_tuned(plan_key(p));
         std::uint32_t R = opt.parts;
-        if (!R) {
-            const char* env = std::getenv("PYRIT_B200_PARTS");
-            R = env ? static_cast<std::uint32_t>(std::atoi(env)) : 0;
-        }
-        if (!R) {
-            const std::uint64_t want = (p.stats.xors + 449) / 450;
-            R = 1;
-            while (R < want && R < 8) R *= 2;
-        }
+        if (!R && env_u("PYRIT_B200_PARTS") > 0) R = static_cast<std::uint32_t>(env_u("PYRIT_B200_PARTS"));
+        if (!R && tuned) R = tuned->parts;
+        if (!R) R = 1;
         R = std::max<std::uint32_t>(1, std::min(R, e));
         std::uint32_t pg = opt.part_group;
-        if (!pg) {
-            const char* env = std::getenv("PYRIT_B200_PART_GROUP");
-            pg = env ? static_cast<std::uint32_t>(std::atoi(env)) : 8;
-        }
+        if (!pg && env_u("PYRIT_B200_PART_GROUP") > 0) pg = static_cast<std::uint32_t>(env_u("PYRIT_B200_PART_GROUP"));
+        if (!pg && tuned) pg = tuned->part_group;
+        if (!pg) pg = std::max<std::uint32_t>(1, (48 + w / 2) / w);
         pg = std::max<std::uint32_t>(1, std::min(pg, k));
-        for (std::uint32_t r = 0, row0 = 0; r < R; ++r) {
-            const std::uint32_t nrows = e / R + (r < e % R ? 1 : 0);
-            Matrix sub(nrows, k);
-            for (std::uint32_t i = 0; i < nrows; ++i)
-                for (std::uint32_t j = 0; j < k; ++j) sub.at(i, j) = m.at(row0 + i, j);
-            CompileOptions o2 = opt;
-            o2.parts = 1;
-            o2.group = pg;
-            if (const char* env = std::getenv("PYRIT_B200_PART_CSE")) o2.cse = std::atoi(env) != 0;
-            p.parts.push_back(compile_program(f, kind, sub, o2));
-            p.part_row0.push_back(row0);
-            row0 += nrows;
+        int pcse = env_u("PYRIT_B200_PART_CSE");
+        if (pcse < 0 && tuned) pcse = tuned->part_cse;
+        auto build_parts = [&](bool cse) {
+            p.parts.clear();
+            p.part_row0.clear();
+            for (std::uint32_t r = 0, row0 = 0; r < R; ++r) {
+                const std::uint32_t nrows = e / R + (r < e % R ? 1 : 0);
+                Matrix sub(nrows, k);
+                for (std::uint32_t i = 0; i < nrows; ++i)
+                    for (std::uint32_t j = 0; j < k; ++j) sub.at(i, j) = m.at(row0 + i, j);
+                CompileOptions o2 = opt;
+                o2.parts = 1;
+                o2.group = pg;
+                o2.cse = cse && opt.cse;
+                p.parts.push_back(compile_program(f, kind, sub, o2));
+                p.part_row0.push_back(row0);
+                row0 += nrows;
+            }
+        };
+        if (pcse >= 0) {
+            build_parts(pcse != 0);
+        } else {
+            build_parts(true);
+            std::uint64_t worst = 0;
+            for (const Program& q : p.parts) worst = std::max<std::uint64_t>(worst, q.stats.xors);
+            if (worst > 1000) build_parts(false);
         }
     }
     return p;

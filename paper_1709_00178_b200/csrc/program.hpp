@@ -68,6 +68,17 @@ struct CompileOptions {
     std::uint32_t part_group = 0; // fragment group of the parts: 0 auto
 };
 
+// Measured staged-kernel choices for specific programs (tuned.tsv):
+//   <plan_key> <parts> <part_group> <part_cse>
+struct TunedEntry {
+    std::string key;
+    std::uint32_t parts = 1, part_group = 1;
+    int part_cse = 0;
+};
+std::string plan_key(const Program& p); // field + transform + ring representatives
+void set_tuned_path(const std::string& path);
+const TunedEntry* find_tuned(const std::string& key);
+
 // compile_schedule analogue: matrix (rows x cols, GF(2^w) entries) -> program
 Program compile_program(const Field& f, TransformKind kind, const Matrix& m, const CompileOptions& opt);
 

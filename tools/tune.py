@@ -88,7 +88,7 @@ def main():
             if ref is None:
                 ref = dg
             info = P.Plan.last_launch()
-            print(json.dumps({"variant": spec, "kernel": info["kernel"], "grid": [info["blocks"], info["threads"]],
+            print(json.dumps({"variant": spec, "key": plan.key(), "kernel": info["kernel"], "grid": [info["blocks"], info["threads"]],
                               "ms": ms, "moved_GBps": moved / ms / 1e6,
                               "source_GBps": wl.k * sym / ms / 1e6, "frac_of_6452.8": moved / ms / 1e6 / 6452.8,
                               "matches_first": dg == ref}), flush=True)
