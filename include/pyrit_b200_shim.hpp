@@ -1,0 +1,72 @@
+// pyrit_b200_shim.hpp -- drop-in GPU replacements for the reference codec's
+// top-level calls, written against the reference's OWN types.
+//
+//   pyrit::encode(data, code, threads)          codec.hpp:469-477
+//     -> pyrit::cuda::encode(data, code, device)
+//   pyrit::decode(symbols, erased, code, threads) codec.hpp:498-541
+//     -> pyrit::cuda::decode(symbols, erased, code, device)
+//
+// Include after the reference headers (it needs SymbolBuffer, CodeSpec,
+// Error from proj/include/pyrit/) and link libpyrit_b200.so.  Validation and
+// error behaviour follow the reference: shape errors throw pyrit::Error with
+// the same Errc (BufferShape, InvalidArgument, InsufficientShards,
+// TooManySymbols); device failures throw std::runtime_error.  Results are
+// byte-identical to the reference's embedding-transform encode/decode (and,
+// for fields the reference cannot represent, e.g. GF(2^8) in R_{2,17}, to its
+// field oracle oracle_apply / encode_crs).
+#pragma once
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "pyrit/codec.hpp"
+#include "pyrit_b200.h"
+
+namespace pyrit::cuda {
+
+inline pyrit_code to_c(const CodeSpec& code) {
+    pyrit_code c{};
+    c.k = code.k;
+    c.r = code.r;
+    c.field.w = code.field.w;
+    c.field.n = code.field.n;
+    c.field.kind = code.field.kind == FieldKind::Esp ? 1u : 0u;
+    c.field.s = code.field.s;
+    c.field.r_esp = code.field.r_esp;
+    c.field.modulus = code.field.modulus;
+    c.transform = static_cast<std::uint32_t>(code.transform);
+    return c;
+}
+
+// 1 + Errc -> pyrit::Error (errors.hpp:57-84); negative -> device failure
+inline void check(int rc) {
+    if (rc == 0) return;
+    if (rc >= 1 && rc <= 11) throw Error(static_cast<Errc>(rc - 1), pyrit_strerror(rc));
+    throw std::runtime_error(std::string("pyrit_b200: ") + pyrit_strerror(rc));
+}
+
+// codec.hpp:469 encode(): parity = C * data, on the GPU (host buffers in,
+// host buffers out; H2D, fused ring kernel and D2H are pipelined inside).
+inline SymbolBuffer encode(const SymbolBuffer& data, const CodeSpec& code, int device = 0) {
+    check_data_shape(data, code); // codec.hpp:462-466, the reference's own validation
+    SymbolBuffer parity(code.r, data.symbol_size(), code.field);
+    const pyrit_code c = to_c(code);
+    if (code.r) check(pyrit_encode_host(&c, data.symbol(0), parity.symbol(0), data.symbol_size(), device));
+    return parity;
+}
+
+// codec.hpp:498 decode(): in-place repair of the listed symbols from any k
+// survivors (lowest index first), one fused pass on the GPU.
+inline void decode(SymbolBuffer& symbols, const std::vector<unsigned>& erased, const CodeSpec& code,
+                   int device = 0) {
+    validate_code(code);
+    if (!(symbols.spec() == code.field) || symbols.symbols() != code.k + code.r)
+        raise(Errc::BufferShape, "symbol buffer does not match the code");
+    const pyrit_code c = to_c(code);
+    std::vector<std::uint32_t> er(erased.begin(), erased.end());
+    check(pyrit_decode_host(&c, symbols.symbol(0), er.data(), static_cast<std::uint32_t>(er.size()),
+                            symbols.symbol_size(), device));
+}
+
+} // namespace pyrit::cuda

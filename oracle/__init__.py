@@ -43,7 +43,8 @@ GF4096 = Field(12, 13, 0, 1, 12, 0x1FFF)  # BASELINE config 5
 
 
 def build() -> None:
-    subprocess.run(["make", "-s", "-C", HERE], check=True)
+    """liboracle.so, and (reference tree present) _ref/libpyrit_ref.so + _ref/shim_check."""
+    subprocess.run(["make", "-s", "-C", HERE, "all", "shim"], check=True)
 
 
 def _load(path: str):

@@ -1,0 +1,75 @@
+// shim_check.cpp -- TEST INFRASTRUCTURE: exercises include/pyrit_b200_shim.hpp
+// exactly the way a reference user would (reference SymbolBuffer/CodeSpec,
+// reference encode()/decode() beside the GPU versions).  Built by
+// oracle/Makefile (target `shim`) against the unmodified reference headers
+// into oracle/_ref/shim_check; run on a GPU box by tests/test_gpu_shim.py.
+#include <cstdio>
+#include <cstring>
+#include <random>
+
+#include "pyrit/codec.hpp"
+#include "pyrit_b200_shim.hpp"
+
+using namespace pyrit;
+
+static bool same(const SymbolBuffer& a, const SymbolBuffer& b) {
+    return a.symbols() == b.symbols() && a.symbol_size() == b.symbol_size() &&
+           std::memcmp(a.symbol(0), b.symbol(0), a.symbols() * a.symbol_size()) == 0;
+}
+
+static void fill(SymbolBuffer& buf, std::uint64_t seed) {
+    std::mt19937_64 rng(seed);
+    for (unsigned s = 0; s < buf.symbols(); ++s)
+        for (std::size_t i = 0; i < buf.symbol_size(); ++i) buf.symbol(s)[i] = static_cast<std::uint8_t>(rng());
+}
+
+int main() {
+    int failures = 0;
+    struct Case {
+        const char* name;
+        FieldSpec f;
+        unsigned k, r;
+        std::size_t symbol_size;
+        bool ring_ok; // the reference's own ring encode() is valid for this field
+    };
+    const Case cases[] = {
+        {"gf16 k4 r2 (BASELINE config 1 shape)", FieldSpec::gf16_aop(), 4, 2, 4 * 4096, true},
+        {"gf64 esp k6 r3", FieldSpec::gf64_esp(), 6, 3, 24 * 1000, true},
+        {"gf1024 k12 r4 (config 3 shape)", FieldSpec{10, 11, FieldKind::Aop, 1, 10, 0x7FF}, 12, 4, 160 * 512, true},
+        {"gf4096 k16 r4 (config 5 shape)", FieldSpec{12, 13, FieldKind::Aop, 1, 12, 0x1FFF}, 16, 4, 192 * 512, true},
+        {"gf256/R17 k10 r4 (configs 2/4)", FieldSpec{8, 17, FieldKind::Aop, 1, 8, 0x139}, 10, 4, 8 * 8192, false},
+    };
+    for (const Case& c : cases) {
+        const CodeSpec code{c.k, c.r, c.f, TransformKind::Embedding};
+        SymbolBuffer data(c.k, c.symbol_size, c.f);
+        fill(data, c.k * 1000 + c.r);
+        const SymbolBuffer want = c.ring_ok ? encode(data, code, 4) : encode_crs(data, code, 4);
+        const SymbolBuffer got = pyrit::cuda::encode(data, code);
+        const bool enc_ok = same(got, want);
+        // decode: erase r symbols (data and parity mixed), repair in place
+        SymbolBuffer full(c.k + c.r, c.symbol_size, c.f);
+        std::memcpy(full.symbol(0), data.symbol(0), c.k * c.symbol_size);
+        std::memcpy(full.symbol(c.k), want.symbol(0), c.r * c.symbol_size);
+        SymbolBuffer work = full;
+        std::vector<unsigned> erased;
+        for (unsigned i = 0; i < c.r; ++i) erased.push_back((i * 5 + 1) % (c.k + c.r));
+        for (unsigned e : erased) std::memset(work.symbol(e), 0xAA, c.symbol_size);
+        pyrit::cuda::decode(work, erased, code);
+        const bool dec_ok = same(work, full);
+        std::printf("%-40s encode %s decode %s\n", c.name, enc_ok ? "OK" : "MISMATCH", dec_ok ? "OK" : "MISMATCH");
+        failures += !enc_ok + !dec_ok;
+    }
+    // error behaviour mirrors the reference
+    try {
+        const CodeSpec code{4, 2, FieldSpec::gf16_aop(), TransformKind::Embedding};
+        SymbolBuffer full(6, 16, FieldSpec::gf16_aop());
+        pyrit::cuda::decode(full, {0, 1, 2}, code);
+        std::printf("InsufficientShards not raised\n");
+        ++failures;
+    } catch (const Error& e) {
+        std::printf("decode 3 erasures with r=2 -> Errc %d (%s)\n", static_cast<int>(e.code()), e.what());
+        failures += e.code() != Errc::InsufficientShards;
+    }
+    std::printf(failures ? "SHIM CHECK FAILED\n" : "SHIM CHECK PASSED\n");
+    return failures ? 1 : 0;
+}

@@ -1,0 +1,96 @@
+"""The C-ABI library on a machine without a GPU: it loads, exports every entry
+point include/pyrit_b200.h declares, and its host-only entry points behave
+(error codes mirror Errc, errors.hpp:57-69).  No device calls here."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_1709_00178_b200 as P
+from paper_1709_00178_b200 import _lib as L
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "pyrit_b200.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pyrit_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for must in ("pyrit_cu_apply", "pyrit_cu_encode", "pyrit_cu_decode", "pyrit_encode_host", "pyrit_decode_host",
+                 "pyrit_plan_create", "pyrit_cauchy_parity_matrix", "pyrit_strerror"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    out = subprocess.run(["nm", "-D", "--defined-only", L.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\sT\s(pyrit_[a-z0-9_]+)", out))
+    missing = [n for n in declared_functions() if n not in exported]
+    assert not missing, missing
+    # and nothing else leaks (internals are hidden; static cudart is excluded)
+    assert all(n.startswith("pyrit_") for n in re.findall(r"\sT\s(\S+)", out))
+    lib = L.load()
+    for n in declared_functions():
+        assert hasattr(lib, n)
+    assert set(L.EXPORTS) <= set(declared_functions())
+
+
+def test_version_and_strerror():
+    lib = L.load()
+    assert b"sm_100a" in lib.pyrit_version()
+    assert lib.pyrit_strerror(0) == b"ok"
+    assert lib.pyrit_strerror(3).startswith(b"TooManySymbols")
+    assert lib.pyrit_strerror(6).startswith(b"InsufficientShards")
+
+
+def test_return_codes_are_errc_plus_one():
+    lib = L.load()
+    code = L.pyrit_code(13, 4, L.pyrit_field(4, 5, 0, 1, 4, 0x1F), 0)
+    out = np.zeros(64, np.uint16)
+    assert lib.pyrit_cauchy_parity_matrix(C.byref(code), out.ctypes.data) == 3  # TooManySymbols
+    code = L.pyrit_code(0, 4, L.pyrit_field(4, 5, 0, 1, 4, 0x1F), 0)
+    assert lib.pyrit_cauchy_parity_matrix(C.byref(code), out.ctypes.data) == 11  # InvalidArgument
+    bad = L.pyrit_field(4, 6, 0, 1, 4, 0x1F)  # p does not divide x^6 + 1
+    assert lib.pyrit_field_validate(C.byref(bad)) == 11
+    f = L.pyrit_field()
+    assert lib.pyrit_field_named(b"gf256_r17", C.byref(f)) == 0 and (f.w, f.n, f.modulus) == (8, 17, 0x139)
+    assert lib.pyrit_field_named(b"nope", C.byref(f)) == 11
+    # symbol size rules of SymbolBuffer (codec.hpp:285-287) are checked before any device work
+    code = L.pyrit_code(4, 2, L.pyrit_field(4, 5, 0, 1, 4, 0x1F), 0)
+    ptrs = (C.c_void_p * 6)()
+    assert lib.pyrit_cu_encode(C.byref(code), ptrs, ptrs, 12, None) == 4  # BufferShape (12 % 8)
+    assert lib.pyrit_cu_encode(C.byref(code), ptrs, ptrs, 0, None) == 4
+    er = (C.c_uint32 * 3)(0, 1, 2)
+    assert lib.pyrit_cu_decode(C.byref(code), ptrs, er, 3, 16, None) == 6  # InsufficientShards
+
+
+def test_plans_describe_themselves():
+    plan = P.Plan.encode(P.CodeSpec(16, 4, P.FieldSpec.aop(12)))
+    st = plan.stats()
+    assert (st["rows"], st["cols"], st["ref_region_ops"]) == (4, 16, 2808)
+    name, src = plan.source(L.SOURCE_STAGED)
+    assert name.startswith("pyrit_ring_k16_e4_w12_n13_cpa") and "cp.async.cg.shared.global" in src
+    assert "mbarrier.try_wait.parity" in src and "__grid_constant__" in src
+    name1, src1 = plan.source(1)
+    assert "_L1_" in name1 and "ld.global.nc" in src1
+    assert plan.key().startswith("w12n13_4x16_")
+    assert plan.reps().shape == (4, 16)
+
+
+def test_tuned_table_entries_match_current_plan_keys():
+    from paper_1709_00178_b200.workloads import WORKLOADS
+    keys = set()
+    for line in open(os.path.join(ROOT, "paper_1709_00178_b200", "tuned.tsv")):
+        if line.strip() and not line.startswith("#"):
+            keys.add(line.split()[0])
+    for cfg in (2, 3, 4, 5):
+        wl = WORKLOADS[cfg]
+        plan = P.Plan.encode(wl.code) if wl.op == "encode" else P.Plan.decode(wl.code, wl.erased)
+        assert plan.key() in keys, cfg
