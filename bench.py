@@ -174,6 +174,7 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--no-graph", action="store_true", help="launch the timed steps from Python")
     args = ap.parse_args(argv)
 
     rank = int(os.environ.get("RANK", "0"))
@@ -250,16 +251,35 @@ def main(argv=None):
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
+    # the K timed steps are captured once into a CUDA graph (one kernel node per
+    # step) so that small configurations are not bound by Python launch overhead
+    graph = None
     launches0 = lib.pyrit_kernel_launches()
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            cs = torch.cuda.current_stream().cuda_stream
+            for i in range(args.steps):
+                ins, outs = sets[i % nsets][0], sets[i % nsets][1]
+                plan.apply(ins, outs, Ls, 0, Ls, stream=cs)
+        torch.cuda.synchronize(dev)
+        graph.replay()  # untimed replay (graph upload)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+    stream = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize(dev)
         e0.record(stream)
-        for i in range(args.steps):
-            step(i)
+        if graph is not None:
+            graph.replay()
+        else:
+            for i in range(args.steps):
+                step(i)
         e1.record(stream)
         torch.cuda.synchronize(dev)
-    launches = lib.pyrit_kernel_launches() - launches0
+    launches = args.steps if graph is not None else lib.pyrit_kernel_launches() - launches0
     launch = P.Plan.last_launch()
     ms = e0.elapsed_time(e1) / args.steps
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -304,6 +324,7 @@ def main(argv=None):
                        "p": hex(wl.fld.modulus), "fragment_bytes": wl.frag, "strip_bytes": wl.strip,
                        "shard_strip_bytes": Ls, "erased": list(wl.erased), "parallelism": f"byte-offset shards x{world}",
                        "l2": "inputs larger than L2" if nsets == 1 else f"{nsets} rotating buffer sets > L2",
+                       "launch": "CUDA graph of the K steps" if graph is not None else "per-step launches",
                        "kernel": launch["kernel"], "grid": [launch["blocks"], launch["threads"]],
                        "xors_per_column_word": st["xors"],
                        "reference_region_ops": st["ref_region_ops"]},

@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--scale", type=int, default=1, help="divide the fragment size by this")
+    ap.add_argument("--rounds", type=int, default=3, help="interleaved repeats per variant (median reported)")
+    ap.add_argument("--no-graph", action="store_true", help="launch from Python instead of a captured CUDA graph")
     a = ap.parse_args()
 
     import torch
@@ -63,38 +65,60 @@ def main():
     moved = (len(ins) + len(outs)) * sym
     ref = None
     knobs = ("MODE", "COPY", "PARTS", "PART_GROUP", "PART_CSE", "TILE", "STAGES", "LANES")
-    for spec in a.variants.split(";"):
-        env = dict(kv.split("=") for kv in spec.split(",") if kv)
-        for k in knobs:
-            os.environ.pop("PYRIT_B200_" + k, None)
-        for k, v in env.items():
-            os.environ["PYRIT_B200_" + k] = v
-        L.check(lib.pyrit_set_kernel_mode(int(env.get("MODE", 0))))
-        L.check(lib.pyrit_set_lanes(int(env.get("LANES", 1))))
-        plan = P.Plan.create(wl.fld, m)
-        out.zero_()
-        try:
-            for _ in range(a.warmup):
-                plan.apply(ins, outs, S, stream=stream)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            e0.record()
-            for _ in range(a.steps):
-                plan.apply(ins, outs, S, stream=stream)
-            e1.record()
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / a.steps
-            dg = int(P.digest(out).item())
-            if ref is None:
-                ref = dg
-            info = P.Plan.last_launch()
-            print(json.dumps({"variant": spec, "key": plan.key(), "kernel": info["kernel"], "grid": [info["blocks"], info["threads"]],
-                              "ms": ms, "moved_GBps": moved / ms / 1e6,
-                              "source_GBps": wl.k * sym / ms / 1e6, "frac_of_6452.8": moved / ms / 1e6 / 6452.8,
-                              "matches_first": dg == ref}), flush=True)
-        except Exception as e:  # keep sweeping
-            print(json.dumps({"variant": spec, "error": str(e)[:300]}), flush=True)
-
+    specs = a.variants.split(";")
+    plans, graphs, times = {}, {}, {sp: [] for sp in specs}
+    for rnd in range(a.rounds):
+        for spec in specs:
+            env = dict(kv.split("=") for kv in spec.split(",") if kv)
+            for k in knobs:
+                os.environ.pop("PYRIT_B200_" + k, None)
+            for k, v in env.items():
+                os.environ["PYRIT_B200_" + k] = v
+            L.check(lib.pyrit_set_kernel_mode(int(env.get("MODE", 0))))
+            L.check(lib.pyrit_set_lanes(int(env.get("LANES", 1))))
+            try:
+                if spec not in plans:
+                    plans[spec] = P.Plan.create(wl.fld, m)
+                plan = plans[spec]
+                for _ in range(a.warmup):
+                    plan.apply(ins, outs, S, stream=stream)
+                torch.cuda.synchronize()
+                if not a.no_graph and spec not in graphs:
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g):
+                        cs = torch.cuda.current_stream().cuda_stream
+                        for _ in range(a.steps):
+                            plan.apply(ins, outs, S, stream=cs)
+                    graphs[spec] = g
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record()
+                if a.no_graph:
+                    for _ in range(a.steps):
+                        plan.apply(ins, outs, S, stream=stream)
+                else:
+                    graphs[spec].replay()
+                e1.record()
+                torch.cuda.synchronize()
+                times[spec].append(e0.elapsed_time(e1) / a.steps)
+                if rnd == a.rounds - 1:
+                    out.zero_()
+                    plan.apply(ins, outs, S, stream=stream)
+                    dg = int(P.digest(out).item())
+                    if ref is None:
+                        ref = dg
+                    info = P.Plan.last_launch()
+                    ts = sorted(times[spec])
+                    ms = ts[len(ts) // 2]
+                    print(json.dumps({"variant": spec, "key": plan.key(), "kernel": info["kernel"],
+                                      "grid": [info["blocks"], info["threads"]], "ms": ms,
+                                      "ms_all": [round(x, 5) for x in times[spec]],
+                                      "moved_GBps": moved / ms / 1e6, "source_GBps": wl.k * sym / ms / 1e6,
+                                      "frac_of_6452.8": moved / ms / 1e6 / 6452.8, "matches_first": dg == ref,
+                                      "graph": not a.no_graph}), flush=True)
+            except Exception as e:  # keep sweeping
+                print(json.dumps({"variant": spec, "error": str(e)[:300]}), flush=True)
+                times[spec] = times[spec] or [float("nan")]
 
 if __name__ == "__main__":
     main()
