@@ -24,14 +24,16 @@ std::uint64_t fnv1a(const std::string& s) {
 namespace {
 
 constexpr std::uint32_t kNone = 0xFFFFFFFFu;
+// bump whenever generated code changes for the same program (prebuilt cubins are keyed by name)
+constexpr int kGeneratorVersion = 4;
 
 // Greedy pair elimination over XOR targets.  Each target is a set of
 // variable ids; the most frequent pair (ties: smallest ids) becomes a new
 // temporary t = a ^ b substituted into every target holding both, until
 // no pair is shared.  Emits the temporaries into `code`.
 void share_pairs(std::vector<std::vector<std::uint32_t>>& targets, std::uint32_t& nvars,
-                 std::vector<Instr>& code) {
-    for (;;) {
+                 std::vector<Instr>& code, std::uint32_t max_temps = 0) {
+    for (std::uint32_t made = 0; !max_temps || made < max_temps; ++made) {
         std::vector<std::uint32_t> ids;
         for (auto& t : targets) ids.insert(ids.end(), t.begin(), t.end());
         std::sort(ids.begin(), ids.end());
@@ -253,7 +255,7 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
                 std::sort(tg.begin(), tg.end());
                 p.stats.naive_xors += tg.size(); // one XOR per term into the row...
             }
-        if (opt.cse) share_pairs(targets, nvars, cp);
+        if (opt.cse) share_pairs(targets, nvars, cp, opt.max_temps);
         const std::size_t ntemps = cp.size();
         for (std::size_t r = 0; r < targets.size(); ++r) {
             auto& tg = targets[r];
@@ -351,6 +353,7 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
                 o2.parts = 1;
                 o2.group = pg;
                 o2.cse = cse && opt.cse;
+                if (const char* env = std::getenv("PYRIT_B200_PART_TEMPS")) o2.max_temps = std::atoi(env);
                 p.parts.push_back(compile_program(f, kind, sub, o2));
                 p.part_row0.push_back(row0);
                 row0 += nrows;
@@ -398,8 +401,8 @@ void interpret_program(const Program& p, const std::uint8_t* const* in, std::uin
 
 std::string kernel_name(const Program& p, const KernelShape& ks) {
     std::ostringstream fp;
-    fp << p.field.w << ',' << p.field.n << ',' << p.field.modulus << ',' << int(p.kind) << ',' << p.rows << ','
-       << p.cols << ',' << p.group << ',' << ks.lanes << ',' << ks.threads << ',' << ks.min_blocks << ','
+    fp << kGeneratorVersion << ';' << p.field.w << ',' << p.field.n << ',' << p.field.modulus << ',' << int(p.kind)
+       << ',' << p.rows << ',' << p.cols << ',' << p.group << ',' << ks.lanes << ',' << ks.threads << ',' << ks.min_blocks << ','
        << ks.staged << ',' << ks.tile << ',' << ks.stages << ',' << ks.bar_bytes << ',' << p.parts.size() << ','
        << (p.parts.empty() ? 0u : p.parts[0].group) << ',' << ks.copy << ',' << p.cse << ',';
     for (const Program& q : p.parts) fp << q.rows << '/' << q.cse << '/' << q.stats.xors << ',';
@@ -535,13 +538,23 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
         // every thread copies 16-byte chunks (a strip tile is TILE/16
         // consecutive chunks: coalesced) and arrives on the slot's FULL
         // barrier once its copies have landed
+        // lanes are laid out strip-major: LPS lanes cover one strip tile (CPL
+        // chunks each), a warp covers SPW strips per step, warps stride
+        // strips by NW*SPW; chunk validity only depends on the tile
         const std::uint32_t cps = TILE / 16;
-        o << "#pragma unroll 2\n";
-        o << "    for (u32 c = threadIdx.x; c < nstr * " << cps << "u; c += " << T << "u) {\n";
-        o << "      const u32 l = c / " << cps << "u, q = c - l * " << cps << "u;\n";
+        const std::uint32_t lps = std::min<std::uint32_t>(32, cps), spw = 32 / lps, cpl = cps / lps, nw = T / 32;
+        o << "    const u32 vb = (u32)(end - o < TILE ? end - o : TILE);\n";
+        o << "    const u32 lq = lane % " << lps << "u, lsub = lane / " << lps << "u;\n";
+        for (std::uint32_t c = 0; c < cpl; ++c)
+            o << "    const u32 n" << c << " = 16u * (lq + " << c * lps << "u) < vb ? 16u : 0u;\n";
+        o << "#pragma unroll 1\n";
+        o << "    for (u32 l = warp * " << spw << "u + lsub; l < nstr; l += " << nw * spw << "u) {\n";
         o << "      const u32 idx = j0 * " << w << "u + l, j = idx / " << w << "u, s = idx - j * " << w << "u;\n";
-        o << "      const u64 off = o + 16u * q;\n";
-        o << "      cpa16(dst + l * TILE + 16u * q, a.in[j] + s * a.S + (off < end ? off : a.off), off < end ? 16u : 0u);\n";
+        o << "      const u8* src = a.in[j] + s * a.S + o + 16u * lq;\n";
+        o << "      const u32 d = dst + l * TILE + 16u * lq;\n";
+        for (std::uint32_t c = 0; c < cpl; ++c)
+            o << "      cpa16(d + " << 16 * c * lps << "u, n" << c << " ? src + " << 16 * c * lps
+              << "u : a.in[0] + a.off, n" << c << ");\n";
         o << "    }\n";
         o << "    cpa_arrive(FULL(sl));\n";
     } else {

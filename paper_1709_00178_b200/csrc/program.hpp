@@ -66,6 +66,7 @@ struct CompileOptions {
     bool dense = false;        // RingRep::Dense (plain phi1) instead of Sparse (schedule.hpp:78)
     std::uint32_t parts = 0;   // output parts for the staged kernel: 0 auto, 1 = do not split
     std::uint32_t part_group = 0; // fragment group of the parts: 0 auto
+    std::uint32_t max_temps = 0;  // cap on shared pair temporaries per group (0 = no cap)
 };
 
 // Measured staged-kernel choices for specific programs (tuned.tsv):

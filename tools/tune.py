@@ -16,6 +16,9 @@ import json
 import os
 import sys
 
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import ClockSampler  # noqa: E402
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
@@ -66,7 +69,7 @@ def main():
     ref = None
     knobs = ("MODE", "COPY", "PARTS", "PART_GROUP", "PART_CSE", "TILE", "STAGES", "LANES")
     specs = a.variants.split(";")
-    plans, graphs, times = {}, {}, {sp: [] for sp in specs}
+    plans, graphs, times, clocks = {}, {}, {sp: [] for sp in specs}, {}
     for rnd in range(a.rounds):
         for spec in specs:
             env = dict(kv.split("=") for kv in spec.split(",") if kv)
@@ -92,14 +95,16 @@ def main():
                     graphs[spec] = g
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 torch.cuda.synchronize()
-                e0.record()
-                if a.no_graph:
-                    for _ in range(a.steps):
-                        plan.apply(ins, outs, S, stream=stream)
-                else:
-                    graphs[spec].replay()
-                e1.record()
-                torch.cuda.synchronize()
+                with ClockSampler(0) as clk:
+                    e0.record()
+                    if a.no_graph:
+                        for _ in range(a.steps):
+                            plan.apply(ins, outs, S, stream=stream)
+                    else:
+                        graphs[spec].replay()
+                    e1.record()
+                    torch.cuda.synchronize()
+                clocks.setdefault(spec, []).append(clk.summary())
                 times[spec].append(e0.elapsed_time(e1) / a.steps)
                 if rnd == a.rounds - 1:
                     out.zero_()
@@ -115,7 +120,8 @@ def main():
                                       "ms_all": [round(x, 5) for x in times[spec]],
                                       "moved_GBps": moved / ms / 1e6, "source_GBps": wl.k * sym / ms / 1e6,
                                       "frac_of_6452.8": moved / ms / 1e6 / 6452.8, "matches_first": dg == ref,
-                                      "graph": not a.no_graph}), flush=True)
+                                      "graph": not a.no_graph,
+                                      "clocks": [(c["sm_mhz"], c["reasons"]) for c in clocks[spec]]}), flush=True)
             except Exception as e:  # keep sweeping
                 print(json.dumps({"variant": spec, "error": str(e)[:300]}), flush=True)
                 times[spec] = times[spec] or [float("nan")]
