@@ -121,7 +121,7 @@ def main():
                                       "moved_GBps": moved / ms / 1e6, "source_GBps": wl.k * sym / ms / 1e6,
                                       "frac_of_6452.8": moved / ms / 1e6 / 6452.8, "matches_first": dg == ref,
                                       "graph": not a.no_graph,
-                                      "clocks": [(c["sm_mhz"], c["reasons"]) for c in clocks[spec]]}), flush=True)
+                                      "clocks": [(c["sm_mhz"], c["power_w_median"], c["reasons"]) for c in clocks[spec]]}), flush=True)
             except Exception as e:  # keep sweeping
                 print(json.dumps({"variant": spec, "error": str(e)[:300]}), flush=True)
                 times[spec] = times[spec] or [float("nan")]
