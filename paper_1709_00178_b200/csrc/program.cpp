@@ -161,10 +161,10 @@ const TunedEntry* find_tuned(const std::string& key) {
                 while (std::fgets(line, sizeof line, fh)) {
                     if (line[0] == '#' || line[0] == '\n') continue;
                     char k[128];
-                    unsigned parts = 0, pg = 0;
+                    unsigned parts = 0, pg = 0, threads = 0;
                     int cse = -1;
-                    if (std::sscanf(line, "%127s %u %u %d", k, &parts, &pg, &cse) == 4)
-                        g_tuned.push_back(TunedEntry{k, parts, pg, cse});
+                    const int got = std::sscanf(line, "%127s %u %u %d %u", k, &parts, &pg, &cse, &threads);
+                    if (got >= 4) g_tuned.push_back(TunedEntry{k, parts, pg, cse, got == 5 ? threads : 0u});
                 }
                 std::fclose(fh);
             }
@@ -329,6 +329,10 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
             return v ? std::atoi(v) : -1;
         };
         const TunedEntry* tuned = find_tuned(plan_key(p));
+        p.staged_threads = opt.staged_threads;
+        if (!p.staged_threads && env_u("PYRIT_B200_THREADS") > 0)
+            p.staged_threads = static_cast<std::uint32_t>(env_u("PYRIT_B200_THREADS"));
+        if (!p.staged_threads && tuned) p.staged_threads = tuned->threads;
         std::uint32_t R = opt.parts;
         if (!R && env_u("PYRIT_B200_PARTS") > 0) R = static_cast<std::uint32_t>(env_u("PYRIT_B200_PARTS"));
         if (!R && tuned) R = tuned->parts;
@@ -433,7 +437,9 @@ KernelShape staged_shape(const Program& p, std::uint32_t smem_limit) {
     // cap); part r owns 256/R consumer threads, one 4-byte column word each,
     // so a strip tile is 1024/R bytes.  The shared-memory ring holds one
     // fragment group of one tile per slot.
-    for (std::uint32_t threads : {256u, 128u}) {
+    std::vector<std::uint32_t> choices = {256u, 128u};
+    if (p.staged_threads) choices.insert(choices.begin(), p.staged_threads);
+    for (std::uint32_t threads : choices) {
         if (threads % R) continue;
         const std::uint32_t tile = 4 * (threads / R);
         if (tile < 64) continue;

@@ -57,6 +57,7 @@ struct Program {
     // computes rows [part_row0[r], part_row0[r] + parts[r].rows)
     std::vector<Program> parts;
     std::vector<std::uint32_t> part_row0;
+    std::uint32_t staged_threads = 0; // staged CTA size override (0 = 256)
     ProgramStats stats;
 };
 
@@ -67,6 +68,7 @@ struct CompileOptions {
     std::uint32_t parts = 0;   // output parts for the staged kernel: 0 auto, 1 = do not split
     std::uint32_t part_group = 0; // fragment group of the parts: 0 auto
     std::uint32_t max_temps = 0;  // cap on shared pair temporaries per group (0 = no cap)
+    std::uint32_t staged_threads = 0; // staged CTA size (0 = tuned table / 256)
 };
 
 // Measured staged-kernel choices for specific programs (tuned.tsv):
@@ -75,6 +77,7 @@ struct TunedEntry {
     std::string key;
     std::uint32_t parts = 1, part_group = 1;
     int part_cse = 0;
+    std::uint32_t threads = 0; // staged CTA size (0 = default)
 };
 std::string plan_key(const Program& p); // field + transform + ring representatives
 void set_tuned_path(const std::string& path);
