@@ -6,27 +6,27 @@
  *
  *   reference (C++, header only)                    here
  *   ----------------------------------------------  -------------------------------
- *   FieldSpec            field.hpp:116-137          pyrit_field
- *   CodeSpec             matrix.hpp:263-270         pyrit_code
- *   cauchy_parity_matrix matrix.hpp:301-327         pyrit_cauchy_parity_matrix
- *   decode_matrix        matrix.hpp:440-467         pyrit_decode_matrix
+ *   FieldSpec            field.hpp:30-51          pyrit_field
+ *   CodeSpec             matrix.hpp:16-23         pyrit_code
+ *   cauchy_parity_matrix matrix.hpp:54-80         pyrit_cauchy_parity_matrix
+ *   decode_matrix        matrix.hpp:193-220         pyrit_decode_matrix
  *   sparse_transform     ring.hpp:77-90             pyrit_sparse_transform
  *   compile_schedule     schedule.hpp:94-163        pyrit_plan_create (+ _encode/_decode)
  *   schedule_stats       schedule.hpp:216-223       pyrit_plan_get_stats
- *   replay / parallel_replay codec.hpp:375-450      pyrit_cu_apply
- *   encode               codec.hpp:469-477          pyrit_cu_encode   (device buffers)
+ *   replay / parallel_replay codec.hpp:118-193      pyrit_cu_apply
+ *   encode               codec.hpp:212-220          pyrit_cu_encode   (device buffers)
  *                                                    pyrit_encode_host (host buffers)
- *   decode               codec.hpp:498-541          pyrit_cu_decode   (device buffers)
+ *   decode               codec.hpp:241-284          pyrit_cu_decode   (device buffers)
  *                                                    pyrit_decode_host (host buffers)
- *   Errc / Error         errors.hpp:57-84           return codes, pyrit_strerror
+ *   Errc / Error         errors.hpp:12-39           return codes, pyrit_strerror
  *
  * Symbols are bit-sliced exactly as SymbolBuffer stores them
- * (codec.hpp:281-330): a symbol of symbol_size bytes is w contiguous strips
+ * (codec.hpp:24-73): a symbol of symbol_size bytes is w contiguous strips
  * of symbol_size / w bytes, strip i holding coefficient i of every bit
  * column.  symbol_size must be a positive multiple of w and of 8
- * (codec.hpp:285-287).
+ * (codec.hpp:28-30).
  *
- * Return codes: 0 ok; 1 + Errc (1..11, errors.hpp:57-69) for argument,
+ * Return codes: 0 ok; 1 + Errc (1..11, errors.hpp:12-24) for argument,
  * shape and algebra errors; negative for device failures: -e for a
  * cudaError_t e, -1000 - r for an nvrtcResult r, -2000 - r for a driver
  * CUresult r.  Nothing throws across this boundary.
@@ -49,22 +49,22 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-/* field.hpp:116-137 (ring elements widened: n <= 32, any p | x^n + 1) */
+/* field.hpp:30-51 (ring elements widened: n <= 32, any p | x^n + 1) */
 typedef struct pyrit_field {
     uint32_t w;       /* extension degree, elements are w-bit (<= 16) */
     uint32_t n;       /* ring length, w < n <= 32 */
-    uint32_t kind;    /* 0 = Aop, 1 = Esp (FieldKind, field.hpp:100-103) */
+    uint32_t kind;    /* 0 = Aop, 1 = Esp (FieldKind, field.hpp:14-17) */
     uint32_t s;       /* coefficient spacing */
     uint32_t r_esp;   /* degree of the ESP base polynomial (w for AOP) */
     uint32_t modulus; /* p(x), bit i = coefficient of x^i */
 } pyrit_field;
 
-/* matrix.hpp:263-270 */
+/* matrix.hpp:16-23 */
 typedef struct pyrit_code {
     uint32_t k;         /* data symbols */
     uint32_t r;         /* parity symbols */
     pyrit_field field;
-    uint32_t transform; /* 0 = Embedding, 1 = Parity (transform.hpp:142) */
+    uint32_t transform; /* 0 = Embedding, 1 = Parity (transform.hpp:24) */
 } pyrit_code;
 
 /* schedule.hpp:61-67 ScheduleStats, extended with the fused-program counts */
@@ -84,16 +84,16 @@ typedef struct pyrit_plan pyrit_plan;
 const char* pyrit_version(void);
 const char* pyrit_strerror(int code);
 
-/* FieldSpec::gf16_aop / gf64_esp (field.hpp:124-129) and the BASELINE fields */
+/* FieldSpec::gf16_aop / gf64_esp (field.hpp:38-43) and the BASELINE fields */
 int pyrit_field_named(const char* name, pyrit_field* out); /* "gf16", "gf64", "gf256_r17", "gf1024", "gf4096" */
 int pyrit_field_validate(const pyrit_field* f);
-int pyrit_gf_mul(const pyrit_field* f, uint32_t a, uint32_t b, uint32_t* out);   /* field.hpp:154 */
-int pyrit_gf_inv(const pyrit_field* f, uint32_t a, uint32_t* out);               /* field.hpp:168 */
+int pyrit_gf_mul(const pyrit_field* f, uint32_t a, uint32_t b, uint32_t* out);   /* field.hpp:68 */
+int pyrit_gf_inv(const pyrit_field* f, uint32_t a, uint32_t* out);               /* field.hpp:82 */
 int pyrit_sparse_transform(const pyrit_field* f, uint32_t u, uint32_t* rep);     /* ring.hpp:77 */
 int pyrit_fold_table(const pyrit_field* f, uint32_t* fold /* n - w entries */);  /* x^t mod p */
-/* out: r x k row-major (matrix.hpp:301) */
+/* out: r x k row-major (matrix.hpp:54) */
 int pyrit_cauchy_parity_matrix(const pyrit_code* code, uint16_t* out);
-/* out: (#erased data) x k rows of A^-1, survivors in given order (matrix.hpp:440) */
+/* out: (#erased data) x k rows of A^-1, survivors in given order (matrix.hpp:193) */
 int pyrit_decode_matrix(const pyrit_code* code, const uint32_t* survivors, uint16_t* out, uint32_t* rows);
 /* fused repair matrix: survivors (k, lowest index first), outputs (erased,
  * data then parity, each ascending), matrix outputs x k */
@@ -125,16 +125,16 @@ int pyrit_plan_interpret(const pyrit_plan* plan, const uint8_t* const* in, uint8
 void pyrit_plan_destroy(pyrit_plan* plan);
 
 /* ---- device path ------------------------------------------------------ */
-/* replay (codec.hpp:375): window [off, off+len) of every strip; in[j] /
+/* replay (codec.hpp:118): window [off, off+len) of every strip; in[j] /
  * out[i] are device base pointers of the input / output symbols */
 int pyrit_cu_apply(const pyrit_plan* plan, const uint8_t* const* in, uint8_t* const* out, uint64_t strip_bytes,
                    uint64_t off, uint64_t len, void* stream);
 /* compile + load the plan's kernel for the current device (no launch) */
 int pyrit_cu_prepare(const pyrit_plan* plan);
-/* encode (codec.hpp:469): data[k], parity[r] device symbol pointers */
+/* encode (codec.hpp:212): data[k], parity[r] device symbol pointers */
 int pyrit_cu_encode(const pyrit_code* code, const uint8_t* const* data, uint8_t* const* parity,
                     uint64_t symbol_size, void* stream);
-/* decode (codec.hpp:498): symbols[k + r] device pointers, repaired in place */
+/* decode (codec.hpp:241): symbols[k + r] device pointers, repaired in place */
 int pyrit_cu_decode(const pyrit_code* code, uint8_t* const* symbols, const uint32_t* erased, uint32_t n_erased,
                     uint64_t symbol_size, void* stream);
 

@@ -1,9 +1,9 @@
 // pyrit_b200_shim.hpp -- drop-in GPU replacements for the reference codec's
 // top-level calls, written against the reference's OWN types.
 //
-//   pyrit::encode(data, code, threads)          codec.hpp:469-477
+//   pyrit::encode(data, code, threads)          codec.hpp:212-220
 //     -> pyrit::cuda::encode(data, code, device)
-//   pyrit::decode(symbols, erased, code, threads) codec.hpp:498-541
+//   pyrit::decode(symbols, erased, code, threads) codec.hpp:241-284
 //     -> pyrit::cuda::decode(symbols, erased, code, device)
 //
 // Include after the reference headers (it needs SymbolBuffer, CodeSpec,
@@ -39,24 +39,24 @@ inline pyrit_code to_c(const CodeSpec& code) {
     return c;
 }
 
-// 1 + Errc -> pyrit::Error (errors.hpp:57-84); negative -> device failure
+// 1 + Errc -> pyrit::Error (errors.hpp:12-39); negative -> device failure
 inline void check(int rc) {
     if (rc == 0) return;
     if (rc >= 1 && rc <= 11) throw Error(static_cast<Errc>(rc - 1), pyrit_strerror(rc));
     throw std::runtime_error(std::string("pyrit_b200: ") + pyrit_strerror(rc));
 }
 
-// codec.hpp:469 encode(): parity = C * data, on the GPU (host buffers in,
+// codec.hpp:212 encode(): parity = C * data, on the GPU (host buffers in,
 // host buffers out; H2D, fused ring kernel and D2H are pipelined inside).
 inline SymbolBuffer encode(const SymbolBuffer& data, const CodeSpec& code, int device = 0) {
-    check_data_shape(data, code); // codec.hpp:462-466, the reference's own validation
+    check_data_shape(data, code); // codec.hpp:205-209, the reference's own validation
     SymbolBuffer parity(code.r, data.symbol_size(), code.field);
     const pyrit_code c = to_c(code);
     if (code.r) check(pyrit_encode_host(&c, data.symbol(0), parity.symbol(0), data.symbol_size(), device));
     return parity;
 }
 
-// codec.hpp:498 decode(): in-place repair of the listed symbols from any k
+// codec.hpp:241 decode(): in-place repair of the listed symbols from any k
 // survivors (lowest index first), one fused pass on the GPU.
 inline void decode(SymbolBuffer& symbols, const std::vector<unsigned>& erased, const CodeSpec& code,
                    int device = 0) {

@@ -26,7 +26,7 @@ u64p = C.POINTER(C.c_uint64)
 
 @dataclass(frozen=True)
 class Field:
-    """FieldSpec (field.hpp:116-137), ring elements widened to 32 bits."""
+    """FieldSpec (field.hpp:30-51), ring elements widened to 32 bits."""
     w: int
     n: int
     kind: int  # 0 Aop, 1 Esp
@@ -35,8 +35,8 @@ class Field:
     modulus: int
 
 
-GF16 = Field(4, 5, 0, 1, 4, 0x1F)        # FieldSpec::gf16_aop (field.hpp:124-126)
-GF64 = Field(6, 9, 1, 3, 2, 0x49)        # FieldSpec::gf64_esp (field.hpp:127-129)
+GF16 = Field(4, 5, 0, 1, 4, 0x1F)        # FieldSpec::gf16_aop (field.hpp:38-40)
+GF64 = Field(6, 9, 1, 3, 2, 0x49)        # FieldSpec::gf64_esp (field.hpp:41-43)
 GF256_R17 = Field(8, 17, 0, 1, 8, 0x139)  # BASELINE configs 2 and 4
 GF1024 = Field(10, 11, 0, 1, 10, 0x7FF)   # BASELINE config 3
 GF4096 = Field(12, 13, 0, 1, 12, 0x1FFF)  # BASELINE config 5
@@ -192,7 +192,7 @@ def ring_replay(f: Field, m, ins, strip, kind=0, off=0, length=None, outs=None, 
 
 
 def decode(k, r, f: Field, symbols, erased, strip, kind=0, off=0, length=None):
-    """codec.hpp:498-541 restated in place over k + r symbol arrays."""
+    """codec.hpp:241-284 restated in place over k + r symbol arrays."""
     length = strip - off if length is None else length
     er = np.asarray(sorted(erased) if False else list(erased), dtype=np.uint32)
     rc = lib().or_decode(k, r, f.w, f.n, f.s, f.modulus, kind, _ptrs(symbols), er.ctypes.data_as(u32p),

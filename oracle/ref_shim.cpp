@@ -7,7 +7,7 @@
 // reference's own CPU path.  Output: oracle/_ref/libpyrit_ref.so.
 //
 // Every function forwards to the reference symbol named in its comment;
-// pyrit::Error is mapped to 1 + Errc (errors.hpp:57-69).
+// pyrit::Error is mapped to 1 + Errc (errors.hpp:12-24).
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -48,7 +48,7 @@ FieldMatrix make_matrix(const FieldSpec& spec, unsigned rows, unsigned cols, con
 
 } // namespace
 
-// field.hpp:154 gf_mul / :168 gf_inv
+// field.hpp:68 gf_mul / :168 gf_inv
 REF_EXPORT std::uint32_t ref_gf_mul(std::uint32_t a, std::uint32_t b, unsigned w, unsigned n,
                                     std::uint32_t modulus) {
     return gf_mul(static_cast<FieldElem>(a), static_cast<FieldElem>(b),
@@ -60,7 +60,7 @@ REF_EXPORT std::uint32_t ref_gf_inv(std::uint32_t a, unsigned w, unsigned n, std
     return out;
 }
 
-// ring.hpp:24 ring_mul, :77 sparse_transform, transform.hpp:157 phi_E_inv
+// ring.hpp:24 ring_mul, :77 sparse_transform, transform.hpp:39 phi_E_inv
 REF_EXPORT std::uint32_t ref_ring_mul(std::uint32_t a, std::uint32_t b, unsigned w, unsigned n,
                                       std::uint32_t modulus) {
     return ring_mul(static_cast<RingElem>(a), static_cast<RingElem>(b),
@@ -75,7 +75,7 @@ REF_EXPORT std::uint32_t ref_phi_E_inv(std::uint32_t a, unsigned w, unsigned n, 
     return phi_E_inv(static_cast<RingElem>(a), make_field(w, n, kind, s, r_esp, modulus));
 }
 
-// matrix.hpp:301 cauchy_parity_matrix
+// matrix.hpp:54 cauchy_parity_matrix
 REF_EXPORT int ref_cauchy(unsigned k, unsigned r, unsigned w, unsigned n, std::uint32_t modulus,
                           std::uint16_t* out) {
     return guarded([&] {
@@ -84,7 +84,7 @@ REF_EXPORT int ref_cauchy(unsigned k, unsigned r, unsigned w, unsigned n, std::u
     });
 }
 
-// matrix.hpp:343 invert
+// matrix.hpp:96 invert
 REF_EXPORT int ref_invert(unsigned dim, unsigned w, unsigned n, std::uint32_t modulus,
                           const std::uint16_t* in, std::uint16_t* out) {
     return guarded([&] {
@@ -93,7 +93,7 @@ REF_EXPORT int ref_invert(unsigned dim, unsigned w, unsigned n, std::uint32_t mo
     });
 }
 
-// matrix.hpp:440 decode_matrix
+// matrix.hpp:193 decode_matrix
 REF_EXPORT int ref_decode_matrix(unsigned k, unsigned r, unsigned w, unsigned n, std::uint32_t modulus,
                                  const std::uint32_t* survivors, std::uint16_t* out,
                                  unsigned* rows_out) {
@@ -148,7 +148,7 @@ REF_EXPORT int ref_oracle_apply(unsigned w, unsigned n, unsigned kind, unsigned 
     });
 }
 
-// codec.hpp:469 encode (ring) and :480 encode_crs, whole symbols
+// codec.hpp:212 encode (ring) and :480 encode_crs, whole symbols
 REF_EXPORT int ref_encode(unsigned w, unsigned n, unsigned kind, unsigned s, unsigned r_esp,
                           std::uint32_t modulus, unsigned k, unsigned r, unsigned transform,
                           unsigned crs, const std::uint8_t* data, std::uint64_t symbol_size,
@@ -163,7 +163,7 @@ REF_EXPORT int ref_encode(unsigned w, unsigned n, unsigned kind, unsigned s, uns
     });
 }
 
-// codec.hpp:498 decode, in place over k + r contiguous symbols
+// codec.hpp:241 decode, in place over k + r contiguous symbols
 REF_EXPORT int ref_decode(unsigned w, unsigned n, unsigned kind, unsigned s, unsigned r_esp,
                           std::uint32_t modulus, unsigned k, unsigned r, unsigned transform,
                           std::uint8_t* symbols, std::uint64_t symbol_size, const unsigned* erased,
@@ -183,7 +183,7 @@ REF_EXPORT int ref_decode(unsigned w, unsigned n, unsigned kind, unsigned s, uns
 // does (schedule compiled once, buffers preallocated, parallel_replay timed).
 // mode 0: encode with the ring schedule (compile_schedule, schedule.hpp:94)
 // mode 1: encode with the CRS schedule  (compile_crs_schedule, schedule.hpp:168)
-// mode 2: decode (codec.hpp:498-541 restated with CRS schedules): erased data
+// mode 2: decode (codec.hpp:241-284 restated with CRS schedules): erased data
 //         via decode_matrix, then erased parity re-encoded from data.
 // mode 3: decode, same two passes with ring schedules (the reference's own
 //         decode(); valid for the AOP/ESP fields only).

@@ -5,7 +5,7 @@ Names, argument meaning and errors follow the reference library
 by libpyrit_b200.so (C++ host algebra + generated sm_100a kernels) through the
 C ABI in include/pyrit_b200.h.  Device entry points take CUDA torch tensors;
 host entry points take numpy arrays laid out like SymbolBuffer
-(codec.hpp:281-330: symbols contiguous, each w strips of symbol_size/w bytes).
+(codec.hpp:24-73: symbols contiguous, each w strips of symbol_size/w bytes).
 """
 from __future__ import annotations
 
@@ -26,7 +26,7 @@ __all__ = [
 ]
 
 
-class TransformKind(enum.IntEnum):  # transform.hpp:142
+class TransformKind(enum.IntEnum):  # transform.hpp:24
     Embedding = 0
     Parity = 1
 
@@ -42,7 +42,7 @@ def choose_transform(k: int, r: int) -> TransformKind:  # schedule.hpp:71-73
 
 @dataclass(frozen=True)
 class FieldSpec:
-    """field.hpp:116-137; ring elements are 32-bit so R_{2,17} is representable."""
+    """field.hpp:30-51; ring elements are 32-bit so R_{2,17} is representable."""
     w: int
     n: int
     kind: int = 0
@@ -51,11 +51,11 @@ class FieldSpec:
     modulus: int = 0
 
     @staticmethod
-    def gf16_aop() -> "FieldSpec":  # field.hpp:124-126
+    def gf16_aop() -> "FieldSpec":  # field.hpp:38-40
         return FieldSpec(4, 5, 0, 1, 4, 0b11111)
 
     @staticmethod
-    def gf64_esp() -> "FieldSpec":  # field.hpp:127-129
+    def gf64_esp() -> "FieldSpec":  # field.hpp:41-43
         return FieldSpec(6, 9, 1, 3, 2, 0b001001001)
 
     @staticmethod
@@ -63,7 +63,7 @@ class FieldSpec:
         return FieldSpec(8, 17, 0, 1, 8, 0x139)
 
     @staticmethod
-    def aop(w: int) -> "FieldSpec":  # all-one p of degree w in R_{2,w+1} (field.hpp:189-218)
+    def aop(w: int) -> "FieldSpec":  # all-one p of degree w in R_{2,w+1} (field.hpp:103-132)
         return FieldSpec(w, w + 1, 0, 1, w, (1 << (w + 1)) - 1)
 
     def c(self) -> L.pyrit_field:
@@ -75,7 +75,7 @@ class FieldSpec:
 
 @dataclass(frozen=True)
 class CodeSpec:
-    """matrix.hpp:263-270."""
+    """matrix.hpp:16-23."""
     k: int
     r: int
     field: FieldSpec
@@ -93,13 +93,13 @@ def _u32(x) -> C.c_uint32:
     return C.c_uint32(x)
 
 
-def gf_mul(a: int, b: int, f: FieldSpec) -> int:  # field.hpp:154
+def gf_mul(a: int, b: int, f: FieldSpec) -> int:  # field.hpp:68
     out = C.c_uint32()
     L.check(_clib().pyrit_gf_mul(C.byref(f.c()), a, b, C.byref(out)))
     return out.value
 
 
-def gf_inv(a: int, f: FieldSpec) -> int:  # field.hpp:168
+def gf_inv(a: int, f: FieldSpec) -> int:  # field.hpp:82
     out = C.c_uint32()
     L.check(_clib().pyrit_gf_inv(C.byref(f.c()), a, C.byref(out)))
     return out.value
@@ -117,13 +117,13 @@ def fold_table(f: FieldSpec) -> list[int]:
     return list(out[: f.n - f.w])
 
 
-def cauchy_parity_matrix(code: CodeSpec) -> np.ndarray:  # matrix.hpp:301-327
+def cauchy_parity_matrix(code: CodeSpec) -> np.ndarray:  # matrix.hpp:54-80
     out = np.zeros(max(code.r * code.k, 1), dtype=np.uint16)
     L.check(_clib().pyrit_cauchy_parity_matrix(C.byref(code.c()), out.ctypes.data))
     return out[: code.r * code.k].reshape(code.r, code.k)
 
 
-def decode_matrix(code: CodeSpec, survivors: Sequence[int]) -> np.ndarray:  # matrix.hpp:440-467
+def decode_matrix(code: CodeSpec, survivors: Sequence[int]) -> np.ndarray:  # matrix.hpp:193-220
     surv = np.asarray(survivors, dtype=np.uint32)
     if surv.size != code.k:
         raise PyritError(11, "need exactly k survivors")
@@ -219,7 +219,7 @@ class Plan:
 
     def apply(self, in_ptrs: Sequence[int], out_ptrs: Sequence[int], strip: int, off: int = 0,
               length: int | None = None, stream: int | None = None) -> None:
-        """replay (codec.hpp:375) over device pointers, asynchronously on `stream`."""
+        """replay (codec.hpp:118) over device pointers, asynchronously on `stream`."""
         length = strip - off if length is None else length
         L.check(_clib().pyrit_cu_apply(self._h, _ptr_array(list(in_ptrs)), _ptr_array(list(out_ptrs)), strip, off,
                                       length, stream))
@@ -257,7 +257,7 @@ def _rows(t) -> list[int]:
 
 
 def encode(data, code: CodeSpec):
-    """encode (codec.hpp:469-477): data is a (k, symbol_size) uint8 CUDA tensor; returns (r, symbol_size)."""
+    """encode (codec.hpp:212-220): data is a (k, symbol_size) uint8 CUDA tensor; returns (r, symbol_size)."""
     import torch
     if data.dim() != 2 or data.shape[0] != code.k or data.dtype != torch.uint8 or not data.is_cuda:
         raise PyritError(4, "data buffer does not match the code")
@@ -269,7 +269,7 @@ def encode(data, code: CodeSpec):
 
 
 def decode(symbols, erased: Iterable[int], code: CodeSpec) -> None:
-    """decode (codec.hpp:498-541), in place on a (k + r, symbol_size) uint8 CUDA tensor."""
+    """decode (codec.hpp:241-284), in place on a (k + r, symbol_size) uint8 CUDA tensor."""
     import torch
     if symbols.dim() != 2 or symbols.shape[0] != code.k + code.r or symbols.dtype != torch.uint8:
         raise PyritError(4, "symbol buffer does not match the code")

@@ -34,7 +34,7 @@ SOURCE_STAGED = 100
 
 
 class PyritError(RuntimeError):
-    """Mirror of pyrit::Error (errors.hpp:71-80): carries the Errc name/code."""
+    """Mirror of pyrit::Error (errors.hpp:26-35): carries the Errc name/code."""
 
     def __init__(self, rc: int, msg: str):
         self.rc = rc

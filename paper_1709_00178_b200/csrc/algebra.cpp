@@ -193,7 +193,7 @@ Matrix decode_matrix(std::uint32_t k, std::uint32_t r, const Field& f, const Mat
 
 RepairPlan repair_matrix(std::uint32_t k, std::uint32_t r, const Field& f,
                          const std::vector<std::uint32_t>& erased) {
-    // validation mirrors decode (codec.hpp:500-512)
+    // validation mirrors decode (codec.hpp:243-255)
     if (k == 0) raise(Errc::InvalidArgument, "k must be at least 1");
     if (k + r > f.field_size()) raise(Errc::TooManySymbols, "k + r exceeds field size");
     std::vector<bool> gone(k + r, false);

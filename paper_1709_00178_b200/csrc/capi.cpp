@@ -60,14 +60,14 @@ Field to_field(const pyrit_field* f) {
 
 void check_code(const pyrit_code* c) {
     if (!c) raise(Errc::InvalidArgument, "null code");
-    if (c->k == 0) raise(Errc::InvalidArgument, "k must be at least 1");          // matrix.hpp:272-273
+    if (c->k == 0) raise(Errc::InvalidArgument, "k must be at least 1");          // matrix.hpp:25-26
     if (c->transform > 1) raise(Errc::InvalidArgument, "unknown transform");
     const Field f = to_field(&c->field);
     if (c->k + c->r > f.field_size()) raise(Errc::TooManySymbols, "k + r exceeds field size"); // :274-277
 }
 
 std::uint64_t strip_of(const pyrit_code* c, std::uint64_t symbol_size) {
-    // SymbolBuffer shape rule, codec.hpp:285-287
+    // SymbolBuffer shape rule, codec.hpp:28-30
     if (symbol_size == 0 || symbol_size % c->field.w != 0 || symbol_size % 8 != 0)
         raise(Errc::BufferShape, "symbol size must be a positive multiple of w and of the word width");
     return symbol_size / c->field.w;
@@ -176,8 +176,8 @@ int pyrit_field_named(const char* name, pyrit_field* out) {
     return guarded([&] {
         if (!name || !out) raise(Errc::InvalidArgument, "null argument");
         const std::string n = name;
-        if (n == "gf16") *out = pyrit_field{4, 5, 0, 1, 4, 0x1F};          // field.hpp:124-126
-        else if (n == "gf64") *out = pyrit_field{6, 9, 1, 3, 2, 0x49};     // field.hpp:127-129
+        if (n == "gf16") *out = pyrit_field{4, 5, 0, 1, 4, 0x1F};          // field.hpp:38-40
+        else if (n == "gf64") *out = pyrit_field{6, 9, 1, 3, 2, 0x49};     // field.hpp:41-43
         else if (n == "gf256_r17") *out = pyrit_field{8, 17, 0, 1, 8, 0x139};
         else if (n == "gf1024") *out = pyrit_field{10, 11, 0, 1, 10, 0x7FF};
         else if (n == "gf4096") *out = pyrit_field{12, 13, 0, 1, 12, 0x1FFF};

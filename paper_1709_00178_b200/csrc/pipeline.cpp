@@ -1,5 +1,5 @@
 // Host-buffer path: the end-to-end encode()/decode() a reference user calls
-// with SymbolBuffer-resident bytes (codec.hpp:469, :498).  Strips are moved
+// with SymbolBuffer-resident bytes (codec.hpp:212, :241).  Strips are moved
 // in column chunks through a ring of device staging slots, one stream per
 // slot, so the H2D copy of chunk c+1, the fused kernel of chunk c and the
 // D2H copy of chunk c-1 overlap on the two copy engines and the SMs.

@@ -1,6 +1,6 @@
 """The C-ABI library on a machine without a GPU: it loads, exports every entry
 point include/pyrit_b200.h declares, and its host-only entry points behave
-(error codes mirror Errc, errors.hpp:57-69).  No device calls here."""
+(error codes mirror Errc, errors.hpp:12-24).  No device calls here."""
 import ctypes as C
 import os
 import re
@@ -62,7 +62,7 @@ def test_return_codes_are_errc_plus_one():
     f = L.pyrit_field()
     assert lib.pyrit_field_named(b"gf256_r17", C.byref(f)) == 0 and (f.w, f.n, f.modulus) == (8, 17, 0x139)
     assert lib.pyrit_field_named(b"nope", C.byref(f)) == 11
-    # symbol size rules of SymbolBuffer (codec.hpp:285-287) are checked before any device work
+    # symbol size rules of SymbolBuffer (codec.hpp:28-30) are checked before any device work
     code = L.pyrit_code(4, 2, L.pyrit_field(4, 5, 0, 1, 4, 0x1F), 0)
     ptrs = (C.c_void_p * 6)()
     assert lib.pyrit_cu_encode(C.byref(code), ptrs, ptrs, 12, None) == 4  # BufferShape (12 % 8)

@@ -179,7 +179,7 @@ def test_production_size_codes_random_patterns():
 
 
 def test_config4_fused_repair_matches_two_pass_reference_semantics():
-    """Fused rows (erased data of A^-1, then C_i A^-1) == decode()'s two passes (codec.hpp:526-540)."""
+    """Fused rows (erased data of A^-1, then C_i A^-1) == decode()'s two passes (codec.hpp:269-283)."""
     wl = WORKLOADS[4]
     f = wl.fld
     strip = 64

@@ -4,7 +4,7 @@ Full-size outputs are too large for the CPU oracle to recompute in seconds, so
 parity is checked through properties that do not depend on size:
   * windowed oracle: every strip's byte window [off, off+len) of the GPU output
     equals the oracle applied to the same window of the inputs (a window of an
-    encode is the encode of the window -- column independence, codec.hpp:416-450),
+    encode is the encode of the window -- column independence, codec.hpp:159-193),
     at the start, the middle and the end of the strips;
   * encode -> erase -> decode round trip on the GPU, compared byte for byte;
   * byte-offset shard invariance (2 and 8 shards == one launch), i.e. the

@@ -85,7 +85,7 @@ def test_config4_decode(cuda, erased):
     work[list(erased)] = 0xAA
     got = dev_decode(cuda, wl.code, work, erased)
     np.testing.assert_array_equal(got, full)
-    # and the C oracle's decode (codec.hpp:498 restated) agrees on a window
+    # and the C oracle's decode (codec.hpp:241 restated) agrees on a window
     work2 = full.copy()
     work2[list(erased)] = 0x55
     syms = [work2[i] for i in range(len(work2))]

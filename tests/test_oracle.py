@@ -54,7 +54,7 @@ def test_ring_kats():
 
 
 def test_fold_table_matches_reference_rule_for_aop_esp():
-    # transform.hpp:157-164: top coefficient w + j folds into every i with i % s == j
+    # transform.hpp:39-46: top coefficient w + j folds into every i with i % s == j
     for f in (O.GF16, O.GF64, O.GF1024, O.GF4096):
         fold = O.fold_table(f)
         for t in range(f.w, f.n):
