@@ -18,6 +18,10 @@
  *                                                    pyrit_encode_host (host buffers)
  *   decode               codec.hpp:241-284          pyrit_cu_decode   (device buffers)
  *                                                    pyrit_decode_host (host buffers)
+ *   (per-stripe calls)   container.hpp:207-218      pyrit_cu_encode_batch / _decode_batch
+ *   serialize/parse_header container.hpp:114-161    pyrit_header_serialize / _parse
+ *   encode_file          container.hpp:168-222      pyrit_encode_file
+ *   decode_file          container.hpp:249-299      pyrit_decode_file
  *   Errc / Error         errors.hpp:12-39           return codes, pyrit_strerror
  *
  * Symbols are bit-sliced exactly as SymbolBuffer stores them
@@ -138,6 +142,21 @@ int pyrit_cu_encode(const pyrit_code* code, const uint8_t* const* data, uint8_t*
 int pyrit_cu_decode(const pyrit_code* code, uint8_t* const* symbols, const uint32_t* erased, uint32_t n_erased,
                     uint64_t symbol_size, void* stream);
 
+/* ---- stripe batches (encode_file / decode_file call encode()/decode()
+ * once per stripe, container.hpp:207-218, :284-297; here one launch covers
+ * `stripes` stripes).  Input symbol j of stripe b is at in[j] + b * in_pitch,
+ * output i at out[i] + b * out_pitch; each symbol is w strips of
+ * strip_bytes (apply) or symbol_size / w (encode/decode) bytes. */
+int pyrit_cu_apply_batch(const pyrit_plan* plan, const uint8_t* const* in, uint8_t* const* out,
+                         uint64_t strip_bytes, uint64_t off, uint64_t len, uint64_t stripes, uint64_t in_pitch,
+                         uint64_t out_pitch, void* stream);
+int pyrit_cu_encode_batch(const pyrit_code* code, const uint8_t* const* data, uint8_t* const* parity,
+                          uint64_t symbol_size, uint64_t stripes, uint64_t data_pitch, uint64_t parity_pitch,
+                          void* stream);
+/* symbols[k + r]: symbol i of stripe b at symbols[i] + b * pitch, repaired in place */
+int pyrit_cu_decode_batch(const pyrit_code* code, uint8_t* const* symbols, const uint32_t* erased,
+                          uint32_t n_erased, uint64_t symbol_size, uint64_t stripes, uint64_t pitch, void* stream);
+
 /* ---- host-buffer path (end to end: H2D, fused kernel, D2H, pipelined) -- */
 /* data: k * symbol_size contiguous host bytes (SymbolBuffer layout);
  * parity: r * symbol_size host bytes.  Synchronous. Pinned buffers overlap. */
@@ -148,6 +167,36 @@ int pyrit_decode_host(const pyrit_code* code, uint8_t* symbols, const uint32_t* 
                       uint64_t symbol_size, int device);
 /* bytes per strip per pipeline chunk (0 = automatic) */
 int pyrit_set_host_chunk(uint64_t strip_chunk_bytes);
+
+/* ---- shard container and file codec (container.hpp) ------------------ */
+#define PYRIT_HEADER_SIZE 29 /* container.hpp:38 */
+/* container.hpp:57-84; serialized little-endian as container.hpp:16-36 */
+typedef struct pyrit_shard_header {
+    uint8_t version;   /* 1 */
+    uint8_t field;     /* field id (pyrit_field_id) */
+    uint8_t transform; /* 0 = Embedding, 1 = Parity */
+    uint16_t k, r, shard_index;
+    uint32_t symbol_size;
+    uint64_t original_length;
+} pyrit_shard_header;
+uint32_t pyrit_crc32(const uint8_t* bytes, size_t len);                         /* container.hpp:41-55 */
+int pyrit_header_serialize(const pyrit_shard_header* h, uint8_t* out /* 29 */); /* container.hpp:114-127 */
+int pyrit_header_parse(const uint8_t* bytes, size_t len, pyrit_shard_header* out); /* container.hpp:132-161 */
+/* header field ids: 0 = gf16_aop, 1 = gf64_esp (field.hpp:54-62), and for
+ * the fields the reference cannot record: 2 = GF(2^8) in R_{2,17} (0x139),
+ * 3 = GF(2^10) AOP, 4 = GF(2^12) AOP */
+int pyrit_field_id(const pyrit_field* f, uint8_t* id);
+int pyrit_field_from_id(uint8_t id, pyrit_field* out);
+/* "<out_dir>/<basename(input)>.sNNN.pyrit" (container.hpp:186-189) */
+int pyrit_shard_path(const char* input, const char* out_dir, uint32_t index, char* buf, size_t cap);
+/* encode_file (container.hpp:168-222): writes k + r shard files; batches of
+ * stripes go through `device` (pinned staging, three streams).  Synchronous. */
+int pyrit_encode_file(const pyrit_code* code, const char* input, const char* out_dir, uint32_t symbol_size,
+                      int device);
+/* decode_file (container.hpp:249-299) from any k (or more) shard files */
+int pyrit_decode_file(const char* const* shard_paths, uint32_t n_paths, const char* output, int device);
+/* source bytes per pipeline chunk of the file codec (0 = automatic) */
+int pyrit_set_file_chunk(uint64_t bytes);
 
 /* ---- synthetic inputs and verification digests ----------------------- */
 int pyrit_cu_fill(uint64_t seed, uint64_t frag, uint8_t* dst, uint64_t begin, uint64_t len, uint64_t valid,

@@ -5,6 +5,10 @@
 //     -> pyrit::cuda::encode(data, code, device)
 //   pyrit::decode(symbols, erased, code, threads) codec.hpp:241-284
 //     -> pyrit::cuda::decode(symbols, erased, code, device)
+//   pyrit::encode_file(input, out_dir, code, symbol_size) container.hpp:168-222
+//     -> pyrit::cuda::encode_file(input, out_dir, code, symbol_size, device)
+//   pyrit::decode_file(shard_paths, output)      container.hpp:249-299
+//     -> pyrit::cuda::decode_file(shard_paths, output, device)
 //
 // Include after the reference headers (it needs SymbolBuffer, CodeSpec,
 // Error from proj/include/pyrit/) and link libpyrit_b200.so.  Validation and
@@ -16,6 +20,7 @@
 // field oracle oracle_apply / encode_crs).
 #pragma once
 
+#include <filesystem>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -67,6 +72,30 @@ inline void decode(SymbolBuffer& symbols, const std::vector<unsigned>& erased, c
     std::vector<std::uint32_t> er(erased.begin(), erased.end());
     check(pyrit_decode_host(&c, symbols.symbol(0), er.data(), static_cast<std::uint32_t>(er.size()),
                             symbols.symbol_size(), device));
+}
+
+// container.hpp:168 encode_file(): same shard files (names, 29-byte headers,
+// stripe layout) as the reference; stripes go through the GPU in batches.
+inline std::vector<std::filesystem::path> encode_file(const std::filesystem::path& input,
+                                                      const std::filesystem::path& out_dir, const CodeSpec& code,
+                                                      std::uint32_t symbol_size, int device = 0) {
+    const pyrit_code c = to_c(code);
+    check(pyrit_encode_file(&c, input.c_str(), out_dir.c_str(), symbol_size, device));
+    std::vector<std::filesystem::path> paths;
+    char buf[4096];
+    for (unsigned i = 0; i < code.k + code.r; ++i) {
+        check(pyrit_shard_path(input.c_str(), out_dir.c_str(), i, buf, sizeof buf));
+        paths.emplace_back(buf);
+    }
+    return paths;
+}
+
+// container.hpp:249 decode_file(): rebuild the original file from any k shards.
+inline void decode_file(const std::vector<std::filesystem::path>& shard_paths, const std::filesystem::path& output,
+                        int device = 0) {
+    std::vector<const char*> ps;
+    for (const auto& p : shard_paths) ps.push_back(p.c_str());
+    check(pyrit_decode_file(ps.data(), static_cast<std::uint32_t>(ps.size()), output.c_str(), device));
 }
 
 } // namespace pyrit::cuda

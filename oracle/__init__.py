@@ -94,6 +94,8 @@ def ref():
         _ref.ref_plan_symbol.argtypes = [C.c_void_p, C.c_uint]
         _ref.ref_plan_run.argtypes = [C.c_void_p, C.c_uint]
         _ref.ref_plan_destroy.argtypes = [C.c_void_p]
+        _ref.ref_crc32.restype = C.c_uint32
+        _ref.ref_crc32.argtypes = [C.c_char_p, C.c_uint64]
     return _ref
 
 
@@ -328,3 +330,115 @@ class RefPlan:
 
     def __del__(self):
         self.close()
+
+
+# ------------------------------------------------ file codec (container.hpp)
+# Restated in Python over the C oracle's ring_replay/decode, one stripe at a
+# time exactly as the reference does (test sizes only).
+HEADER_SIZE = 29  # container.hpp:38
+_FIELD_IDS = {GF16: 0, GF64: 1, GF256_R17: 2, GF1024: 3, GF4096: 4}  # 0/1: field.hpp:54-62
+
+
+def crc32(b: bytes) -> int:
+    """container.hpp:41-55: reflected CRC-32, polynomial 0xEDB88320, init/xorout ~0."""
+    c = 0xFFFFFFFF
+    for x in b:
+        c ^= x
+        for _ in range(8):
+            c = (c >> 1) ^ (0xEDB88320 if c & 1 else 0)
+    return c ^ 0xFFFFFFFF
+
+
+def serialize_header(field_id, transform, k, r, index, symbol_size, length) -> bytes:
+    """container.hpp:114-127 (layout container.hpp:16-36, little endian)."""
+    b = (b"PYRT" + bytes([1, field_id, transform]) + k.to_bytes(2, "little") + r.to_bytes(2, "little")
+         + index.to_bytes(2, "little") + symbol_size.to_bytes(4, "little") + length.to_bytes(8, "little"))
+    return b + crc32(b).to_bytes(4, "little")
+
+
+def shard_name(input_path, index) -> str:  # container.hpp:186-189
+    return f"{os.path.basename(str(input_path))}.s{index:03d}.pyrit"
+
+
+def encode_file(input_path, out_dir, k, r, f: Field, symbol_size, kind=0) -> list[str]:
+    """container.hpp:168-222: stripes of k symbols, zero padded, encode() per stripe."""
+    data = np.fromfile(str(input_path), dtype=np.uint8)
+    length = data.size
+    stripe = k * symbol_size
+    stripes = 0 if length == 0 else -(-length // stripe)
+    padded = np.zeros(stripes * stripe, dtype=np.uint8)
+    padded[:length] = data
+    m = cauchy(k, r, f)
+    strip = symbol_size // f.w
+    payload = [[] for _ in range(k + r)]
+    for s in range(stripes):
+        ins = [padded[s * stripe + j * symbol_size: s * stripe + (j + 1) * symbol_size].copy() for j in range(k)]
+        outs = ring_replay(f, m, ins, strip, kind) if r else []
+        for j in range(k):
+            payload[j].append(ins[j])
+        for i in range(r):
+            payload[k + i].append(outs[i])
+    os.makedirs(str(out_dir), exist_ok=True)
+    paths = []
+    for i in range(k + r):
+        p = os.path.join(str(out_dir), shard_name(input_path, i))
+        with open(p, "wb") as fh:
+            fh.write(serialize_header(_FIELD_IDS[f], kind, k, r, i, symbol_size, length))
+            for sym in payload[i]:
+                fh.write(sym.tobytes())
+        paths.append(p)
+    return paths
+
+
+def decode_file(paths, output, k, r, f: Field, symbol_size, length, kind=0) -> None:
+    """container.hpp:249-299 for a consistent set (first occurrence of an index wins)."""
+    have = {}
+    for p in paths:
+        b = open(str(p), "rb").read()
+        idx = int.from_bytes(b[11:13], "little")
+        have.setdefault(idx, np.frombuffer(b[HEADER_SIZE:], dtype=np.uint8))
+    stripes = 0 if length == 0 else -(-length // (k * symbol_size))
+    erased = [i for i in range(k + r) if i not in have]
+    out = bytearray()
+    strip = symbol_size // f.w
+    for s in range(stripes):
+        syms = [have[i][s * symbol_size:(s + 1) * symbol_size].copy() if i in have
+                else np.zeros(symbol_size, np.uint8) for i in range(k + r)]
+        if erased:
+            decode(k, r, f, syms, erased, strip, kind)
+        for j in range(k):
+            out += syms[j].tobytes()
+    with open(str(output), "wb") as fh:
+        fh.write(bytes(out[:length]))
+
+
+def ref_encode_file(input_path, out_dir, k, r, f: Field, symbol_size, kind=0) -> None:
+    rc = ref().ref_encode_file(str(input_path).encode(), str(out_dir).encode(), *_fa(f), k, r, kind,
+                               C.c_uint32(symbol_size))
+    if rc:
+        raise OracleError(rc)
+
+
+def ref_decode_file(paths, output) -> None:
+    arr = (C.c_char_p * max(len(paths), 1))(*[str(p).encode() for p in paths])
+    rc = ref().ref_decode_file(arr, len(paths), str(output).encode())
+    if rc:
+        raise OracleError(rc)
+
+
+def ref_serialize_header(field_id, transform, k, r, index, symbol_size, length) -> bytes:
+    out = (C.c_uint8 * HEADER_SIZE)()
+    rc = ref().ref_serialize_header(field_id, transform, k, r, index, C.c_uint32(symbol_size),
+                                    C.c_uint64(length), out)
+    if rc:
+        raise OracleError(rc)
+    return bytes(out)
+
+
+def ref_parse_header(b: bytes):
+    buf = (C.c_uint8 * max(len(b), 1)).from_buffer_copy(b if b else b"\0")
+    out = (C.c_uint64 * 8)()
+    rc = ref().ref_parse_header(buf, C.c_uint64(len(b)), out)
+    if rc:
+        raise OracleError(rc)
+    return tuple(out)

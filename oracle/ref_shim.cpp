@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "pyrit/codec.hpp"
+#include "pyrit/container.hpp"
 #include "pyrit/matrix.hpp"
 #include "pyrit/schedule.hpp"
 
@@ -262,3 +263,60 @@ REF_EXPORT int ref_plan_run(void* plan, unsigned threads) {
 }
 
 REF_EXPORT void ref_plan_destroy(void* plan) { delete static_cast<RefPlan*>(plan); }
+
+// ---------------------------------------------------------------------------
+// Shard container and file codec (container.hpp), for pinning the GPU file
+// path byte for byte.  The reference's field_id() records any AOP field as
+// 0 (field.hpp:54-56), so only gf16_aop / gf64_esp shard sets round-trip.
+
+// container.hpp:114-127 serialize_header
+REF_EXPORT int ref_serialize_header(unsigned field, unsigned transform, unsigned k, unsigned r, unsigned index,
+                                    std::uint32_t symbol_size, std::uint64_t length, std::uint8_t* out) {
+    return guarded([&] {
+        ShardHeader h;
+        h.field = static_cast<std::uint8_t>(field);
+        h.transform = static_cast<std::uint8_t>(transform);
+        h.k = static_cast<std::uint16_t>(k);
+        h.r = static_cast<std::uint16_t>(r);
+        h.shard_index = static_cast<std::uint16_t>(index);
+        h.symbol_size = symbol_size;
+        h.original_length = length;
+        const auto b = serialize_header(h);
+        std::memcpy(out, b.data(), b.size());
+    });
+}
+
+// container.hpp:132-161 parse_header; fields out[0..7] =
+// version, field, transform, k, r, shard_index, symbol_size, original_length
+REF_EXPORT int ref_parse_header(const std::uint8_t* bytes, std::uint64_t len, std::uint64_t* out) {
+    return guarded([&] {
+        const ShardHeader h = parse_header(std::span<const std::uint8_t>(bytes, len));
+        const std::uint64_t v[8] = {h.version, h.field, h.transform, h.k, h.r, h.shard_index, h.symbol_size,
+                                    h.original_length};
+        std::memcpy(out, v, sizeof v);
+    });
+}
+
+// container.hpp:41-55
+REF_EXPORT std::uint32_t ref_crc32(const std::uint8_t* bytes, std::uint64_t len) {
+    return crc32(std::span<const std::uint8_t>(bytes, len));
+}
+
+// container.hpp:168-222 encode_file
+REF_EXPORT int ref_encode_file(const char* input, const char* out_dir, unsigned w, unsigned n, unsigned kind,
+                               unsigned s, unsigned r_esp, std::uint32_t modulus, unsigned k, unsigned r,
+                               unsigned transform, std::uint32_t symbol_size) {
+    return guarded([&] {
+        const CodeSpec code{k, r, make_field(w, n, kind, s, r_esp, modulus), static_cast<TransformKind>(transform)};
+        encode_file(input, out_dir, code, symbol_size);
+    });
+}
+
+// container.hpp:249-299 decode_file
+REF_EXPORT int ref_decode_file(const char* const* paths, unsigned n_paths, const char* output) {
+    return guarded([&] {
+        std::vector<std::filesystem::path> ps;
+        for (unsigned i = 0; i < n_paths; ++i) ps.emplace_back(paths[i]);
+        decode_file(ps, output);
+    });
+}

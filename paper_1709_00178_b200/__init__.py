@@ -22,7 +22,9 @@ from ._lib import PyritError
 __all__ = [
     "FieldSpec", "CodeSpec", "TransformKind", "RingRep", "PyritError", "Plan", "gf_mul", "gf_inv",
     "sparse_transform", "fold_table", "cauchy_parity_matrix", "decode_matrix", "repair_matrix", "encode",
-    "decode", "encode_host", "decode_host", "fill", "digest", "choose_transform",
+    "decode", "encode_host", "decode_host", "fill", "digest", "choose_transform", "encode_batch", "decode_batch",
+    "ShardHeader", "crc32", "serialize_header", "parse_header", "field_id", "field_from_id", "shard_path",
+    "encode_file", "decode_file", "HEADER_SIZE",
 ]
 
 
@@ -232,6 +234,14 @@ class Plan:
         L.check(_clib().pyrit_cu_last_launch(name, 128, C.byref(blocks), C.byref(threads)))
         return {"kernel": name.value.decode(), "blocks": blocks.value, "threads": threads.value}
 
+    def apply_batch(self, in_ptrs: Sequence[int], out_ptrs: Sequence[int], strip: int, stripes: int,
+                    in_pitch: int, out_pitch: int, off: int = 0, length: int | None = None,
+                    stream: int | None = None) -> None:
+        """`stripes` stripes in one launch: input j of stripe b at in_ptrs[j] + b * in_pitch."""
+        length = strip - off if length is None else length
+        L.check(_clib().pyrit_cu_apply_batch(self._h, _ptr_array(list(in_ptrs)), _ptr_array(list(out_ptrs)), strip,
+                                            off, length, stripes, in_pitch, out_pitch, stream))
+
     def prepare(self) -> None:
         L.check(_clib().pyrit_cu_prepare(self._h))
 
@@ -314,3 +324,112 @@ def digest(t, word_offset: int = 0, out=None, stream: int | None = None):
     L.check(_clib().pyrit_cu_digest(t.data_ptr(), t.numel(), word_offset, out.data_ptr(),
                                    _stream_of(t) if stream is None else stream))
     return out
+
+
+def encode_batch(data, code: CodeSpec, symbol_size: int):
+    """Stripe batch encode: data is a (stripes, k * symbol_size) uint8 CUDA tensor laid out
+    like the input file of encode_file (container.hpp:204-212: stripe = k symbols);
+    returns parity (r, stripes, symbol_size) -- shard order, one launch for all stripes."""
+    import torch
+    if data.dim() != 2 or data.shape[1] != code.k * symbol_size or data.dtype != torch.uint8 or not data.is_cuda:
+        raise PyritError(4, "data buffer does not match the code")
+    data = data.contiguous()
+    nb = data.shape[0]
+    parity = torch.empty((code.r, nb, symbol_size), dtype=torch.uint8, device=data.device)
+    base = data.data_ptr()
+    ins = [base + j * symbol_size for j in range(code.k)]
+    outs = [parity[i].data_ptr() for i in range(code.r)]
+    L.check(_clib().pyrit_cu_encode_batch(C.byref(code.c()), _ptr_array(ins), _ptr_array(outs), symbol_size, nb,
+                                         code.k * symbol_size, symbol_size, _stream_of(data)))
+    return parity
+
+
+def decode_batch(symbols, erased: Iterable[int], code: CodeSpec) -> None:
+    """Stripe batch repair in place: symbols is a (k + r, stripes, symbol_size) uint8 CUDA tensor."""
+    import torch
+    if symbols.dim() != 3 or symbols.shape[0] != code.k + code.r or symbols.dtype != torch.uint8:
+        raise PyritError(4, "symbol buffer does not match the code")
+    if not symbols.is_contiguous():
+        raise PyritError(4, "symbol buffer must be contiguous")
+    er = np.asarray(list(erased), dtype=np.uint32)
+    ss = symbols.shape[2]
+    L.check(_clib().pyrit_cu_decode_batch(C.byref(code.c()), _ptr_array(_rows(symbols)), er.ctypes.data, er.size,
+                                         ss, symbols.shape[1], ss, _stream_of(symbols)))
+
+
+# ---- shard container (container.hpp) -------------------------------------
+
+HEADER_SIZE = L.HEADER_SIZE
+
+
+@dataclass(frozen=True)
+class ShardHeader:
+    """container.hpp:57-84."""
+    version: int = 1
+    field: int = 0
+    transform: int = 0
+    k: int = 0
+    r: int = 0
+    shard_index: int = 0
+    symbol_size: int = 0
+    original_length: int = 0
+
+    def same_set(self, o: "ShardHeader") -> bool:  # container.hpp:70-74
+        return (self.version, self.field, self.transform, self.k, self.r, self.symbol_size,
+                self.original_length) == (o.version, o.field, o.transform, o.k, o.r, o.symbol_size,
+                                          o.original_length)
+
+    def stripe_count(self) -> int:  # container.hpp:80-83
+        sb = self.k * self.symbol_size
+        return 0 if sb == 0 else (self.original_length + sb - 1) // sb
+
+
+def crc32(data: bytes) -> int:  # container.hpp:41-55
+    buf = np.frombuffer(bytes(data), dtype=np.uint8)
+    return int(_clib().pyrit_crc32(buf.ctypes.data if buf.size else None, buf.size))
+
+
+def serialize_header(h: ShardHeader) -> bytes:  # container.hpp:114-127
+    out = (C.c_uint8 * HEADER_SIZE)()
+    ch = L.pyrit_shard_header(h.version, h.field, h.transform, h.k, h.r, h.shard_index, h.symbol_size,
+                              h.original_length)
+    L.check(_clib().pyrit_header_serialize(C.byref(ch), out))
+    return bytes(out)
+
+
+def parse_header(data: bytes) -> ShardHeader:  # container.hpp:132-161
+    buf = np.frombuffer(bytes(data), dtype=np.uint8)
+    ch = L.pyrit_shard_header()
+    L.check(_clib().pyrit_header_parse(buf.ctypes.data if buf.size else None, buf.size, C.byref(ch)))
+    return ShardHeader(*(getattr(ch, k) for k, _ in L.pyrit_shard_header._fields_))
+
+
+def field_id(f: FieldSpec) -> int:  # field.hpp:54-56 (+ ids 2..4 for the BASELINE fields)
+    out = C.c_uint8()
+    L.check(_clib().pyrit_field_id(C.byref(f.c()), C.byref(out)))
+    return out.value
+
+
+def field_from_id(i: int) -> FieldSpec:  # field.hpp:58-62
+    out = L.pyrit_field()
+    L.check(_clib().pyrit_field_from_id(i, C.byref(out)))
+    return FieldSpec(out.w, out.n, out.kind, out.s, out.r_esp, out.modulus)
+
+
+def shard_path(input_path: str, out_dir: str, index: int) -> str:  # container.hpp:186-189
+    buf = C.create_string_buffer(4096)
+    L.check(_clib().pyrit_shard_path(str(input_path).encode(), str(out_dir).encode(), index, buf, 4096))
+    return buf.value.decode()
+
+
+def encode_file(input_path, out_dir, code: CodeSpec, symbol_size: int, device: int = 0) -> list[str]:
+    """encode_file (container.hpp:168-222) through the GPU; returns the shard paths in index order."""
+    L.check(_clib().pyrit_encode_file(C.byref(code.c()), str(input_path).encode(), str(out_dir).encode(),
+                                     symbol_size, device))
+    return [shard_path(input_path, out_dir, i) for i in range(code.k + code.r)]
+
+
+def decode_file(shard_paths: Sequence, output, device: int = 0) -> None:
+    """decode_file (container.hpp:249-299) through the GPU."""
+    arr = (C.c_char_p * max(len(shard_paths), 1))(*[str(p).encode() for p in shard_paths])
+    L.check(_clib().pyrit_decode_file(arr, len(shard_paths), str(output).encode(), device))

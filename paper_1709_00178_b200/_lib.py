@@ -51,8 +51,19 @@ EXPORTS = (
     "pyrit_plan_reps", "pyrit_plan_key", "pyrit_plan_source", "pyrit_plan_interpret", "pyrit_plan_destroy", "pyrit_cu_apply",
     "pyrit_cu_prepare", "pyrit_cu_encode", "pyrit_cu_decode", "pyrit_encode_host", "pyrit_decode_host",
     "pyrit_set_host_chunk", "pyrit_cu_fill", "pyrit_cu_digest", "pyrit_set_lanes", "pyrit_set_kernel_mode", "pyrit_set_kernel_dir",
-    "pyrit_cu_last_launch", "pyrit_jit_compiles", "pyrit_kernel_launches",
+    "pyrit_cu_last_launch", "pyrit_jit_compiles", "pyrit_kernel_launches", "pyrit_cu_apply_batch",
+    "pyrit_cu_encode_batch", "pyrit_cu_decode_batch", "pyrit_crc32", "pyrit_header_serialize", "pyrit_header_parse",
+    "pyrit_field_id", "pyrit_field_from_id", "pyrit_shard_path", "pyrit_encode_file", "pyrit_decode_file",
+    "pyrit_set_file_chunk",
 )
+
+HEADER_SIZE = 29
+
+
+class pyrit_shard_header(C.Structure):
+    _fields_ = [("version", C.c_uint8), ("field", C.c_uint8), ("transform", C.c_uint8), ("k", C.c_uint16),
+                ("r", C.c_uint16), ("shard_index", C.c_uint16), ("symbol_size", C.c_uint32),
+                ("original_length", C.c_uint64)]
 
 
 def load():
@@ -103,6 +114,19 @@ def load():
     lib.pyrit_cauchy_parity_matrix.argtypes = [P(pyrit_code), vp]
     lib.pyrit_decode_matrix.argtypes = [P(pyrit_code), vp, vp, P(u32)]
     lib.pyrit_repair_matrix.argtypes = [P(pyrit_code), vp, u32, vp, vp, vp]
+    lib.pyrit_cu_apply_batch.argtypes = [vp, vp, vp, u64, u64, u64, u64, u64, u64, vp]
+    lib.pyrit_cu_encode_batch.argtypes = [P(pyrit_code), vp, vp, u64, u64, u64, u64, vp]
+    lib.pyrit_cu_decode_batch.argtypes = [P(pyrit_code), vp, vp, u32, u64, u64, u64, vp]
+    lib.pyrit_crc32.argtypes = [vp, C.c_size_t]
+    lib.pyrit_crc32.restype = u32
+    lib.pyrit_header_serialize.argtypes = [P(pyrit_shard_header), vp]
+    lib.pyrit_header_parse.argtypes = [vp, C.c_size_t, P(pyrit_shard_header)]
+    lib.pyrit_field_id.argtypes = [P(pyrit_field), P(C.c_uint8)]
+    lib.pyrit_field_from_id.argtypes = [C.c_uint8, P(pyrit_field)]
+    lib.pyrit_shard_path.argtypes = [C.c_char_p, C.c_char_p, u32, vp, C.c_size_t]
+    lib.pyrit_encode_file.argtypes = [P(pyrit_code), C.c_char_p, C.c_char_p, u32, i32]
+    lib.pyrit_decode_file.argtypes = [P(C.c_char_p), u32, C.c_char_p, i32]
+    lib.pyrit_set_file_chunk.argtypes = [u64]
     _lib = lib
     return lib
 

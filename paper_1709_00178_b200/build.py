@@ -30,9 +30,9 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-HOST_SOURCES = ["algebra.cpp", "program.cpp", "runtime.cpp", "pipeline.cpp", "capi.cpp"]
+HOST_SOURCES = ["algebra.cpp", "program.cpp", "runtime.cpp", "pipeline.cpp", "plans.cpp", "container.cpp", "capi.cpp"]
 CUDA_SOURCES = ["kernels.cu"]
-HEADERS = ["algebra.hpp", "program.hpp", "runtime.hpp", "pipeline.hpp", "kernels.hpp"]
+HEADERS = ["algebra.hpp", "program.hpp", "runtime.hpp", "pipeline.hpp", "plans.hpp", "container.hpp", "kernels.hpp"]
 
 
 def _run(cmd, **kw):
@@ -121,10 +121,15 @@ def prebuild_kernels(lanes=(100, 1), force=False) -> list[str]:
                 with open(cu, "w") as f:
                     f.write(buf.value.decode())
                 if force or not os.path.exists(cubin):
-                    _run([NVCC, "-cubin", *ARCH, "-lineinfo", "-O3", "-Xptxas", "-v", cu, "-o", cubin])
+                    _run([NVCC, "-cubin", *ARCH, "-lineinfo", "-O3", "-diag-suppress", "177", "-Xptxas", "-v", cu,
+                          "-o", cubin])
                 built.append(cubin)
         finally:
             lib.pyrit_plan_destroy(plan)
+    # cubins of older generator versions are never loaded again: drop them
+    for f in os.listdir(KDIR):
+        if f.endswith(".cubin") and os.path.join(KDIR, f) not in built:
+            os.remove(os.path.join(KDIR, f))
     return built
 
 

@@ -12,6 +12,8 @@
 #include "algebra.hpp"
 #include "kernels.hpp"
 #include "pipeline.hpp"
+#include "plans.hpp"
+#include "container.hpp"
 #include "program.hpp"
 #include "runtime.hpp"
 
@@ -73,77 +75,19 @@ std::uint64_t strip_of(const pyrit_code* c, std::uint64_t symbol_size) {
     return symbol_size / c->field.w;
 }
 
-// compiled programs for the top-level API, keyed by code (+ erasures)
-class PlanCache {
-public:
-    std::shared_ptr<const Program> get(const std::string& key) {
-        std::lock_guard<std::mutex> lk(mu_);
-        auto it = map_.find(key);
-        if (it == map_.end()) return nullptr;
-        lru_.splice(lru_.begin(), lru_, it->second.second);
-        return it->second.first;
-    }
-    void put(const std::string& key, std::shared_ptr<const Program> p) {
-        std::lock_guard<std::mutex> lk(mu_);
-        if (map_.count(key)) return;
-        lru_.push_front(key);
-        map_[key] = {std::move(p), lru_.begin()};
-        while (map_.size() > 512) {
-            map_.erase(lru_.back());
-            lru_.pop_back();
-        }
-    }
-
-private:
-    std::mutex mu_;
-    std::list<std::string> lru_;
-    std::unordered_map<std::string, std::pair<std::shared_ptr<const Program>, std::list<std::string>::iterator>> map_;
-};
-
-PlanCache& cache() {
-    static PlanCache c;
-    return c;
-}
-
-std::string code_key(const pyrit_code* c) {
-    std::ostringstream s;
-    s << c->k << ',' << c->r << ',' << c->field.w << ',' << c->field.n << ',' << c->field.kind << ','
-      << c->field.s << ',' << c->field.r_esp << ',' << c->field.modulus << ',' << c->transform;
-    return s.str();
-}
-
-std::shared_ptr<const Program> encode_program(const pyrit_code* c) {
-    const std::string key = "E" + code_key(c);
-    if (auto p = cache().get(key)) return p;
-    const Field f = to_field(&c->field);
-    auto p = std::make_shared<const Program>(compile_program(
-        f, static_cast<TransformKind>(c->transform), cauchy_parity_matrix(c->k, c->r, f), CompileOptions{}));
-    cache().put(key, p);
+CodeParams params_of(const pyrit_code* c) {
+    CodeParams p;
+    p.k = c->k;
+    p.r = c->r;
+    p.field = to_field(&c->field);
+    p.kind = static_cast<TransformKind>(c->transform);
     return p;
 }
 
-struct DecodeProgram {
-    std::shared_ptr<const Program> prog;
-    RepairPlan repair;
-};
+std::shared_ptr<const Program> encode_program(const pyrit_code* c) { return encode_program(params_of(c)); }
 
 DecodeProgram decode_program(const pyrit_code* c, const std::vector<std::uint32_t>& erased) {
-    const Field f = to_field(&c->field);
-    DecodeProgram d;
-    d.repair = repair_matrix(c->k, c->r, f, erased);
-    if (d.repair.outputs.empty()) return d;
-    std::ostringstream key;
-    key << "D" << code_key(c) << ':';
-    for (std::uint32_t o : d.repair.outputs) key << o << ',';
-    if (auto p = cache().get(key.str())) {
-        d.prog = p;
-        return d;
-    }
-    auto p = std::make_shared<const Program>(
-        compile_program(f, static_cast<TransformKind>(c->transform), d.repair.m, CompileOptions{}));
-    cache().put(key.str(), p);
-    d.prog = p;
-    return d;
+    return decode_program(params_of(c), erased);
 }
 
 } // namespace
@@ -397,6 +341,47 @@ int pyrit_cu_decode(const pyrit_code* code, uint8_t* const* symbols, const uint3
     });
 }
 
+int pyrit_cu_apply_batch(const pyrit_plan* plan, const uint8_t* const* in, uint8_t* const* out,
+                         uint64_t strip_bytes, uint64_t off, uint64_t len, uint64_t stripes, uint64_t in_pitch,
+                         uint64_t out_pitch, void* stream) {
+    return guarded([&] {
+        if (!plan || !in || !out) raise(Errc::InvalidArgument, "null argument");
+        launch_batch(plan->prog, in, out, strip_bytes, off, len, stripes, in_pitch, out_pitch,
+                     static_cast<cudaStream_t>(stream));
+    });
+}
+
+int pyrit_cu_encode_batch(const pyrit_code* code, const uint8_t* const* data, uint8_t* const* parity,
+                          uint64_t symbol_size, uint64_t stripes, uint64_t data_pitch, uint64_t parity_pitch,
+                          void* stream) {
+    return guarded([&] {
+        check_code(code);
+        const std::uint64_t strip = strip_of(code, symbol_size);
+        if (!data || (!parity && code->r)) raise(Errc::InvalidArgument, "null symbol array");
+        if (code->r == 0) return;
+        auto p = encode_program(code);
+        launch_batch(*p, data, parity, strip, 0, strip, stripes, data_pitch, parity_pitch,
+                     static_cast<cudaStream_t>(stream));
+    });
+}
+
+int pyrit_cu_decode_batch(const pyrit_code* code, uint8_t* const* symbols, const uint32_t* erased,
+                          uint32_t n_erased, uint64_t symbol_size, uint64_t stripes, uint64_t pitch, void* stream) {
+    return guarded([&] {
+        check_code(code);
+        const std::uint64_t strip = strip_of(code, symbol_size);
+        if (!symbols || (!erased && n_erased)) raise(Errc::InvalidArgument, "null argument");
+        const DecodeProgram d = decode_program(code, std::vector<uint32_t>(erased, erased + n_erased));
+        if (!d.prog) return;
+        std::vector<const uint8_t*> in;
+        std::vector<uint8_t*> out;
+        for (uint32_t s : d.repair.survivors) in.push_back(symbols[s]);
+        for (uint32_t o : d.repair.outputs) out.push_back(symbols[o]);
+        launch_batch(*d.prog, in.data(), out.data(), strip, 0, strip, stripes, pitch, pitch,
+                     static_cast<cudaStream_t>(stream));
+    });
+}
+
 int pyrit_encode_host(const pyrit_code* code, const uint8_t* data, uint8_t* parity, uint64_t symbol_size,
                       int device) {
     return guarded([&] {
@@ -434,6 +419,83 @@ int pyrit_set_host_chunk(uint64_t strip_chunk_bytes) {
         if (strip_chunk_bytes % 16) raise(Errc::InvalidArgument, "chunk must be a multiple of 16 bytes");
         set_host_chunk(strip_chunk_bytes);
     });
+}
+
+uint32_t pyrit_crc32(const uint8_t* bytes, size_t len) { return bytes || !len ? crc32(bytes, len) : 0u; }
+
+int pyrit_header_serialize(const pyrit_shard_header* h, uint8_t* out) {
+    return guarded([&] {
+        if (!h || !out) raise(Errc::InvalidArgument, "null argument");
+        ShardHeader x;
+        x.version = h->version;
+        x.field = h->field;
+        x.transform = h->transform;
+        x.k = h->k;
+        x.r = h->r;
+        x.shard_index = h->shard_index;
+        x.symbol_size = h->symbol_size;
+        x.original_length = h->original_length;
+        serialize_header(x, out);
+    });
+}
+
+int pyrit_header_parse(const uint8_t* bytes, size_t len, pyrit_shard_header* out) {
+    return guarded([&] {
+        if ((!bytes && len) || !out) raise(Errc::InvalidArgument, "null argument");
+        const ShardHeader h = parse_header(bytes, len);
+        *out = pyrit_shard_header{h.version, h.field, h.transform, h.k, h.r, h.shard_index, h.symbol_size,
+                                  h.original_length};
+    });
+}
+
+int pyrit_field_id(const pyrit_field* f, uint8_t* id) {
+    return guarded([&] {
+        if (!id) raise(Errc::InvalidArgument, "null argument");
+        *id = field_id(to_field(f));
+    });
+}
+
+int pyrit_field_from_id(uint8_t id, pyrit_field* out) {
+    return guarded([&] {
+        if (!out) raise(Errc::InvalidArgument, "null argument");
+        const Field f = field_from_id(id);
+        *out = pyrit_field{f.w, f.n, static_cast<uint32_t>(f.kind), f.s, f.r_esp, f.modulus};
+    });
+}
+
+int pyrit_shard_path(const char* input, const char* out_dir, uint32_t index, char* buf, size_t cap) {
+    return guarded([&] {
+        if (!input || !out_dir || !buf) raise(Errc::InvalidArgument, "null argument");
+        const std::string p = shard_path(input, out_dir, index);
+        if (p.size() + 1 > cap) raise(Errc::InvalidArgument, "path buffer too small");
+        std::memcpy(buf, p.c_str(), p.size() + 1);
+    });
+}
+
+int pyrit_encode_file(const pyrit_code* code, const char* input, const char* out_dir, uint32_t symbol_size,
+                      int device) {
+    return guarded([&] {
+        if (!code || !input || !out_dir) raise(Errc::InvalidArgument, "null argument");
+        if (code->transform > 1) raise(Errc::InvalidArgument, "unknown transform");
+        encode_file(input, out_dir, code->k, code->r, to_field(&code->field),
+                    static_cast<TransformKind>(code->transform), symbol_size, device);
+    });
+}
+
+int pyrit_decode_file(const char* const* shard_paths, uint32_t n_paths, const char* output, int device) {
+    return guarded([&] {
+        if ((!shard_paths && n_paths) || !output) raise(Errc::InvalidArgument, "null argument");
+        std::vector<std::string> paths;
+        for (uint32_t i = 0; i < n_paths; ++i) {
+            if (!shard_paths[i]) raise(Errc::InvalidArgument, "null shard path");
+            paths.emplace_back(shard_paths[i]);
+        }
+        decode_file(paths, output, device);
+    });
+}
+
+int pyrit_set_file_chunk(uint64_t bytes) {
+    return guarded([&] { set_file_chunk(bytes); });
 }
 
 int pyrit_cu_fill(uint64_t seed, uint64_t frag, uint8_t* dst, uint64_t begin, uint64_t len, uint64_t valid,

@@ -25,7 +25,7 @@ namespace {
 
 constexpr std::uint32_t kNone = 0xFFFFFFFFu;
 // bump whenever generated code changes for the same program (prebuilt cubins are keyed by name)
-constexpr int kGeneratorVersion = 4;
+constexpr int kGeneratorVersion = 5;
 
 // Greedy pair elimination over XOR targets.  Each target is a set of
 // variable ids; the most frequent pair (ties: smallest ids) becomes a new
@@ -489,7 +489,9 @@ std::string generate_staged(const Program& p, const KernelShape& ks) {
       << p.stats.ref_region_ops << " region ops); " << T << " threads, tile " << TILE << " B/strip, ring of "
       << NSLOT << " slots x " << G << " fragment(s)\n";
     o << "typedef unsigned int u32; typedef unsigned long long u64; typedef unsigned char u8;\n";
-    o << "struct Args { const u8* in[" << k << "]; u8* out[" << p.rows << "]; u64 S; u64 off; u64 len; };\n";
+    // nb stripes of the batch: input j of stripe b at in[j] + b * ibp, output i at out[i] + b * obp
+    o << "struct Args { const u8* in[" << k << "]; u8* out[" << p.rows
+      << "]; u64 S; u64 off; u64 len; u64 nb; u64 ibp; u64 obp; };\n";
     o << R"(static __device__ __forceinline__ u32 smem_u32(const void* p) {
   u32 r; asm("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(r) : "l"(p)); return r; }
 static __device__ __forceinline__ void mbar_init(u32 bar, u32 count) {
@@ -519,8 +521,8 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
       << "(const __grid_constant__ Args a)\n{\n";
     o << "  extern __shared__ __align__(1024) u8 sm[];\n";
     o << "  const u32 sbase = smem_u32(sm);\n";
-    o << "  const u64 end = a.off + a.len;\n";
-    o << "  const u32 ntiles = (u32)((a.len + TILE - 1) / TILE);\n";
+    o << "  const u32 tpb = (u32)((a.len + TILE - 1) / TILE);\n"; // tiles per stripe
+    o << "  const u32 ntiles = tpb * (u32)a.nb;\n";
     o << "  if (threadIdx.x == 0) {\n";
     o << "    for (u32 s = 0; s < NSLOT; ++s) { mbar_init(FULL(s), " << (ks.copy ? T : 1u) << "u); mbar_init(EMPTY(s), "
       << T << "u); }\n";
@@ -536,7 +538,8 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
     o << "    if (t2 >= ntiles) return;\n";
     o << "    const u32 sl = u2 % NSLOT, ph = (u2 / NSLOT) & 1u;\n";
     o << "    mbar_wait(EMPTY(sl), ph ^ 1u);\n";
-    o << "    const u64 o = a.off + (u64)t2 * TILE;\n";
+    o << "    const u32 b2 = t2 / tpb, tt2 = t2 - b2 * tpb;\n";
+    o << "    const u64 o = a.off + (u64)tt2 * TILE;\n";
     o << "    const u32 dst = sbase + BAR_BYTES + sl * SLOT_BYTES;\n";
     o << "    const u32 j0 = g2 * " << G << "u;\n";
     o << "    const u32 nstr = (g2 + 1u == NG ? " << k << "u - j0 : " << G << "u) * " << w << "u;\n";
@@ -549,14 +552,15 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
         // strips by NW*SPW; chunk validity only depends on the tile
         const std::uint32_t cps = TILE / 16;
         const std::uint32_t lps = std::min<std::uint32_t>(32, cps), spw = 32 / lps, cpl = cps / lps, nw = T / 32;
-        o << "    const u32 vb = (u32)(end - o < TILE ? end - o : TILE);\n";
+        o << "    const u64 rem = a.len - (u64)tt2 * TILE;\n";
+        o << "    const u32 vb = (u32)(rem < TILE ? rem : TILE);\n";
         o << "    const u32 lq = lane % " << lps << "u, lsub = lane / " << lps << "u;\n";
         for (std::uint32_t c = 0; c < cpl; ++c)
             o << "    const u32 n" << c << " = 16u * (lq + " << c * lps << "u) < vb ? 16u : 0u;\n";
         o << "#pragma unroll 1\n";
         o << "    for (u32 l = warp * " << spw << "u + lsub; l < nstr; l += " << nw * spw << "u) {\n";
         o << "      const u32 idx = j0 * " << w << "u + l, j = idx / " << w << "u, s = idx - j * " << w << "u;\n";
-        o << "      const u8* src = a.in[j] + s * a.S + o + 16u * lq;\n";
+        o << "      const u8* src = a.in[j] + b2 * a.ibp + s * a.S + o + 16u * lq;\n";
         o << "      const u32 d = dst + l * TILE + 16u * lq;\n";
         for (std::uint32_t c = 0; c < cpl; ++c)
             o << "      cpa16(d + " << 16 * c * lps << "u, n" << c << " ? src + " << 16 * c * lps
@@ -566,13 +570,14 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
     } else {
         // warp 0: lane 0 posts the byte count, the lanes issue one
         // cp.async.bulk per strip tile
-        o << "    const u32 bytes = (u32)(end - o < TILE ? end - o : TILE);\n";
+        o << "    const u64 rem = a.len - (u64)tt2 * TILE;\n";
+        o << "    const u32 bytes = (u32)(rem < TILE ? rem : TILE);\n";
         o << "    if (lane == 0) mbar_expect_tx(FULL(sl), bytes * nstr);\n";
         o << "    __syncwarp();\n";
         o << "#pragma unroll 1\n";
         o << "    for (u32 l = lane; l < nstr; l += 32u) {\n";
         o << "      const u32 idx = j0 * " << w << "u + l, j = idx / " << w << "u, s = idx - j * " << w << "u;\n";
-        o << "      bulk_g2s(dst + l * TILE, a.in[j] + s * a.S + o, bytes, FULL(sl), pol);\n";
+        o << "      bulk_g2s(dst + l * TILE, a.in[j] + b2 * a.ibp + s * a.S + o, bytes, FULL(sl), pol);\n";
         o << "    }\n";
     }
     o << "  };\n";
@@ -587,8 +592,10 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
         o << "  " << (r ? "else if" : "if") << " (part == " << r << "u) {\n";
         o << "   u32 it = 0;\n";
         o << "   for (u32 t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {\n";
-        o << "    const u64 o = a.off + (u64)t * TILE + 4u * col;\n";
-        o << "    const bool live = o < end;\n";
+        o << "    const u32 bb = t / tpb, tt = t - bb * tpb;\n";
+        o << "    const u64 rel = (u64)tt * TILE + 4u * col;\n";
+        o << "    const u64 o = a.off + rel + bb * a.obp;\n";
+        o << "    const bool live = rel < a.len;\n";
         std::vector<bool> out_ptr(q.rows, false);
         std::string cur_sp;
         auto emit = [&](const Instr& ins) {
@@ -648,7 +655,10 @@ std::string generate_cuda(const Program& p, const KernelShape& ks) {
       << p.stats.xors << " XORs (naive ring program " << p.stats.naive_xors << ", reference schedule "
       << p.stats.ref_region_ops << " region ops)\n";
     o << "typedef unsigned int u32; typedef unsigned long long u64; typedef unsigned char u8;\n";
-    o << "struct Args { const u8* in[" << p.cols << "]; u8* out[" << p.rows << "]; u64 S; u64 off; u64 nwords; };\n";
+    // nb stripes of nwords column words each; the grid stride advances
+    // (stripe, word) by (sq, sr) = divmod(stride, nwords), precomputed on the host
+    o << "struct Args { const u8* in[" << p.cols << "]; u8* out[" << p.rows
+      << "]; u64 S; u64 off; u64 nwords; u64 nb; u64 ibp; u64 obp; u64 sq; u64 sr; };\n";
     // loads: read-only, no L1 allocation (streamed once); stores: evict-first
     if (bytes) {
         o << "#define LD(v, p) asm(\"ld.global.nc.L1::no_allocate.u8 %0, [%1];\" : \"=r\"(v) : \"l\"(p))\n";
@@ -671,9 +681,11 @@ std::string generate_cuda(const Program& p, const KernelShape& ks) {
     o << "extern \"C\" __global__ void __launch_bounds__(" << ks.threads << ", " << ks.min_blocks << ") " << name
       << "(const Args a)\n{\n";
     o << "  const u64 S = a.S;\n";
-    o << "  const u64 stride = (u64)gridDim.x * " << ks.threads << "u;\n";
-    o << "  for (u64 c = (u64)blockIdx.x * " << ks.threads << "u + threadIdx.x; c < a.nwords; c += stride) {\n";
-    o << "    const u64 o = a.off + c * " << V << "u;\n";
+    o << "  const u64 c0 = (u64)blockIdx.x * " << ks.threads << "u + threadIdx.x;\n";
+    o << "  u64 b = c0 / a.nwords, cw = c0 - b * a.nwords;\n";
+    o << "  while (b < a.nb) {\n";
+    o << "    const u64 o = a.off + cw * " << V << "u;\n";
+    o << "    const u64 oi = o + b * a.ibp, oo = o + b * a.obp;\n";
     auto var = [&](std::uint32_t v, std::uint32_t l) {
         std::string s = "v" + std::to_string(v);
         if (!bytes) s += "_" + std::to_string(l);
@@ -683,7 +695,7 @@ std::string generate_cuda(const Program& p, const KernelShape& ks) {
     for (const Instr& ins : p.code) {
         if (ins.op == Instr::Load) {
             if (!frag_ptr[ins.sym]) {
-                o << "    const u8* i" << ins.sym << " = a.in[" << ins.sym << "] + o;\n";
+                o << "    const u8* i" << ins.sym << " = a.in[" << ins.sym << "] + oi;\n";
                 frag_ptr[ins.sym] = true;
             }
             o << "    u32 ";
@@ -699,7 +711,7 @@ std::string generate_cuda(const Program& p, const KernelShape& ks) {
             }
         } else {
             if (!out_ptr[ins.sym]) {
-                o << "    u8* q" << ins.sym << " = a.out[" << ins.sym << "] + o;\n";
+                o << "    u8* q" << ins.sym << " = a.out[" << ins.sym << "] + oo;\n";
                 out_ptr[ins.sym] = true;
             }
             o << "    { u32 ";
@@ -713,6 +725,8 @@ std::string generate_cuda(const Program& p, const KernelShape& ks) {
             o << ", x); }\n";
         }
     }
+    o << "    b += a.sq; cw += a.sr;\n";
+    o << "    if (cw >= a.nwords) { cw -= a.nwords; ++b; }\n";
     o << "  }\n}\n";
     return o.str();
 }

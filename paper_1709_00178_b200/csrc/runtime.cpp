@@ -239,16 +239,23 @@ void set_kernel_mode(int mode) {
 }
 
 KernelShape choose_shape(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
-                         std::uint64_t strip, std::uint64_t off, std::uint64_t len) {
+                         std::uint64_t strip, std::uint64_t off, std::uint64_t len, std::uint64_t nb,
+                         std::uint64_t in_pitch, std::uint64_t out_pitch) {
     const auto all_aligned = [&](std::uint64_t v) {
         bool ok = strip % v == 0 && off % v == 0 && len % v == 0;
+        if (nb > 1) ok = ok && in_pitch % v == 0 && out_pitch % v == 0;
         for (std::uint32_t j = 0; ok && j < p.cols; ++j) ok = aligned(in[j], v);
         for (std::uint32_t i = 0; ok && i < p.rows; ++i) ok = aligned(out[i], v);
         return ok;
     };
     if (kernel_mode() != 1 && all_aligned(16)) {
         const KernelShape ks = staged_for(p);
-        if (ks.staged) return ks;
+        // short per-stripe windows leave most of a tile idle: the direct
+        // kernel streams them better (auto mode only)
+        const std::uint64_t tiles = ks.staged ? (len + ks.tile - 1) / ks.tile : 0;
+        const bool dense = tiles && 2 * len >= tiles * ks.tile;
+        const bool fits = tiles * nb < (std::uint64_t(1) << 32);
+        if (ks.staged && fits && (dense || kernel_mode() == 2)) return ks;
     }
     // direct mode: widest vector the alignment of every pointer, the strip
     // pitch and the window allows; byte mode otherwise
@@ -275,30 +282,47 @@ std::string prepare_program(const Program& p, std::uint32_t lanes) {
 
 LaunchInfo launch_program(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
                           std::uint64_t strip, std::uint64_t off, std::uint64_t len, cudaStream_t stream) {
+    return launch_batch(p, in, out, strip, off, len, 1, 0, 0, stream);
+}
+
+LaunchInfo launch_batch(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
+                        std::uint64_t strip, std::uint64_t off, std::uint64_t len, std::uint64_t nb,
+                        std::uint64_t in_pitch, std::uint64_t out_pitch, cudaStream_t stream) {
     LaunchInfo info;
     if (off + len > strip) raise(Errc::BufferShape, "column window out of range");
-    if (len == 0) return info;
+    if (len == 0 || nb == 0) return info;
+    if (nb == 1) in_pitch = out_pitch = 0;
     int dev = 0;
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
-    const KernelShape ks = choose_shape(p, in, out, strip, off, len);
+    const KernelShape ks = choose_shape(p, in, out, strip, off, len, nb, in_pitch, out_pitch);
     const LoadedKernel k = load_kernel(p, ks, dev);
-    std::vector<std::uint64_t> args(std::size_t(p.cols) + p.rows + 3);
+    // Args: in[cols], out[rows], S, off, len|nwords, nb, ibp, obp (, sq, sr)
+    std::vector<std::uint64_t> args(std::size_t(p.cols) + p.rows + 8, 0);
     for (std::uint32_t j = 0; j < p.cols; ++j) args[j] = reinterpret_cast<std::uint64_t>(in[j]);
     for (std::uint32_t i = 0; i < p.rows; ++i) args[p.cols + i] = reinterpret_cast<std::uint64_t>(out[i]);
-    args[p.cols + p.rows] = strip;
-    args[p.cols + p.rows + 1] = off;
-    std::uint64_t want;
+    std::uint64_t* tail = &args[p.cols + p.rows];
+    tail[0] = strip;
+    tail[1] = off;
+    tail[3] = nb;
+    tail[4] = in_pitch;
+    tail[5] = out_pitch;
+    const std::uint64_t cap = std::uint64_t(k.sms) * std::uint64_t(k.blocks_per_sm);
+    std::uint64_t want, nwords = 0;
     if (ks.staged) {
-        args[p.cols + p.rows + 2] = len; // bytes; tiles of ks.tile bytes per strip
-        want = (len + ks.tile - 1) / ks.tile;
+        tail[2] = len; // bytes; tiles of ks.tile bytes per strip
+        want = (len + ks.tile - 1) / ks.tile * nb;
     } else {
         const std::uint64_t vbytes = ks.lanes ? 4ull * ks.lanes : 1ull;
-        const std::uint64_t nwords = len / vbytes;
-        args[p.cols + p.rows + 2] = nwords;
-        want = (nwords + ks.threads - 1) / ks.threads;
+        nwords = len / vbytes;
+        tail[2] = nwords;
+        want = (nwords * nb + ks.threads - 1) / ks.threads;
     }
-    const std::uint64_t cap = std::uint64_t(k.sms) * std::uint64_t(k.blocks_per_sm);
     const unsigned blocks = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min(want, cap)));
+    if (!ks.staged) {
+        const std::uint64_t stride = std::uint64_t(blocks) * ks.threads;
+        tail[6] = stride / nwords;
+        tail[7] = stride % nwords;
+    }
     void* params[] = {args.data()};
     check_cu(driver().launchKernel(k.fn, blocks, 1, 1, ks.threads, 1, 1, ks.staged ? ks.smem_bytes : 0,
                                    reinterpret_cast<CUstream>(stream), params, nullptr),

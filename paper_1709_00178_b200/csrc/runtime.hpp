@@ -36,6 +36,14 @@ struct LaunchInfo {
 LaunchInfo launch_program(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
                           std::uint64_t strip, std::uint64_t off, std::uint64_t len, cudaStream_t stream);
 
+// Stripe batch: the same window of `nb` stripes in one launch; input j of
+// stripe b is at in[j] + b * in_pitch, output i at out[i] + b * out_pitch
+// (the per-stripe encode()/decode() calls of encode_file/decode_file,
+// container.hpp:207-218 and :284-297, batched).
+LaunchInfo launch_batch(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
+                        std::uint64_t strip, std::uint64_t off, std::uint64_t len, std::uint64_t nb,
+                        std::uint64_t in_pitch, std::uint64_t out_pitch, cudaStream_t stream);
+
 // Force compilation/loading for the current device (no launch).
 std::string prepare_program(const Program& p, std::uint32_t lanes);
 
@@ -58,6 +66,7 @@ int kernel_mode();
 void set_kernel_mode(int mode);
 // the kernel shape a launch with these arguments uses
 KernelShape choose_shape(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
-                         std::uint64_t strip, std::uint64_t off, std::uint64_t len);
+                         std::uint64_t strip, std::uint64_t off, std::uint64_t len, std::uint64_t nb = 1,
+                         std::uint64_t in_pitch = 0, std::uint64_t out_pitch = 0);
 
 } // namespace pyrit_b200

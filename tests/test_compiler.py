@@ -204,4 +204,4 @@ def test_generated_source_is_straight_line():
     name, src = P.Plan.encode(WORKLOADS[5].code).source(1)
     assert name.startswith("pyrit_ring_k16_e4_w12_n13")
     assert "__launch_bounds__" in src and "ld.global.nc" in src and "st.global.cs" in src
-    assert "for (u64 c" in src and src.count("LD(") == 16 * 12 + 1  # one per strip (+ macro)
+    assert "while (b < a.nb)" in src and src.count("LD(") == 16 * 12 + 1  # one per strip (+ macro)
