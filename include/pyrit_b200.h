@@ -105,7 +105,9 @@ int pyrit_repair_matrix(const pyrit_code* code, const uint32_t* erased, uint32_t
                         uint32_t* survivors, uint32_t* outputs, uint16_t* matrix);
 
 /* ---- compiled plans (schedule.hpp:94 compile_schedule) ---------------- */
-/* rep: 0 = RingRep::Sparse (minimal weight), 1 = Dense (schedule.hpp:78);
+/* rep: 0 = RingRep::Sparse (minimal weight), 1 = Dense (schedule.hpp:78),
+ * 2 = the plain-field Cauchy-RS bitmatrix program instead of the ring
+ * (compile_crs_schedule, schedule.hpp:168-203: the GPU CRS baseline);
  * group: input symbols per register group, 0 = automatic */
 int pyrit_plan_create(const pyrit_field* f, uint32_t transform, const uint16_t* matrix, uint32_t rows,
                       uint32_t cols, uint32_t rep, uint32_t group, pyrit_plan** out);

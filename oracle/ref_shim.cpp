@@ -188,6 +188,7 @@ REF_EXPORT int ref_decode(unsigned w, unsigned n, unsigned kind, unsigned s, uns
 //         via decode_matrix, then erased parity re-encoded from data.
 // mode 3: decode, same two passes with ring schedules (the reference's own
 //         decode(); valid for the AOP/ESP fields only).
+// mode | 0x10: the code uses the Parity transform (ring schedules only).
 struct RefPlan {
     FieldSpec spec;
     CodeSpec code;
@@ -207,11 +208,14 @@ REF_EXPORT void* ref_plan_create(unsigned w, unsigned n, unsigned kind, unsigned
         auto plan = std::make_unique<RefPlan>(RefPlan{make_field(w, n, kind, s, r_esp, modulus),
                                                       CodeSpec{}, mode, nullptr, {}, {}, {}, {},
                                                       {}, {}, false, false});
-        plan->code = CodeSpec{k, r, plan->spec, TransformKind::Embedding};
+        const TransformKind kind = (mode & 0x10) ? TransformKind::Parity : TransformKind::Embedding;
+        mode &= 0xF;
+        plan->mode = mode;
+        plan->code = CodeSpec{k, r, plan->spec, kind};
         plan->symbols = std::make_unique<SymbolBuffer>(k + r, symbol_size, plan->spec);
         const FieldMatrix c = cauchy_parity_matrix(plan->code);
         auto compile = [&](const FieldMatrix& m, bool crs) {
-            return crs ? compile_crs_schedule(m) : compile_schedule(m, TransformKind::Embedding);
+            return crs ? compile_crs_schedule(m) : compile_schedule(m, kind);
         };
         if (mode <= 1) {
             plan->sched_a = compile(c, mode == 1);

@@ -36,6 +36,7 @@ class TransformKind(enum.IntEnum):  # transform.hpp:24
 class RingRep(enum.IntEnum):  # schedule.hpp:78
     Sparse = 0
     Dense = 1
+    Crs = 2  # not a ring representative: the bitmatrix program of compile_crs_schedule (schedule.hpp:168-203)
 
 
 def choose_transform(k: int, r: int) -> TransformKind:  # schedule.hpp:71-73

@@ -197,7 +197,9 @@ int pyrit_plan_create(const pyrit_field* f, uint32_t transform, const uint16_t* 
         std::memcpy(m.e.data(), matrix, std::size_t(rows) * cols * sizeof(uint16_t));
         CompileOptions opt;
         opt.group = group;
+        if (rep > 2) raise(Errc::InvalidArgument, "rep must be 0 (sparse ring), 1 (dense ring) or 2 (CRS bitmatrix)");
         opt.dense = rep == 1;
+        opt.crs = rep == 2;
         auto plan = std::make_unique<pyrit_plan>();
         plan->prog = compile_program(to_field(f), static_cast<TransformKind>(transform), m, opt);
         *out = plan.release();

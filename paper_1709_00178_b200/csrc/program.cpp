@@ -25,7 +25,7 @@ namespace {
 
 constexpr std::uint32_t kNone = 0xFFFFFFFFu;
 // bump whenever generated code changes for the same program (prebuilt cubins are keyed by name)
-constexpr int kGeneratorVersion = 5;
+constexpr int kGeneratorVersion = 6;
 
 // Greedy pair elimination over XOR targets.  Each target is a set of
 // variable ids; the most frequent pair (ties: smallest ids) becomes a new
@@ -119,8 +119,10 @@ std::string plan_key(const Program& p) {
     fp << p.field.w << ',' << p.field.n << ',' << p.field.modulus << ',' << int(p.kind) << ',' << p.rows << ','
        << p.cols << ':';
     for (std::uint32_t r : p.reps) fp << r << ',';
+    if (p.crs) // bitmatrix programs depend on the matrix itself, not on representatives
+        for (std::uint16_t x : p.matrix) fp << 'c' << x;
     char key[64];
-    std::snprintf(key, sizeof key, "w%un%u_%ux%u_%016llx", p.field.w, p.field.n, p.rows, p.cols,
+    std::snprintf(key, sizeof key, "w%un%u_%ux%u%s_%016llx", p.field.w, p.field.n, p.rows, p.cols, p.crs ? "crs" : "",
                   static_cast<unsigned long long>(fnv1a(fp.str())));
     return key;
 }
@@ -187,6 +189,8 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
     p.group = opt.group ? opt.group : std::max<std::uint32_t>(1, 24 / w);
     p.group = std::min(p.group, k);
     p.cse = opt.cse;
+    p.crs = opt.crs;
+    p.matrix = m.e;
     p.fold = fold_table(f);
     p.reps.resize(std::size_t(e) * k);
     for (std::size_t i = 0; i < p.reps.size(); ++i) {
@@ -194,17 +198,42 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
         p.reps[i] = opt.dense ? dense_transform(m.e[i], f) : sparse_transform(m.e[i], f);
         p.stats.matrix_ones += std::uint64_t(std::popcount(p.reps[i])) * w;
     }
+    // CRS: the w x w bitmatrix of every entry (field_to_bitmatrix, field.hpp:198-207):
+    // column c = coefficients of entry * x^c; rows[b] = mask of input strips feeding output strip b
+    std::vector<std::uint32_t> bits;
+    if (opt.crs) {
+        if (kind != TransformKind::Embedding) raise(Errc::InvalidArgument, "CRS programs are plain field codes");
+        bits.assign(std::size_t(e) * k * w, 0);
+        p.stats.matrix_ones = 0;
+        for (std::size_t idx = 0; idx < std::size_t(e) * k; ++idx)
+            for (std::uint32_t c = 0; c < w; ++c) {
+                const std::uint32_t prod = gf_mul(m.e[idx], 1u << c, f);
+                for (std::uint32_t b = 0; b < w; ++b)
+                    if ((prod >> b) & 1u) {
+                        bits[idx * w + b] |= 1u << c;
+                        ++p.stats.matrix_ones;
+                    }
+            }
+    }
 
     const bool emb = kind == TransformKind::Embedding;
-    const std::uint32_t out_rows = emb ? n : w; // schedule.hpp:132
+    const bool crs = opt.crs;
+    const std::uint32_t out_rows = emb && !crs ? n : w; // schedule.hpp:132 (CRS: w bit rows)
 
     // reference op count (compile_schedule), generalized post phase
     {
         std::uint64_t ops = 0;
-        if (!emb)
+        if (crs) // compile_crs_schedule (schedule.hpp:186-201): one op per bitmatrix one, Zero for empty rows
+            for (std::uint32_t i = 0; i < e; ++i)
+                for (std::uint32_t b = 0; b < w; ++b) {
+                    std::uint64_t row = 0;
+                    for (std::uint32_t j = 0; j < k; ++j) row += std::popcount(bits[(std::size_t(i) * k + j) * w + b]);
+                    ops += row ? row : 1;
+                }
+        if (!emb && !crs)
             for (std::uint32_t t = 0; t < n - w; ++t)
                 for (std::uint32_t i = t; i < w; i += f.s) ops += k;
-        for (std::uint32_t i = 0; i < e; ++i)
+        for (std::uint32_t i = 0; i < (crs ? 0u : e); ++i)
             for (std::uint32_t t = 0; t < out_rows; ++t) {
                 std::uint64_t row = 0;
                 for (std::uint32_t j = 0; j < k; ++j)
@@ -217,7 +246,7 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
                 ops += row;
                 if (!row && t < w) ++ops;
             }
-        if (emb)
+        if (emb && !crs)
             for (std::uint32_t fv : p.fold) ops += std::uint64_t(std::popcount(fv)) * e;
         p.stats.ref_region_ops = ops;
     }
@@ -249,9 +278,15 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
             for (std::uint32_t t = 0; t < out_rows; ++t) {
                 auto& tg = targets[i * out_rows + t];
                 for (std::uint32_t j = g0; j < g1; ++j)
-                    for (std::uint32_t sh = 0; sh < n; ++sh)
-                        if ((p.reps[i * k + j] >> sh) & 1u)
-                            for (std::uint32_t s : strips_of((t + n - sh) % n)) toggle(tg, var_of[(j - g0) * w + s]);
+                    if (crs) {
+                        const std::uint32_t row = bits[(std::size_t(i) * k + j) * w + t];
+                        for (std::uint32_t c = 0; c < w; ++c)
+                            if ((row >> c) & 1u) toggle(tg, var_of[(j - g0) * w + c]);
+                    } else {
+                        for (std::uint32_t sh = 0; sh < n; ++sh)
+                            if ((p.reps[i * k + j] >> sh) & 1u)
+                                for (std::uint32_t s : strips_of((t + n - sh) % n)) toggle(tg, var_of[(j - g0) * w + s]);
+                    }
                 std::sort(tg.begin(), tg.end());
                 p.stats.naive_xors += tg.size(); // one XOR per term into the row...
             }
@@ -291,7 +326,7 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
         std::vector<std::vector<std::uint32_t>> targets(w);
         for (std::uint32_t b = 0; b < w; ++b) {
             if (acc[i * out_rows + b] != kNone) targets[b].push_back(acc[i * out_rows + b]);
-            if (emb)
+            if (emb && !crs)
                 for (std::uint32_t t = w; t < n; ++t)
                     if (((p.fold[t - w] >> b) & 1u) && acc[i * out_rows + t] != kNone) {
                         targets[b].push_back(acc[i * out_rows + t]);
@@ -408,7 +443,9 @@ std::string kernel_name(const Program& p, const KernelShape& ks) {
     fp << kGeneratorVersion << ';' << p.field.w << ',' << p.field.n << ',' << p.field.modulus << ',' << int(p.kind)
        << ',' << p.rows << ',' << p.cols << ',' << p.group << ',' << ks.lanes << ',' << ks.threads << ',' << ks.min_blocks << ','
        << ks.staged << ',' << ks.tile << ',' << ks.stages << ',' << ks.bar_bytes << ',' << p.parts.size() << ','
-       << (p.parts.empty() ? 0u : p.parts[0].group) << ',' << ks.copy << ',' << p.cse << ',';
+       << (p.parts.empty() ? 0u : p.parts[0].group) << ',' << ks.copy << ',' << p.cse << ',' << p.crs << ',';
+    if (p.crs)
+        for (std::uint16_t x : p.matrix) fp << 'c' << x;
     for (const Program& q : p.parts) fp << q.rows << '/' << q.cse << '/' << q.stats.xors << ',';
     fp << ':';
     for (std::uint32_t r : p.reps) fp << r << ',';

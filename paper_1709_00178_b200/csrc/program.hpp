@@ -47,7 +47,9 @@ struct Program {
     std::uint32_t rows = 0, cols = 0; // outputs x inputs
     std::uint32_t group = 1;          // input fragments whose strips are live together
     bool cse = true;                  // pair sharing applied
+    bool crs = false;                 // plain-field bitmatrix program (compile_crs_schedule)
     std::vector<std::uint32_t> reps;  // rows x cols ring representatives (n-bit masks)
+    std::vector<std::uint16_t> matrix; // rows x cols GF(2^w) entries the program was compiled from
     std::vector<std::uint32_t> fold;  // fold[t - w] = x^t mod p
     std::vector<Instr> code;          // canonical order (next group's loads before this group's XORs)
     std::vector<std::vector<Instr>> group_loads, group_compute; // per fragment group
@@ -65,6 +67,7 @@ struct CompileOptions {
     std::uint32_t group = 0;   // 0: choose automatically
     bool cse = true;           // greedy pair elimination
     bool dense = false;        // RingRep::Dense (plain phi1) instead of Sparse (schedule.hpp:78)
+    bool crs = false;          // Cauchy-RS bitmatrix baseline instead of the ring (schedule.hpp:168-203)
     std::uint32_t parts = 0;   // output parts for the staged kernel: 0 auto, 1 = do not split
     std::uint32_t part_group = 0; // fragment group of the parts: 0 auto
     std::uint32_t max_temps = 0;  // cap on shared pair temporaries per group (0 = no cap)

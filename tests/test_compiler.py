@@ -205,3 +205,23 @@ def test_generated_source_is_straight_line():
     assert name.startswith("pyrit_ring_k16_e4_w12_n13")
     assert "__launch_bounds__" in src and "ld.global.nc" in src and "st.global.cs" in src
     assert "while (b < a.nb)" in src and src.count("LD(") == 16 * 12 + 1  # one per strip (+ macro)
+
+
+@pytest.mark.parametrize("f,k,r", [(G16, 4, 2), (G64, 6, 3), (G256, 10, 4), (G1024, 12, 4), (G4096, 16, 4)])
+def test_crs_bitmatrix_program(f, k, r):
+    """rep=2: the Cauchy-RS bitmatrix program (compile_crs_schedule, schedule.hpp:168-203)
+    computes the plain field code, and its op count equals the reference's CRS schedule."""
+    c = P.CodeSpec(k, r, f)
+    m = P.cauchy_parity_matrix(c)
+    plan = P.Plan.create(f, m, rep=P.RingRep.Crs)
+    ss = f.w * 40
+    data = rand_symbols(k, ss, k + r)
+    got = np.stack(plan.interpret(list(data), ss // f.w))
+    np.testing.assert_array_equal(got, oracle_encode(f, m, data))
+    st = plan.stats()
+    want = O.ref_schedule_stats(ofield(f), m, crs=1) if f.n <= 16 else None
+    if want:  # the reference's CRS compiler works for every field with 16-bit ring elements
+        assert st["ref_region_ops"] == want["total"] and st["matrix_ones"] == want["matrix_ones"]
+    assert plan.key() != P.Plan.create(f, m).key() and "crs" in plan.key()
+    with pytest.raises(P.PyritError):
+        P.Plan.create(f, m, P.TransformKind.Parity, rep=P.RingRep.Crs)

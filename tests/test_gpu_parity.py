@@ -246,3 +246,30 @@ def test_kernel_modes_agree(cuda, mode, cfg):
             np.testing.assert_array_equal(dev_decode(cuda, wl.code, work, wl.erased), full)
     finally:
         L.check(lib.pyrit_set_kernel_mode(0))
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_crs_baseline_kernel(cuda, cfg, mode):
+    """The GPU CRS bitmatrix baseline (rep=2) is bit-exact with the ring path and the field oracle."""
+    import torch
+    lib = L.load()
+    L.check(lib.pyrit_set_kernel_mode(mode))
+    try:
+        wl = WORKLOADS[cfg]
+        f = wl.fld
+        ss = f.w * (2048 + 16 * 5)
+        data = seeded_symbols(wl.k, ss, f.w, wl.seed)
+        C = P.cauchy_parity_matrix(wl.code)
+        m = C if wl.op == "encode" else P.repair_matrix(wl.code, wl.erased)[2]
+        src = data if wl.op == "encode" else np.concatenate([data, oracle_ring(f, C, data)])[
+            P.repair_matrix(wl.code, wl.erased)[0]]
+        plan = P.Plan.create(f, m, rep=P.RingRep.Crs)
+        d = torch.from_numpy(np.ascontiguousarray(src)).to(cuda)
+        out = torch.zeros((m.shape[0], ss), dtype=torch.uint8, device=cuda)
+        plan.apply([d[j].data_ptr() for j in range(d.shape[0])], [out[i].data_ptr() for i in range(m.shape[0])],
+                   ss // f.w)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(out.cpu().numpy(), oracle_encode(f, m, src))
+    finally:
+        L.check(lib.pyrit_set_kernel_mode(0))

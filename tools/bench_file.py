@@ -1,0 +1,99 @@
+#!/usr/bin/env python
+"""File-codec benchmark: encode_file / decode_file (container.hpp:168-299)
+through the GPU vs the reference's own (oracle/_ref, unmodified headers:
+one encode()/decode() call per stripe, as `pyrit encode` / `pyrit decode` run).
+
+    python tools/bench_file.py [--mib 1024] [--k 4 --r 2 --field gf16 --symbol 4096] [--dir /dev/shm]
+
+Both sides read and write real files (page cache; tmpfs when --dir is
+/dev/shm).  Rates are input-file bytes per second.  Verifies that the GPU's
+shard files are byte-identical to the reference's (gf16/gf64 sets) and that
+both decoders rebuild the input from k survivors (the first r shards erased).
+"""
+from __future__ import annotations
+
+import argparse
+import filecmp
+import json
+import os
+import shutil
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+FIELDS = {"gf16": (4, 5, 0, 1, 4, 0x1F), "gf64": (6, 9, 1, 3, 2, 0x49), "gf1024": (10, 11, 0, 1, 10, 0x7FF),
+          "gf4096": (12, 13, 0, 1, 12, 0x1FFF)}
+
+
+def timed(fn, reps=1):
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return best
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--mib", type=int, default=1024)
+    ap.add_argument("--k", type=int, default=4)
+    ap.add_argument("--r", type=int, default=2)
+    ap.add_argument("--field", default="gf16", choices=sorted(FIELDS))
+    ap.add_argument("--symbol", type=int, default=4096)
+    ap.add_argument("--dir", default="/dev/shm" if os.path.isdir("/dev/shm") else None)
+    ap.add_argument("--no-ref", action="store_true")
+    ap.add_argument("--reps", type=int, default=2)
+    a = ap.parse_args()
+
+    import numpy as np
+
+    import oracle as O
+    import paper_1709_00178_b200 as P
+
+    f = FIELDS[a.field]
+    code = P.CodeSpec(a.k, a.r, P.FieldSpec(*f))
+    base = tempfile.mkdtemp(prefix="pyrit_file_", dir=a.dir)
+    try:
+        n = a.mib << 20
+        src = os.path.join(base, "input.bin")
+        rng = np.random.default_rng(1)
+        with open(src, "wb") as fh:
+            left = n
+            while left:
+                c = min(left, 64 << 20)
+                fh.write(rng.integers(0, 256, c, dtype=np.uint8).tobytes())
+                left -= c
+        gdir, rdir = os.path.join(base, "gpu"), os.path.join(base, "ref")
+        P.encode_file(src, gdir, code, a.symbol)  # warm-up (plan compile, pinned staging)
+        t_enc = timed(lambda: P.encode_file(src, gdir, code, a.symbol), a.reps)
+        shards = [P.shard_path(src, gdir, i) for i in range(a.k + a.r)]
+        surv = shards[a.r:]
+        out = os.path.join(base, "gpu_out.bin")
+        P.decode_file(surv, out)
+        t_dec = timed(lambda: P.decode_file(surv, out), a.reps)
+        ok = filecmp.cmp(src, out, shallow=False)
+        row = {"file_bytes": n, "k": a.k, "r": a.r, "field": a.field, "symbol_size": a.symbol, "dir": a.dir,
+               "gpu_encode_file_GBps": n / t_enc / 1e9, "gpu_decode_file_GBps": n / t_dec / 1e9,
+               "gpu_decode_erased": list(range(a.r)), "gpu_roundtrip_ok": ok}
+        if not a.no_ref:
+            t_renc = timed(lambda: O.ref_encode_file(src, rdir, a.k, a.r, O.Field(*f), a.symbol), 1)
+            rsurv = [os.path.join(rdir, os.path.basename(p)) for p in surv]
+            rout = os.path.join(base, "ref_out.bin")
+            t_rdec = timed(lambda: O.ref_decode_file(rsurv, rout), 1)
+            same = all(filecmp.cmp(p, os.path.join(rdir, os.path.basename(p)), shallow=False) for p in shards)
+            row.update({"ref_encode_file_GBps": n / t_renc / 1e9, "ref_decode_file_GBps": n / t_rdec / 1e9,
+                        "ref_threads": 1, "ref_roundtrip_ok": filecmp.cmp(src, rout, shallow=False),
+                        "shards_identical_to_reference": same if a.field in ("gf16", "gf64") else None,
+                        "speedup_encode": t_renc / t_enc, "speedup_decode": t_rdec / t_dec})
+        print(json.dumps(row), flush=True)
+    finally:
+        shutil.rmtree(base, ignore_errors=True)
+
+
+if __name__ == "__main__":
+    main()
