@@ -95,6 +95,8 @@ def ref():
         _ref.ref_plan_run.argtypes = [C.c_void_p, C.c_uint]
         _ref.ref_plan_destroy.argtypes = [C.c_void_p]
         _ref.ref_crc32.restype = C.c_uint32
+        _ref.ref_bench_point.restype = C.c_double
+        _ref.ref_bench_point.argtypes = [C.c_uint] * 6 + [C.c_uint] * 5 + [C.c_uint64, C.c_uint, C.c_double]
         _ref.ref_crc32.argtypes = [C.c_char_p, C.c_uint64]
     return _ref
 
@@ -442,3 +444,8 @@ def ref_parse_header(b: bytes):
     if rc:
         raise OracleError(rc)
     return tuple(out)
+
+
+def ref_bench_point(f: Field, k, r, codec, op, size, workers, transform=0, target_seconds=0.25) -> float:
+    """bench.hpp:146-208 BenchRunner::run_point (GB/s, (k + r) * size convention); w <= 6 only."""
+    return ref().ref_bench_point(*_fa(f), k, r, transform, codec, op, size, workers, target_seconds)

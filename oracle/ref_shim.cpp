@@ -13,6 +13,7 @@
 #include <memory>
 #include <vector>
 
+#include "pyrit/bench.hpp"
 #include "pyrit/codec.hpp"
 #include "pyrit/container.hpp"
 #include "pyrit/matrix.hpp"
@@ -323,4 +324,22 @@ REF_EXPORT int ref_decode_file(const char* const* paths, unsigned n_paths, const
         for (unsigned i = 0; i < n_paths; ++i) ps.emplace_back(paths[i]);
         decode_file(ps, output);
     });
+}
+
+// bench.hpp:111-208: BenchRunner::run_point, the reference's own benchmark
+// cell (one stripe, column windows over `workers` threads with a barrier
+// per iteration, auto-calibrated to target_seconds).  GB/s in the
+// reference's (k + r) * size convention.  codec 0 pyrit, 1 crs, 2 table;
+// op 0 encode, 1 decode.  Valid only where TableCodec is (w <= 6).
+REF_EXPORT double ref_bench_point(unsigned w, unsigned n, unsigned kind, unsigned s, unsigned r_esp,
+                                  std::uint32_t modulus, unsigned k, unsigned r, unsigned transform, unsigned codec,
+                                  unsigned op, std::uint64_t size, unsigned workers, double target_seconds) {
+    double out = -1.0;
+    guarded([&] {
+        const CodeSpec code{k, r, make_field(w, n, kind, s, r_esp, modulus), static_cast<TransformKind>(transform)};
+        BenchRunner runner(code, size);
+        out = runner.run_point(static_cast<CodecKind>(codec), op ? BenchOp::Decode : BenchOp::Encode, workers, 0,
+                               target_seconds);
+    });
+    return out;
 }

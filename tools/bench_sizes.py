@@ -33,10 +33,21 @@ FIELDS = {"gf16": (4, 5, 0, 1, 4, 0x1F), "gf64": (6, 9, 1, 3, 2, 0x49), "gf256_r
 
 
 def cpu_point(f, k, r, kind, size, op, codec, threads, seconds=0.25):
+    """Seconds per stripe of the reference CPU path.  Fields with w <= 6: the
+    reference's own bench cell (BenchRunner::run_point, bench.hpp:146-208), best
+    of 1 and `threads` workers; wider fields (BenchRunner cannot build its table
+    codec there): precompiled schedule + parallel_replay with `threads`."""
     import numpy as np
 
     import oracle as O
     of = O.Field(*f)
+    if f[0] <= 6:
+        best = 0.0
+        for t in sorted({1, threads}):
+            g = O.ref_bench_point(of, k, r, 1 if codec == "crs" else 0, 0 if op == "encode" else 1, size, t, kind,
+                                  seconds)
+            best = max(best, g)
+        return (k + r) * size / (best * 1e9) if best > 0 else None
     if op == "encode":
         mode = 1 if codec == "crs" else 0
         erased = ()
@@ -76,12 +87,15 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--cpu", action="store_true")
+    ap.add_argument("--mode", type=int, default=0, help="kernel mode: 0 auto, 1 direct, 2 staged")
     a = ap.parse_args()
 
     import torch
 
     import paper_1709_00178_b200 as P
 
+    from paper_1709_00178_b200 import _lib as L
+    L.check(L.load().pyrit_set_kernel_mode(a.mode))
     dev = torch.device("cuda", 0)
     f = FIELDS[a.field]
     fs = P.FieldSpec(*f)
@@ -141,7 +155,7 @@ def main():
                 ms = e0.elapsed_time(e1) / a.steps
                 info = P.Plan.last_launch()
                 src = k * size * nb
-                row = {"field": a.field, "k": k, "r": r, "transform": a.transform, "op": op, "codec": codec,
+                row = {"mode": a.mode, "field": a.field, "k": k, "r": r, "transform": a.transform, "op": op, "codec": codec,
                        "size": size, "stripes": nb, "gpu_ms": ms, "gpu_src_GBps": src / ms / 1e6,
                        "gpu_ref_GBps": (k + r) * size * nb / ms / 1e6,
                        "gpu_moved_GBps": (k + n_out) * size * nb / ms / 1e6, "kernel": info["kernel"],
