@@ -266,12 +266,14 @@ int pyrit_plan_source(const pyrit_plan* plan, uint32_t lanes, char* buf, size_t 
                       size_t name_cap) {
     return guarded([&] {
         if (!plan) raise(Errc::InvalidArgument, "null plan");
-        if (lanes != 0 && lanes != 1 && lanes != 2 && lanes != 4 && lanes != PYRIT_SOURCE_STAGED)
-            raise(Errc::InvalidArgument, "bad lanes");
-        KernelShape ks = shape_for(lanes == PYRIT_SOURCE_STAGED ? 1 : lanes);
-        if (lanes == PYRIT_SOURCE_STAGED) {
+        const bool staged = lanes == PYRIT_SOURCE_STAGED || lanes == PYRIT_SOURCE_STAGED + 4 ||
+                            lanes == PYRIT_SOURCE_STAGED + 8;
+        if (lanes != 0 && lanes != 1 && lanes != 2 && lanes != 4 && !staged) raise(Errc::InvalidArgument, "bad lanes");
+        KernelShape ks = shape_for(staged ? 1 : lanes);
+        if (staged) {
             ks = staged_shape(plan->prog, 227 * 1024);
             if (!ks.staged) raise(Errc::BufferShape, "program tiles do not fit in shared memory");
+            ks.chunk = lanes == PYRIT_SOURCE_STAGED ? 16 : lanes - PYRIT_SOURCE_STAGED;
         }
         const std::string src = generate_cuda(plan->prog, ks);
         const std::string nm = kernel_name(plan->prog, ks);

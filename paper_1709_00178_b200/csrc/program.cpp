@@ -354,10 +354,12 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
 
     // Output parts of the staged kernel (see KernelShape).  Knobs, in order
     // of precedence: CompileOptions, PYRIT_B200_PARTS / _PART_GROUP /
-    // _PART_CSE, the measured tuning table (tuned.tsv next to the library),
-    // and the heuristic: one part; fragment groups of about 48 strips; pair
-    // sharing only while the shared program stays small enough (<= 1000
-    // XORs per column word) for ptxas to keep it spill-free in 255 registers.
+    // _PART_CSE / _THREADS, the measured tuning table (tuned.tsv next to the
+    // library), and the heuristic: the fewest parts that keep <= 64 ring-row
+    // accumulators per thread; fragment groups of about 48 strips; no pair
+    // sharing (its temporaries lengthen live ranges and spill); 512 threads
+    // per CTA when a part's live words (accumulators + one group's strips)
+    // fit the 128 registers that allows, else 256.
     if (opt.parts != 1 && e > 0) {
         const auto env_u = [](const char* name) -> int {
             const char* v = std::getenv(name);
@@ -371,7 +373,11 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
         std::uint32_t R = opt.parts;
         if (!R && env_u("PYRIT_B200_PARTS") > 0) R = static_cast<std::uint32_t>(env_u("PYRIT_B200_PARTS"));
         if (!R && tuned) R = tuned->parts;
-        if (!R) R = 1;
+        const std::uint32_t acc_rows = emb && !crs ? n : w; // accumulators per output row
+        if (!R) {
+            R = 1;
+            while (R < e && (e + R - 1) / R * acc_rows > 64) ++R;
+        }
         R = std::max<std::uint32_t>(1, std::min(R, e));
         std::uint32_t pg = opt.part_group;
         if (!pg && env_u("PYRIT_B200_PART_GROUP") > 0) pg = static_cast<std::uint32_t>(env_u("PYRIT_B200_PART_GROUP"));
@@ -380,6 +386,11 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
         pg = std::max<std::uint32_t>(1, std::min(pg, k));
         int pcse = env_u("PYRIT_B200_PART_CSE");
         if (pcse < 0 && tuned) pcse = tuned->part_cse;
+        if (pcse < 0) pcse = 0;
+        if (!p.staged_threads) {
+            const std::uint32_t live = (e + R - 1) / R * acc_rows + pg * w;
+            p.staged_threads = live <= 96 ? 512 : 256;
+        }
         auto build_parts = [&](bool cse) {
             p.parts.clear();
             p.part_row0.clear();
@@ -398,14 +409,7 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
                 row0 += nrows;
             }
         };
-        if (pcse >= 0) {
-            build_parts(pcse != 0);
-        } else {
-            build_parts(true);
-            std::uint64_t worst = 0;
-            for (const Program& q : p.parts) worst = std::max<std::uint64_t>(worst, q.stats.xors);
-            if (worst > 1000) build_parts(false);
-        }
+        build_parts(pcse != 0);
     }
     return p;
 }
@@ -443,7 +447,8 @@ std::string kernel_name(const Program& p, const KernelShape& ks) {
     fp << kGeneratorVersion << ';' << p.field.w << ',' << p.field.n << ',' << p.field.modulus << ',' << int(p.kind)
        << ',' << p.rows << ',' << p.cols << ',' << p.group << ',' << ks.lanes << ',' << ks.threads << ',' << ks.min_blocks << ','
        << ks.staged << ',' << ks.tile << ',' << ks.stages << ',' << ks.bar_bytes << ',' << p.parts.size() << ','
-       << (p.parts.empty() ? 0u : p.parts[0].group) << ',' << ks.copy << ',' << p.cse << ',' << p.crs << ',';
+       << (p.parts.empty() ? 0u : p.parts[0].group) << ',' << ks.copy << ',' << p.cse << ',' << p.crs << ','
+       << ks.chunk << ',';
     if (p.crs)
         for (std::uint16_t x : p.matrix) fp << 'c' << x;
     for (const Program& q : p.parts) fp << q.rows << '/' << q.cse << '/' << q.stats.xors << ',';
@@ -452,7 +457,8 @@ std::string kernel_name(const Program& p, const KernelShape& ks) {
     char name[112];
     if (ks.staged)
         std::snprintf(name, sizeof name, "pyrit_ring_k%u_e%u_w%u_n%u_%s%ux%u_%016llx", p.cols, p.rows, p.field.w,
-                      p.field.n, ks.copy ? "cpa" : "tma", ks.tile, ks.stages,
+                      p.field.n, !ks.copy ? "tma" : ks.chunk == 16 ? "cpa" : ks.chunk == 8 ? "cpa8_" : "cpa4_",
+                      ks.tile, ks.stages,
                       static_cast<unsigned long long>(fnv1a(fp.str())));
     else
         std::snprintf(name, sizeof name, "pyrit_ring_k%u_e%u_w%u_n%u_L%u_%016llx", p.cols, p.rows, p.field.w,
@@ -475,7 +481,7 @@ KernelShape staged_shape(const Program& p, std::uint32_t smem_limit) {
     // so a strip tile is 1024/R bytes.  The shared-memory ring holds one
     // fragment group of one tile per slot.
     std::vector<std::uint32_t> choices = {256u, 128u};
-    if (p.staged_threads) choices.insert(choices.begin(), p.staged_threads);
+    if (p.staged_threads && p.staged_threads != 256) choices.insert(choices.begin(), p.staged_threads);
     for (std::uint32_t threads : choices) {
         if (threads % R) continue;
         const std::uint32_t tile = 4 * (threads / R);
@@ -489,7 +495,7 @@ KernelShape staged_shape(const Program& p, std::uint32_t smem_limit) {
                 break;
             }
         }
-        if (slots < 2) continue;
+        if (slots < (threads == choices.back() ? 2u : 3u)) continue; // keep >= 2 tiles in flight
         ks.staged = true;
         ks.tile = tile;
         ks.stages = slots;
@@ -545,6 +551,10 @@ static __device__ __forceinline__ void bulk_g2s(u32 dst, const void* src, u32 by
                :: "r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory"); }
 static __device__ __forceinline__ void cpa16(u32 dst, const void* src, u32 n) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(dst), "l"(src), "r"(n) : "memory"); }
+static __device__ __forceinline__ void cpa8(u32 dst, const void* src, u32 n) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" :: "r"(dst), "l"(src), "r"(n) : "memory"); }
+static __device__ __forceinline__ void cpa4(u32 dst, const void* src, u32 n) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" :: "r"(dst), "l"(src), "r"(n) : "memory"); }
 static __device__ __forceinline__ void cpa_arrive(u32 bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(bar) : "memory"); }
 static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
@@ -581,26 +591,27 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
     o << "    const u32 j0 = g2 * " << G << "u;\n";
     o << "    const u32 nstr = (g2 + 1u == NG ? " << k << "u - j0 : " << G << "u) * " << w << "u;\n";
     if (ks.copy) {
-        // every thread copies 16-byte chunks (a strip tile is TILE/16
-        // consecutive chunks: coalesced) and arrives on the slot's FULL
-        // barrier once its copies have landed
-        // lanes are laid out strip-major: LPS lanes cover one strip tile (CPL
-        // chunks each), a warp covers SPW strips per step, warps stride
-        // strips by NW*SPW; chunk validity only depends on the tile
-        const std::uint32_t cps = TILE / 16;
+        // every thread copies CH-byte chunks (16, or 8/4 when the strips are
+        // only that aligned; a strip tile is TILE/CH consecutive chunks:
+        // coalesced) and arrives on the slot's FULL barrier once its copies
+        // have landed.  Lanes are laid out strip-major: LPS lanes cover one
+        // strip tile (CPL chunks each), a warp covers SPW strips per step,
+        // warps stride strips by NW*SPW; chunk validity only depends on the tile
+        const std::uint32_t CH = ks.chunk;
+        const std::uint32_t cps = TILE / CH;
         const std::uint32_t lps = std::min<std::uint32_t>(32, cps), spw = 32 / lps, cpl = cps / lps, nw = T / 32;
         o << "    const u64 rem = a.len - (u64)tt2 * TILE;\n";
         o << "    const u32 vb = (u32)(rem < TILE ? rem : TILE);\n";
         o << "    const u32 lq = lane % " << lps << "u, lsub = lane / " << lps << "u;\n";
         for (std::uint32_t c = 0; c < cpl; ++c)
-            o << "    const u32 n" << c << " = 16u * (lq + " << c * lps << "u) < vb ? 16u : 0u;\n";
+            o << "    const u32 n" << c << " = " << CH << "u * (lq + " << c * lps << "u) < vb ? " << CH << "u : 0u;\n";
         o << "#pragma unroll 1\n";
         o << "    for (u32 l = warp * " << spw << "u + lsub; l < nstr; l += " << nw * spw << "u) {\n";
         o << "      const u32 idx = j0 * " << w << "u + l, j = idx / " << w << "u, s = idx - j * " << w << "u;\n";
-        o << "      const u8* src = a.in[j] + b2 * a.ibp + s * a.S + o + 16u * lq;\n";
-        o << "      const u32 d = dst + l * TILE + 16u * lq;\n";
+        o << "      const u8* src = a.in[j] + b2 * a.ibp + s * a.S + o + " << CH << "u * lq;\n";
+        o << "      const u32 d = dst + l * TILE + " << CH << "u * lq;\n";
         for (std::uint32_t c = 0; c < cpl; ++c)
-            o << "      cpa16(d + " << 16 * c * lps << "u, n" << c << " ? src + " << 16 * c * lps
+            o << "      cpa" << CH << "(d + " << CH * c * lps << "u, n" << c << " ? src + " << CH * c * lps
               << "u : a.in[0] + a.off, n" << c << ");\n";
         o << "    }\n";
         o << "    cpa_arrive(FULL(sl));\n";

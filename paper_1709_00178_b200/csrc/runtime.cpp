@@ -204,20 +204,10 @@ int env_int(const char* name, int dflt) {
     return v ? std::atoi(v) : dflt;
 }
 
-// staged shape for p (optionally overridden by PYRIT_B200_TILE / _STAGES for tuning)
+// staged shape for p (PYRIT_B200_COPY=0 selects the TMA bulk-copy producer)
 KernelShape staged_for(const Program& p) {
     KernelShape ks = staged_shape(p, 227 * 1024);
     ks.copy = env_int("PYRIT_B200_COPY", static_cast<int>(ks.copy)) ? 1u : 0u;
-    const int tile = env_int("PYRIT_B200_TILE", 0), stages = env_int("PYRIT_B200_STAGES", 0);
-    if (ks.staged && (tile || stages)) {
-        if (tile == 256 || tile == 512 || tile == 1024) ks.tile = static_cast<std::uint32_t>(tile);
-        if (stages >= 1 && stages <= 8) ks.stages = static_cast<std::uint32_t>(stages);
-        ks.threads = 32 + ks.tile / 4;
-        const std::uint32_t groups = (p.cols + p.group - 1) / p.group;
-        ks.bar_bytes = (8 * ks.stages * (groups + 1) + 127) / 128 * 128;
-        ks.smem_bytes = ks.bar_bytes + ks.stages * p.cols * p.field.w * ks.tile;
-        if (ks.smem_bytes > 227 * 1024) ks.staged = false;
-    }
     return ks;
 }
 
@@ -248,8 +238,13 @@ KernelShape choose_shape(const Program& p, const std::uint8_t* const* in, std::u
         for (std::uint32_t i = 0; ok && i < p.rows; ++i) ok = aligned(out[i], v);
         return ok;
     };
-    if (kernel_mode() != 1 && all_aligned(16)) {
-        const KernelShape ks = staged_for(p);
+    // staged kernel: cp.async chunks of the widest alignment every pointer,
+    // pitch and the window share (the TMA producer needs 16)
+    const std::uint32_t chunk = all_aligned(16) ? 16 : all_aligned(8) ? 8 : all_aligned(4) ? 4 : 0;
+    if (kernel_mode() != 1 && chunk) {
+        KernelShape ks = staged_for(p);
+        ks.chunk = chunk;
+        if (!ks.copy && chunk != 16) ks.staged = false;
         // short per-stripe windows leave most of a tile idle: the direct
         // kernel streams them better (auto mode only)
         const std::uint64_t tiles = ks.staged ? (len + ks.tile - 1) / ks.tile : 0;

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--scale", type=int, default=1, help="divide the fragment size by this")
+    ap.add_argument("--frag", type=int, default=0, help="fragment bytes (overrides the config's; > L2 working set)")
     ap.add_argument("--rounds", type=int, default=3, help="interleaved repeats per variant (median reported)")
     ap.add_argument("--no-graph", action="store_true", help="launch from Python instead of a captured CUDA graph")
     a = ap.parse_args()
@@ -44,7 +45,7 @@ def main():
     dev = torch.device("cuda", 0)
     wl = WORKLOADS[a.config]
     w = wl.fld.w
-    S = wl.strip // a.scale // 16 * 16
+    S = (a.frag // w if a.frag else wl.strip // a.scale) // 16 * 16
     sym = w * S
     stream = torch.cuda.current_stream(dev).cuda_stream
     full = torch.empty((wl.k + wl.m, sym), dtype=torch.uint8, device=dev)
