@@ -269,7 +269,7 @@ int pyrit_plan_source(const pyrit_plan* plan, uint32_t lanes, char* buf, size_t 
         const bool staged = lanes == PYRIT_SOURCE_STAGED || lanes == PYRIT_SOURCE_STAGED + 4 ||
                             lanes == PYRIT_SOURCE_STAGED + 8;
         if (lanes != 0 && lanes != 1 && lanes != 2 && lanes != 4 && !staged) raise(Errc::InvalidArgument, "bad lanes");
-        KernelShape ks = shape_for(staged ? 1 : lanes);
+        KernelShape ks = direct_shape(plan->prog, staged ? 1 : lanes);
         if (staged) {
             ks = staged_shape(plan->prog, 227 * 1024);
             if (!ks.staged) raise(Errc::BufferShape, "program tiles do not fit in shared memory");

@@ -25,7 +25,7 @@ namespace {
 
 constexpr std::uint32_t kNone = 0xFFFFFFFFu;
 // bump whenever generated code changes for the same program (prebuilt cubins are keyed by name)
-constexpr int kGeneratorVersion = 6;
+constexpr int kGeneratorVersion = 8;
 
 // Greedy pair elimination over XOR targets.  Each target is a set of
 // variable ids; the most frequent pair (ties: smallest ids) becomes a new
@@ -374,15 +374,17 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
         if (!R && env_u("PYRIT_B200_PARTS") > 0) R = static_cast<std::uint32_t>(env_u("PYRIT_B200_PARTS"));
         if (!R && tuned) R = tuned->parts;
         const std::uint32_t acc_rows = emb && !crs ? n : w; // accumulators per output row
-        if (!R) {
+        if (!R) { // a power of two (it must divide the CTA) no larger than e
             R = 1;
-            while (R < e && (e + R - 1) / R * acc_rows > 64) ++R;
+            while (2 * R <= e && (e + R - 1) / R * acc_rows > 64) R *= 2;
         }
         R = std::max<std::uint32_t>(1, std::min(R, e));
         std::uint32_t pg = opt.part_group;
         if (!pg && env_u("PYRIT_B200_PART_GROUP") > 0) pg = static_cast<std::uint32_t>(env_u("PYRIT_B200_PART_GROUP"));
         if (!pg && tuned) pg = tuned->part_group;
-        if (!pg) pg = std::max<std::uint32_t>(1, (48 + w / 2) / w);
+        // ~48 strips per group; ~24 when the rows are split (those programs
+        // also run as direct split kernels, 128 registers per thread)
+        if (!pg) pg = std::max<std::uint32_t>(1, ((R > 1 ? 24 : 48) + w / 2) / w);
         pg = std::max<std::uint32_t>(1, std::min(pg, k));
         int pcse = env_u("PYRIT_B200_PART_CSE");
         if (pcse < 0 && tuned) pcse = tuned->part_cse;
@@ -448,7 +450,7 @@ std::string kernel_name(const Program& p, const KernelShape& ks) {
        << ',' << p.rows << ',' << p.cols << ',' << p.group << ',' << ks.lanes << ',' << ks.threads << ',' << ks.min_blocks << ','
        << ks.staged << ',' << ks.tile << ',' << ks.stages << ',' << ks.bar_bytes << ',' << p.parts.size() << ','
        << (p.parts.empty() ? 0u : p.parts[0].group) << ',' << ks.copy << ',' << p.cse << ',' << p.crs << ','
-       << ks.chunk << ',';
+       << ks.chunk << ',' << ks.split << ',';
     if (p.crs)
         for (std::uint16_t x : p.matrix) fp << 'c' << x;
     for (const Program& q : p.parts) fp << q.rows << '/' << q.cse << '/' << q.stats.xors << ',';
@@ -461,8 +463,9 @@ std::string kernel_name(const Program& p, const KernelShape& ks) {
                       ks.tile, ks.stages,
                       static_cast<unsigned long long>(fnv1a(fp.str())));
     else
-        std::snprintf(name, sizeof name, "pyrit_ring_k%u_e%u_w%u_n%u_L%u_%016llx", p.cols, p.rows, p.field.w,
-                      p.field.n, ks.lanes, static_cast<unsigned long long>(fnv1a(fp.str())));
+        std::snprintf(name, sizeof name, "pyrit_ring_k%u_e%u_w%u_n%u_L%u%s_%016llx", p.cols, p.rows, p.field.w,
+                      p.field.n, ks.lanes, ks.split > 1 ? ("p" + std::to_string(ks.split)).c_str() : "",
+                      static_cast<unsigned long long>(fnv1a(fp.str())));
     return name;
 }
 
@@ -697,30 +700,40 @@ std::string generate_cuda(const Program& p, const KernelShape& ks) {
     const std::uint32_t L = ks.lanes == 0 ? 1 : ks.lanes;
     const bool bytes = ks.lanes == 0;
     const std::uint32_t V = bytes ? 1 : 4 * L; // bytes per thread per strip
+    // split: the output rows are divided over R thread groups (p.parts) that
+    // walk the same column words; every group loads all input strips, the
+    // first touch of a line fills L1 and the other groups hit it, so HBM
+    // still sees each input byte once while no thread holds more than one
+    // part's accumulators (large codes otherwise spill)
+    const std::uint32_t R = ks.split > 1 ? static_cast<std::uint32_t>(p.parts.size()) : 1;
+    const std::uint32_t CPB = ks.threads / R; // column threads per block
     std::ostringstream o;
     o << "// generated by pyrit_b200 program compiler: field w=" << p.field.w << " n=" << p.field.n << " p=0x"
       << std::hex << p.field.modulus << std::dec << ", " << p.rows << "x" << p.cols << " ring matrix, "
       << p.stats.xors << " XORs (naive ring program " << p.stats.naive_xors << ", reference schedule "
-      << p.stats.ref_region_ops << " region ops)\n";
+      << p.stats.ref_region_ops << " region ops)" << (R > 1 ? ", rows split over " + std::to_string(R) + " thread groups" : "")
+      << "\n";
     o << "typedef unsigned int u32; typedef unsigned long long u64; typedef unsigned char u8;\n";
     // nb stripes of nwords column words each; the grid stride advances
     // (stripe, word) by (sq, sr) = divmod(stride, nwords), precomputed on the host
     o << "struct Args { const u8* in[" << p.cols << "]; u8* out[" << p.rows
       << "]; u64 S; u64 off; u64 nwords; u64 nb; u64 ibp; u64 obp; u64 sq; u64 sr; };\n";
-    // loads: read-only, no L1 allocation (streamed once); stores: evict-first
+    // loads: read-only, no L1 allocation (streamed once) -- L1-cached when
+    // split, the other row groups re-read the line; stores: evict-first
+    const std::string l1 = R > 1 ? "" : ".L1::no_allocate";
     if (bytes) {
-        o << "#define LD(v, p) asm(\"ld.global.nc.L1::no_allocate.u8 %0, [%1];\" : \"=r\"(v) : \"l\"(p))\n";
+        o << "#define LD(v, p) asm(\"ld.global.nc" << l1 << ".u8 %0, [%1];\" : \"=r\"(v) : \"l\"(p))\n";
         o << "#define ST(p, v) asm volatile(\"st.global.cs.u8 [%0], %1;\" :: \"l\"(p), \"r\"(v) : \"memory\")\n";
     } else if (L == 1) {
-        o << "#define LD(v, p) asm(\"ld.global.nc.L1::no_allocate.b32 %0, [%1];\" : \"=r\"(v##_0) : \"l\"(p))\n";
+        o << "#define LD(v, p) asm(\"ld.global.nc" << l1 << ".b32 %0, [%1];\" : \"=r\"(v##_0) : \"l\"(p))\n";
         o << "#define ST(p, v) asm volatile(\"st.global.cs.b32 [%0], %1;\" :: \"l\"(p), \"r\"(v##_0) : \"memory\")\n";
     } else if (L == 2) {
-        o << "#define LD(v, p) asm(\"ld.global.nc.L1::no_allocate.v2.b32 {%0, %1}, [%2];\" : \"=r\"(v##_0), "
+        o << "#define LD(v, p) asm(\"ld.global.nc" << l1 << ".v2.b32 {%0, %1}, [%2];\" : \"=r\"(v##_0), "
              "\"=r\"(v##_1) : \"l\"(p))\n";
         o << "#define ST(p, v) asm volatile(\"st.global.cs.v2.b32 [%0], {%1, %2};\" :: \"l\"(p), \"r\"(v##_0), "
              "\"r\"(v##_1) : \"memory\")\n";
     } else {
-        o << "#define LD(v, p) asm(\"ld.global.nc.L1::no_allocate.v4.b32 {%0, %1, %2, %3}, [%4];\" : "
+        o << "#define LD(v, p) asm(\"ld.global.nc" << l1 << ".v4.b32 {%0, %1, %2, %3}, [%4];\" : "
              "\"=r\"(v##_0), \"=r\"(v##_1), \"=r\"(v##_2), \"=r\"(v##_3) : \"l\"(p))\n";
         o << "#define ST(p, v) asm volatile(\"st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};\" :: \"l\"(p), "
              "\"r\"(v##_0), \"r\"(v##_1), \"r\"(v##_2), \"r\"(v##_3) : \"memory\")\n";
@@ -729,53 +742,71 @@ std::string generate_cuda(const Program& p, const KernelShape& ks) {
     o << "extern \"C\" __global__ void __launch_bounds__(" << ks.threads << ", " << ks.min_blocks << ") " << name
       << "(const Args a)\n{\n";
     o << "  const u64 S = a.S;\n";
-    o << "  const u64 c0 = (u64)blockIdx.x * " << ks.threads << "u + threadIdx.x;\n";
-    o << "  u64 b = c0 / a.nwords, cw = c0 - b * a.nwords;\n";
-    o << "  while (b < a.nb) {\n";
-    o << "    const u64 o = a.off + cw * " << V << "u;\n";
-    o << "    const u64 oi = o + b * a.ibp, oo = o + b * a.obp;\n";
+    o << "  const u32 part = threadIdx.x / " << CPB << "u;\n";
+    o << "  const u64 c0 = (u64)blockIdx.x * " << CPB << "u + threadIdx.x % " << CPB << "u;\n";
     auto var = [&](std::uint32_t v, std::uint32_t l) {
         std::string s = "v" + std::to_string(v);
         if (!bytes) s += "_" + std::to_string(l);
         return s;
     };
-    std::vector<bool> frag_ptr(p.cols, false), out_ptr(p.rows, false);
-    for (const Instr& ins : p.code) {
-        if (ins.op == Instr::Load) {
-            if (!frag_ptr[ins.sym]) {
-                o << "    const u8* i" << ins.sym << " = a.in[" << ins.sym << "] + oi;\n";
-                frag_ptr[ins.sym] = true;
+    for (std::uint32_t r = 0; r < R; ++r) {
+        const Program& q = R > 1 ? p.parts[r] : p;
+        const std::uint32_t row0 = R > 1 ? p.part_row0[r] : 0;
+        o << "  " << (r ? "else if" : "if") << " (part == " << r << "u) {\n";
+        o << "  u64 b = c0 / a.nwords, cw = c0 - b * a.nwords;\n";
+        o << "  while (b < a.nb) {\n";
+        o << "    const u64 o = a.off + cw * " << V << "u;\n";
+        o << "    const u64 oi = o + b * a.ibp, oo = o + b * a.obp;\n";
+        std::vector<bool> frag_ptr(q.cols, false), out_ptr(q.rows, false);
+        // split kernels: one fragment group's loads at a time (no prefetch of
+        // the next group) so a part stays within the 128 registers of 2 CTAs/SM
+        std::vector<Instr> seq;
+        if (R > 1) {
+            for (std::size_t g = 0; g < q.group_loads.size(); ++g) {
+                seq.insert(seq.end(), q.group_loads[g].begin(), q.group_loads[g].end());
+                seq.insert(seq.end(), q.group_compute[g].begin(), q.group_compute[g].end());
             }
-            o << "    u32 ";
-            for (std::uint32_t l = 0; l < L; ++l) o << (l ? ", " : "") << var(ins.dst, l);
-            o << "; LD(v" << ins.dst << ", i" << ins.sym;
-            if (ins.strip) o << " + " << ins.strip << "u * S";
-            o << ");\n";
-        } else if (ins.op == Instr::Xor) {
-            for (std::uint32_t l = 0; l < L; ++l) {
-                o << "    const u32 " << var(ins.dst, l) << " = ";
-                for (std::size_t s = 0; s < ins.src.size(); ++s) o << (s ? " ^ " : "") << var(ins.src[s], l);
-                o << ";\n";
-            }
-        } else {
-            if (!out_ptr[ins.sym]) {
-                o << "    u8* q" << ins.sym << " = a.out[" << ins.sym << "] + oo;\n";
-                out_ptr[ins.sym] = true;
-            }
-            o << "    { u32 ";
-            for (std::uint32_t l = 0; l < L; ++l) {
-                o << (l ? ", " : "") << "x" << (bytes ? "" : "_" + std::to_string(l)) << " = ";
-                if (ins.src.empty()) o << "0u";
-                for (std::size_t s = 0; s < ins.src.size(); ++s) o << (s ? " ^ " : "") << var(ins.src[s], l);
-            }
-            o << "; ST(q" << ins.sym;
-            if (ins.strip) o << " + " << ins.strip << "u * S";
-            o << ", x); }\n";
+            seq.insert(seq.end(), q.tail.begin(), q.tail.end());
         }
+        for (const Instr& ins : R > 1 ? seq : q.code) {
+            if (ins.op == Instr::Load) {
+                if (!frag_ptr[ins.sym]) {
+                    o << "    const u8* i" << ins.sym << " = a.in[" << ins.sym << "] + oi;\n";
+                    frag_ptr[ins.sym] = true;
+                }
+                o << "    u32 ";
+                for (std::uint32_t l = 0; l < L; ++l) o << (l ? ", " : "") << var(ins.dst, l);
+                o << "; LD(v" << ins.dst << ", i" << ins.sym;
+                if (ins.strip) o << " + " << ins.strip << "u * S";
+                o << ");\n";
+            } else if (ins.op == Instr::Xor) {
+                for (std::uint32_t l = 0; l < L; ++l) {
+                    o << "    const u32 " << var(ins.dst, l) << " = ";
+                    for (std::size_t s = 0; s < ins.src.size(); ++s) o << (s ? " ^ " : "") << var(ins.src[s], l);
+                    o << ";\n";
+                }
+            } else {
+                const std::uint32_t row = row0 + ins.sym;
+                if (!out_ptr[ins.sym]) {
+                    o << "    u8* q" << row << " = a.out[" << row << "] + oo;\n";
+                    out_ptr[ins.sym] = true;
+                }
+                o << "    { u32 ";
+                for (std::uint32_t l = 0; l < L; ++l) {
+                    o << (l ? ", " : "") << "x" << (bytes ? "" : "_" + std::to_string(l)) << " = ";
+                    if (ins.src.empty()) o << "0u";
+                    for (std::size_t s = 0; s < ins.src.size(); ++s) o << (s ? " ^ " : "") << var(ins.src[s], l);
+                }
+                o << "; ST(q" << row;
+                if (ins.strip) o << " + " << ins.strip << "u * S";
+                o << ", x); }\n";
+            }
+        }
+        o << "    b += a.sq; cw += a.sr;\n";
+        o << "    if (cw >= a.nwords) { cw -= a.nwords; ++b; }\n";
+        o << "  }\n  }\n";
     }
-    o << "    b += a.sq; cw += a.sr;\n";
-    o << "    if (cw >= a.nwords) { cw -= a.nwords; ++b; }\n";
-    o << "  }\n}\n";
+    o << "}\n";
     return o.str();
 }
 

@@ -118,6 +118,7 @@ struct KernelShape {
     std::uint32_t smem_bytes = 0;   // staged: dynamic shared memory per CTA
     std::uint32_t copy = 1;         // staged: 0 = TMA cp.async.bulk by warp 0, 1 = cp.async by every thread
     std::uint32_t chunk = 16;       // staged cp.async: bytes per copy (16; 8 or 4 for less aligned strips)
+    std::uint32_t split = 0;        // direct: rows split over p.parts.size() thread groups (0/1 = no split)
 };
 std::string kernel_name(const Program& p, const KernelShape& ks);
 std::string generate_cuda(const Program& p, const KernelShape& ks);

@@ -184,6 +184,13 @@ std::string kernel_dir() {
 std::uint64_t jit_compiles() { return g_jit.load(); }
 std::uint64_t kernel_launches() { return g_launches.load(); }
 
+KernelShape direct_shape(const Program& p, std::uint32_t lanes) {
+    KernelShape ks = shape_for(lanes);
+    const std::uint32_t R = static_cast<std::uint32_t>(p.parts.size());
+    if (R > 1 && ks.threads % R == 0 && ks.threads / R >= 32) { ks.split = R; ks.min_blocks = 2; }
+    return ks;
+}
+
 KernelShape shape_for(std::uint32_t lanes) {
     KernelShape ks;
     ks.lanes = lanes;
@@ -253,20 +260,22 @@ KernelShape choose_shape(const Program& p, const std::uint8_t* const* in, std::u
         if (ks.staged && fits && (dense || kernel_mode() == 2)) return ks;
     }
     // direct mode: widest vector the alignment of every pointer, the strip
-    // pitch and the window allows; byte mode otherwise
+    // pitch and the window allows; byte mode otherwise.  Programs compiled
+    // with several output parts (large codes) split their rows over thread
+    // groups instead of holding every accumulator in one thread.
     std::uint32_t lanes = 0;
     for (std::uint32_t l = preferred_lanes(); l >= 1; l /= 2)
         if (all_aligned(4ull * l)) {
             lanes = l;
             break;
         }
-    return shape_for(lanes);
+    return direct_shape(p, lanes);
 }
 
 std::string prepare_program(const Program& p, std::uint32_t lanes) {
     int dev = 0;
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
-    KernelShape ks = shape_for(lanes);
+    KernelShape ks = direct_shape(p, lanes);
     if (kernel_mode() != 1) {
         const KernelShape st = staged_for(p);
         if (st.staged) ks = st;
@@ -302,6 +311,7 @@ LaunchInfo launch_batch(const Program& p, const std::uint8_t* const* in, std::ui
     tail[4] = in_pitch;
     tail[5] = out_pitch;
     const std::uint64_t cap = std::uint64_t(k.sms) * std::uint64_t(k.blocks_per_sm);
+    const std::uint64_t cpb = ks.split > 1 ? ks.threads / ks.split : ks.threads; // column threads per block
     std::uint64_t want, nwords = 0;
     if (ks.staged) {
         tail[2] = len; // bytes; tiles of ks.tile bytes per strip
@@ -310,11 +320,11 @@ LaunchInfo launch_batch(const Program& p, const std::uint8_t* const* in, std::ui
         const std::uint64_t vbytes = ks.lanes ? 4ull * ks.lanes : 1ull;
         nwords = len / vbytes;
         tail[2] = nwords;
-        want = (nwords * nb + ks.threads - 1) / ks.threads;
+        want = (nwords * nb + cpb - 1) / cpb;
     }
     const unsigned blocks = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min(want, cap)));
     if (!ks.staged) {
-        const std::uint64_t stride = std::uint64_t(blocks) * ks.threads;
+        const std::uint64_t stride = std::uint64_t(blocks) * cpb;
         tail[6] = stride / nwords;
         tail[7] = stride % nwords;
     }

@@ -60,6 +60,8 @@ std::uint64_t jit_compiles(); // number of NVRTC compilations performed so far
 std::uint64_t kernel_launches(); // number of generated-kernel launches so far
 
 KernelShape shape_for(std::uint32_t lanes);
+// direct-kernel shape for p: rows split over thread groups when p has several output parts
+KernelShape direct_shape(const Program& p, std::uint32_t lanes);
 
 // 0 = auto (TMA-staged whenever alignment allows), 1 = direct LDG only, 2 = staged
 int kernel_mode();

@@ -273,3 +273,26 @@ def test_crs_baseline_kernel(cuda, cfg, mode):
         np.testing.assert_array_equal(out.cpu().numpy(), oracle_encode(f, m, src))
     finally:
         L.check(lib.pyrit_set_kernel_mode(0))
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("k,r,kind,ss", [(40, 20, 0, 4104), (40, 20, 0, 96 * 43), (20, 40, 1, 4104),
+                                         (20, 40, 1, 8 * 6 * 35)])
+def test_large_codes_split_rows(cuda, mode, k, r, kind, ss):
+    """The paper's (60,40) and (60,20) GF(2^6) codes: rows split over thread groups
+    (direct kernel) or warp groups (staged; 4/8/16-byte cp.async chunks)."""
+    lib = L.load()
+    L.check(lib.pyrit_set_kernel_mode(mode))
+    try:
+        code = P.CodeSpec(k, r, G64, P.TransformKind(kind))
+        data = rand_symbols(k, ss, k * r + ss)
+        C = P.cauchy_parity_matrix(code)
+        par = dev_encode(cuda, code, data)
+        np.testing.assert_array_equal(par, oracle_ring(G64, C, data, kind=kind))
+        full = np.concatenate([data, par])
+        erased = sorted(random.Random(ss).sample(range(k + r), min(k, r)))
+        work = full.copy()
+        work[erased] = 0
+        np.testing.assert_array_equal(dev_decode(cuda, code, work, erased), full)
+    finally:
+        L.check(lib.pyrit_set_kernel_mode(0))
