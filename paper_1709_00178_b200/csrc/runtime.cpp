@@ -252,12 +252,14 @@ KernelShape choose_shape(const Program& p, const std::uint8_t* const* in, std::u
         KernelShape ks = staged_for(p);
         ks.chunk = chunk;
         if (!ks.copy && chunk != 16) ks.staged = false;
-        // short per-stripe windows leave most of a tile idle: the direct
-        // kernel streams them better (auto mode only)
+        // auto mode keeps the staged kernel where it measured faster than the
+        // direct one (profiles/r01_s2/sizes_*): 16-byte chunks, at most two
+        // output parts, and per-stripe windows that fill at least half a tile
         const std::uint64_t tiles = ks.staged ? (len + ks.tile - 1) / ks.tile : 0;
         const bool dense = tiles && 2 * len >= tiles * ks.tile;
         const bool fits = tiles * nb < (std::uint64_t(1) << 32);
-        if (ks.staged && fits && (dense || kernel_mode() == 2)) return ks;
+        const bool suited = dense && chunk == 16 && p.parts.size() <= 2;
+        if (ks.staged && fits && (suited || kernel_mode() == 2)) return ks;
     }
     // direct mode: widest vector the alignment of every pointer, the strip
     // pitch and the window allows; byte mode otherwise.  Programs compiled
