@@ -7,6 +7,9 @@
 
 #include <algorithm>
 #include <cerrno>
+#include <condition_variable>
+#include <functional>
+#include <thread>
 #include <climits>
 #include <cstring>
 #include <filesystem>
@@ -112,6 +115,113 @@ void pwritev_full(int fd, std::vector<iovec>& iov, std::uint64_t off, const std:
         }
         while (i < iov.size() && iov[i].iov_len == 0) ++i;
     }
+}
+
+// ---- host I/O workers: shard files are read and written in parallel ------
+
+class IoPool {
+public:
+    IoPool() {
+        const unsigned n = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        for (unsigned i = 0; i + 1 < n; ++i) workers_.emplace_back([this] { loop(); });
+    }
+    ~IoPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& th : workers_) th.join();
+    }
+    // f(0..n-1) on the workers and the caller; rethrows the first failure
+    void run(std::size_t n, const std::function<void(std::size_t)>& f) {
+        if (n == 0) return;
+        Job job{&f, n, 0, 0, nullptr};
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            jobs_.push_back(&job);
+        }
+        cv_.notify_all();
+        work(job);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return job.finished == job.n; });
+        jobs_.erase(std::remove(jobs_.begin(), jobs_.end(), &job), jobs_.end());
+        if (job.error) std::rethrow_exception(job.error);
+    }
+
+private:
+    struct Job {
+        const std::function<void(std::size_t)>* f;
+        std::size_t n, next = 0, finished = 0;
+        std::exception_ptr error;
+    };
+    void work(Job& job) {
+        for (;;) {
+            std::size_t i;
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (job.next >= job.n) return;
+                i = job.next++;
+            }
+            std::exception_ptr err;
+            try {
+                (*job.f)(i);
+            } catch (...) {
+                err = std::current_exception();
+            }
+            std::lock_guard<std::mutex> lk(mu_);
+            if (err && !job.error) job.error = err;
+            if (++job.finished == job.n) done_cv_.notify_all();
+        }
+    }
+    void loop() {
+        for (;;) {
+            Job* job = nullptr;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] {
+                    if (stop_) return true;
+                    for (Job* j : jobs_)
+                        if (j->next < j->n) return true;
+                    return false;
+                });
+                if (stop_) return;
+                for (Job* j : jobs_)
+                    if (j->next < j->n) {
+                        job = j;
+                        break;
+                    }
+            }
+            work(*job);
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    std::vector<Job*> jobs_;
+    std::vector<std::thread> workers_;
+    bool stop_ = false;
+};
+
+IoPool& io_pool() {
+    static IoPool pool;
+    return pool;
+}
+
+// pread of [off, off+len) split over the pool; returns the bytes read
+std::size_t pread_parallel(int fd, std::uint8_t* dst, std::size_t len, std::uint64_t off, const std::string& path) {
+    constexpr std::size_t kPiece = 8u << 20;
+    const std::size_t pieces = (len + kPiece - 1) / kPiece;
+    std::vector<std::size_t> got(pieces, 0);
+    io_pool().run(pieces, [&](std::size_t i) {
+        const std::size_t b = i * kPiece, n = std::min(kPiece, len - b);
+        got[i] = pread_full(fd, dst + b, n, off + b, path);
+    });
+    std::size_t total = 0;
+    for (std::size_t i = 0; i < pieces; ++i) {
+        total += got[i];
+        if (got[i] < std::min(kPiece, len - i * kPiece)) break; // end of file
+    }
+    return total;
 }
 
 // ---- per-device staging: pinned host + device buffers, one stream per stage
@@ -336,8 +446,8 @@ std::vector<std::string> encode_file(const std::string& input, const std::string
         if (pending[c % kStages].valid()) pending[c % kStages].get();
         const std::uint64_t nb = std::min(B, stripes - s0);
         const std::uint64_t bytes = nb * stripe_bytes, at = s0 * stripe_bytes;
-        const std::size_t got = pread_full(in.fd, st.h_in, static_cast<std::size_t>(std::min(bytes, length - at)), at,
-                                           input);
+        const std::size_t got = pread_parallel(in.fd, st.h_in, static_cast<std::size_t>(std::min(bytes, length - at)),
+                                               at, input);
         std::memset(st.h_in + got, 0, static_cast<std::size_t>(bytes - got)); // container.hpp:209-211
         if (prog) {
             check_cuda(cudaMemcpyAsync(st.d_in, st.h_in, bytes, cudaMemcpyHostToDevice, st.stream), "H2D");
@@ -350,14 +460,15 @@ std::vector<std::string> encode_file(const std::string& input, const std::string
             check_cuda(cudaSetDevice(device), "cudaSetDevice");
             check_cuda(cudaStreamSynchronize(sp->stream), "cudaStreamSynchronize");
             const std::uint64_t at_shard = kHeaderSize + s0 * ss;
-            std::vector<iovec> iov(nb);
-            for (std::uint32_t j = 0; j < k; ++j) {
-                iov.resize(nb);
-                for (std::uint64_t b = 0; b < nb; ++b) iov[b] = {sp->h_in + b * stripe_bytes + j * ss, ss};
-                pwritev_full(out[j].fd, iov, at_shard, paths[j]);
-            }
-            for (std::uint32_t i = 0; i < r; ++i)
-                pwrite_full(out[k + i].fd, sp->h_out + i * nb * ss, nb * ss, at_shard, paths[k + i]);
+            io_pool().run(total, [&](std::size_t i) { // one shard file per task
+                if (i < k) {
+                    std::vector<iovec> iov(nb);
+                    for (std::uint64_t b = 0; b < nb; ++b) iov[b] = {sp->h_in + b * stripe_bytes + i * ss, ss};
+                    pwritev_full(out[i].fd, iov, at_shard, paths[i]);
+                } else {
+                    pwrite_full(out[i].fd, sp->h_out + (i - k) * nb * ss, nb * ss, at_shard, paths[i]);
+                }
+            });
         });
     }
     for (auto& p : pending)
@@ -453,12 +564,12 @@ void decode_file(const std::vector<std::string>& shard_paths, const std::string&
         if (pending[c % kStages].valid()) pending[c % kStages].get();
         const std::uint64_t nb = std::min(B, stripes - s0);
         // survivor-major staging: survivor i's nb symbols are contiguous
-        for (std::size_t i = 0; i < surv.size(); ++i) {
+        io_pool().run(surv.size(), [&](std::size_t i) {
             const Loaded& L = byindex[surv[i]];
             const std::size_t want = static_cast<std::size_t>(nb * ss);
             if (pread_full(L.fd.fd, st.h_in + i * nb * ss, want, kHeaderSize + s0 * ss, L.path) != want)
                 raise(Errc::IoError, "short read on " + L.path);
-        }
+        });
         if (dp.prog) {
             check_cuda(cudaMemcpyAsync(st.d_in, st.h_in, k * nb * ss, cudaMemcpyHostToDevice, st.stream), "H2D");
             for (std::uint32_t i = 0; i < k; ++i) din[i] = st.d_in + i * nb * ss;
@@ -469,20 +580,25 @@ void decode_file(const std::vector<std::string>& shard_paths, const std::string&
         pending[c % kStages] = std::async(std::launch::async, [&, s0, nb, sp = &st] {
             check_cuda(cudaSetDevice(device), "cudaSetDevice");
             check_cuda(cudaStreamSynchronize(sp->stream), "cudaStreamSynchronize");
-            const std::uint64_t at = s0 * stripe_bytes;
-            if (at >= length) return;
-            std::vector<iovec> iov;
-            iov.reserve(nb * k);
-            std::uint64_t remaining = length - at;
-            for (std::uint64_t b = 0; b < nb && remaining; ++b)
-                for (std::uint32_t j = 0; j < k && remaining; ++j) {
-                    const std::uint64_t take = std::min<std::uint64_t>(ss, remaining);
-                    std::uint8_t* src = from_in[j] >= 0 ? sp->h_in + (from_in[j] * nb + b) * ss
-                                                        : sp->h_out + (from_out[j] * nb + b) * ss;
-                    iov.push_back({src, static_cast<std::size_t>(take)});
-                    remaining -= take;
-                }
-            pwritev_full(out.fd, iov, at, output);
+            // the output range of this chunk, written by several tasks (runs of stripes)
+            const std::uint64_t pieces = std::min<std::uint64_t>(nb, 16);
+            io_pool().run(pieces, [&](std::size_t q) {
+                const std::uint64_t b0 = nb * q / pieces, b1 = nb * (q + 1) / pieces;
+                const std::uint64_t at = (s0 + b0) * stripe_bytes;
+                if (at >= length) return;
+                std::vector<iovec> iov;
+                iov.reserve((b1 - b0) * k);
+                std::uint64_t remaining = std::min(length - at, (b1 - b0) * stripe_bytes);
+                for (std::uint64_t b = b0; b < b1 && remaining; ++b)
+                    for (std::uint32_t j = 0; j < k && remaining; ++j) {
+                        const std::uint64_t take = std::min<std::uint64_t>(ss, remaining);
+                        std::uint8_t* src = from_in[j] >= 0 ? sp->h_in + (from_in[j] * nb + b) * ss
+                                                            : sp->h_out + (from_out[j] * nb + b) * ss;
+                        iov.push_back({src, static_cast<std::size_t>(take)});
+                        remaining -= take;
+                    }
+                pwritev_full(out.fd, iov, at, output);
+            });
         });
     }
     for (auto& p : pending)
