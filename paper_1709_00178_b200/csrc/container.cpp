@@ -137,13 +137,17 @@ public:
     void run(std::size_t n, const std::function<void(std::size_t)>& f) {
         if (n == 0) return;
         Job job{&f, n, 0, 0, nullptr};
-        {
-            std::lock_guard<std::mutex> lk(mu_);
-            jobs_.push_back(&job);
-        }
-        cv_.notify_all();
-        work(job);
         std::unique_lock<std::mutex> lk(mu_);
+        jobs_.push_back(&job);
+        cv_.notify_all();
+        // an item is claimed (next++) under the lock and counted as finished
+        // only after it ran, so the job outlives every worker touching it
+        while (job.next < job.n) {
+            const std::size_t i = job.next++;
+            lk.unlock();
+            execute(job, i);
+            lk.lock();
+        }
         done_cv_.wait(lk, [&] { return job.finished == job.n; });
         jobs_.erase(std::remove(jobs_.begin(), jobs_.end(), &job), jobs_.end());
         if (job.error) std::rethrow_exception(job.error);
@@ -152,47 +156,39 @@ public:
 private:
     struct Job {
         const std::function<void(std::size_t)>* f;
-        std::size_t n, next = 0, finished = 0;
+        std::size_t n, next, finished;
         std::exception_ptr error;
     };
-    void work(Job& job) {
-        for (;;) {
-            std::size_t i;
-            {
-                std::lock_guard<std::mutex> lk(mu_);
-                if (job.next >= job.n) return;
-                i = job.next++;
-            }
-            std::exception_ptr err;
-            try {
-                (*job.f)(i);
-            } catch (...) {
-                err = std::current_exception();
-            }
-            std::lock_guard<std::mutex> lk(mu_);
-            if (err && !job.error) job.error = err;
-            if (++job.finished == job.n) done_cv_.notify_all();
+    // runs item i of job (claimed by the caller) and records completion
+    void execute(Job& job, std::size_t i) {
+        std::exception_ptr err;
+        try {
+            (*job.f)(i);
+        } catch (...) {
+            err = std::current_exception();
         }
+        std::lock_guard<std::mutex> lk(mu_);
+        if (err && !job.error) job.error = err;
+        if (++job.finished == job.n) done_cv_.notify_all();
     }
     void loop() {
+        std::unique_lock<std::mutex> lk(mu_);
         for (;;) {
             Job* job = nullptr;
-            {
-                std::unique_lock<std::mutex> lk(mu_);
-                cv_.wait(lk, [&] {
-                    if (stop_) return true;
-                    for (Job* j : jobs_)
-                        if (j->next < j->n) return true;
-                    return false;
-                });
-                if (stop_) return;
+            cv_.wait(lk, [&] {
+                if (stop_) return true;
                 for (Job* j : jobs_)
                     if (j->next < j->n) {
                         job = j;
-                        break;
+                        return true;
                     }
-            }
-            work(*job);
+                return false;
+            });
+            if (stop_) return;
+            const std::size_t i = job->next++;
+            lk.unlock();
+            execute(*job, i);
+            lk.lock();
         }
     }
     std::mutex mu_;
