@@ -80,6 +80,8 @@ typedef struct pyrit_plan_stats {
     uint64_t xors;             /* 2-input XORs of the compiled program */
     uint64_t loads, stores;    /* strip words read / written per column word */
     uint32_t group;            /* input symbols whose strips are live together */
+    uint32_t parts;            /* output parts (row groups) of the staged / split kernels */
+    uint64_t part_xors;        /* 2-input XORs per column word summed over the parts */
 } pyrit_plan_stats;
 
 typedef struct pyrit_plan pyrit_plan;

@@ -27,7 +27,8 @@ class pyrit_code(C.Structure):
 class pyrit_plan_stats(C.Structure):
     _fields_ = [("rows", C.c_uint32), ("cols", C.c_uint32), ("matrix_ones", C.c_uint64),
                 ("ref_region_ops", C.c_uint64), ("naive_xors", C.c_uint64), ("xors", C.c_uint64),
-                ("loads", C.c_uint64), ("stores", C.c_uint64), ("group", C.c_uint32)]
+                ("loads", C.c_uint64), ("stores", C.c_uint64), ("group", C.c_uint32), ("parts", C.c_uint32),
+                ("part_xors", C.c_uint64)]
 
 
 SOURCE_STAGED = 100

@@ -242,6 +242,9 @@ int pyrit_plan_get_stats(const pyrit_plan* plan, pyrit_plan_stats* out) {
         out->loads = s.loads;
         out->stores = s.stores;
         out->group = plan->prog.group;
+        out->parts = static_cast<uint32_t>(plan->prog.parts.size());
+        out->part_xors = 0;
+        for (const Program& q : plan->prog.parts) out->part_xors += q.stats.xors;
     });
 }
 

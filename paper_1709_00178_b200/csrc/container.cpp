@@ -1,6 +1,7 @@
 #include "container.hpp"
 
 #include <fcntl.h>
+#include <sys/mman.h>
 #include <sys/stat.h>
 #include <sys/uio.h>
 #include <unistd.h>
@@ -527,8 +528,25 @@ void decode_file(const std::vector<std::string>& shard_paths, const std::string&
         raise(Errc::InsufficientShards,
               "have " + std::to_string(k + r - erased.size()) + " shards, need " + std::to_string(k));
 
-    Fd out(::open(output.c_str(), O_WRONLY | O_CREAT | O_TRUNC | O_CLOEXEC, 0644));
+    Fd out(::open(output.c_str(), O_RDWR | O_CREAT | O_TRUNC | O_CLOEXEC, 0644));
     if (out.fd < 0) raise(Errc::IoError, "cannot create " + output);
+    // the output is one file: concurrent write() calls would serialise on its
+    // inode lock, so the workers copy into a shared mapping instead (falls
+    // back to pwritev where the file cannot be mapped)
+    struct Mapping {
+        std::uint8_t* p = nullptr;
+        std::size_t n = 0;
+        ~Mapping() {
+            if (p) ::munmap(p, n);
+        }
+    } map;
+    if (ref.original_length && ::ftruncate(out.fd, static_cast<off_t>(ref.original_length)) == 0) {
+        void* m = ::mmap(nullptr, ref.original_length, PROT_READ | PROT_WRITE, MAP_SHARED, out.fd, 0);
+        if (m != MAP_FAILED) {
+            map.p = static_cast<std::uint8_t*>(m);
+            map.n = ref.original_length;
+        }
+    }
 
     const std::uint64_t stripes = ref.stripe_count(), ss = ref.symbol_size, length = ref.original_length;
     const std::uint64_t stripe_bytes = std::uint64_t(k) * ss;
@@ -593,7 +611,15 @@ void decode_file(const std::vector<std::string>& shard_paths, const std::string&
                         iov.push_back({src, static_cast<std::size_t>(take)});
                         remaining -= take;
                     }
-                pwritev_full(out.fd, iov, at, output);
+                if (map.p) {
+                    std::uint64_t pos = at;
+                    for (const iovec& v : iov) {
+                        std::memcpy(map.p + pos, v.iov_base, v.iov_len);
+                        pos += v.iov_len;
+                    }
+                } else {
+                    pwritev_full(out.fd, iov, at, output);
+                }
             });
         });
     }

@@ -11,10 +11,10 @@ input-file layout, stripe = k symbols, parity written in shard order;
 decode: shard-major symbols, erased data {0..min(k,r)-1} as BenchRunner,
 bench.hpp:124-134).  K launches captured in a CUDA graph, CUDA events.
 Rates: source GB/s (k * size per stripe) and the reference's (k+r) * size
-convention (bench.hpp:205-207).  --cpu adds the reference itself
-(oracle/_ref: precompiled schedule + parallel_replay on one stripe, all host
-threads, best of a ~0.25 s loop -- cache resident for small sizes, exactly
-like the reference bench).  One JSON line per point.
+convention (bench.hpp:205-207).  --cpu adds the reference itself (oracle/_ref):
+its own bench cell BenchRunner::run_point (bench.hpp:146-208, one stripe,
+column windows over 1 and all host threads, best of the two) for w <= 6, else a
+precompiled schedule + parallel_replay on one stripe.  One JSON line per point.
 """
 from __future__ import annotations
 
@@ -159,7 +159,8 @@ def main():
                        "size": size, "stripes": nb, "gpu_ms": ms, "gpu_src_GBps": src / ms / 1e6,
                        "gpu_ref_GBps": (k + r) * size * nb / ms / 1e6,
                        "gpu_moved_GBps": (k + n_out) * size * nb / ms / 1e6, "kernel": info["kernel"],
-                       "xors_per_word": plan.stats()["xors"]}
+                       "xors_per_word": plan.stats()["part_xors" if ("_cpa" in info["kernel"] or
+                                                                     "_tma" in info["kernel"]) else "xors"]}
                 if a.cpu:
                     dt = cpu_point(f, k, r, a.transform, size, op, codec, threads)
                     if dt:
