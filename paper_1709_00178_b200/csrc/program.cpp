@@ -25,7 +25,7 @@ namespace {
 
 constexpr std::uint32_t kNone = 0xFFFFFFFFu;
 // bump whenever generated code changes for the same program (prebuilt cubins are keyed by name)
-constexpr int kGeneratorVersion = 8;
+constexpr int kGeneratorVersion = 9;
 
 // Greedy pair elimination over XOR targets.  Each target is a set of
 // variable ids; the most frequent pair (ties: smallest ids) becomes a new
@@ -582,43 +582,75 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
     // produce(u2): fill the slot of pipeline unit u2 = (tile it2, fragment group g2)
     o << "  u64 pol = 0;\n";
     if (!ks.copy) o << "  if (warp == 0) asm volatile(\"createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\" : \"=l\"(pol));\n";
-    o << "  auto produce = [&](u32 u2) {\n";
-    o << "    const u32 it2 = u2 / NG, g2 = u2 - it2 * NG;\n";
-    o << "    const u32 t2 = blockIdx.x + it2 * gridDim.x;\n";
-    o << "    if (t2 >= ntiles) return;\n";
-    o << "    const u32 sl = u2 % NSLOT, ph = (u2 / NSLOT) & 1u;\n";
-    o << "    mbar_wait(EMPTY(sl), ph ^ 1u);\n";
-    o << "    const u32 b2 = t2 / tpb, tt2 = t2 - b2 * tpb;\n";
-    o << "    const u64 o = a.off + (u64)tt2 * TILE;\n";
-    o << "    const u32 dst = sbase + BAR_BYTES + sl * SLOT_BYTES;\n";
-    o << "    const u32 j0 = g2 * " << G << "u;\n";
-    o << "    const u32 nstr = (g2 + 1u == NG ? " << k << "u - j0 : " << G << "u) * " << w << "u;\n";
     if (ks.copy) {
         // every thread copies CH-byte chunks (16, or 8/4 when the strips are
         // only that aligned; a strip tile is TILE/CH consecutive chunks:
         // coalesced) and arrives on the slot's FULL barrier once its copies
         // have landed.  Lanes are laid out strip-major: LPS lanes cover one
         // strip tile (CPL chunks each), a warp covers SPW strips per step,
-        // warps stride strips by NW*SPW; chunk validity only depends on the tile
+        // warps stride strips by NWS = NW*SPW.  The strips a thread copies are
+        // fixed per fragment group, so their base pointers are computed once
+        // (registers) and a unit only adds its tile offset; chunks past the
+        // window are skipped (their columns are never stored)
         const std::uint32_t CH = ks.chunk;
         const std::uint32_t cps = TILE / CH;
         const std::uint32_t lps = std::min<std::uint32_t>(32, cps), spw = 32 / lps, cpl = cps / lps, nw = T / 32;
+        const std::uint32_t nws = nw * spw;
+        o << "  const u32 lq = lane % " << lps << "u, lsub = lane / " << lps << "u;\n";
+        o << "  const u32 lbase = warp * " << spw << "u + lsub;\n";
+        std::vector<std::uint32_t> per_group(groups);
+        for (std::uint32_t g = 0; g < groups; ++g) {
+            const std::uint32_t nstr = (std::min(k, (g + 1) * G) - g * G) * w;
+            per_group[g] = (nstr + nws - 1) / nws;
+            for (std::uint32_t m = 0; m < per_group[g]; ++m) {
+                o << "  const u8* sp" << g << "_" << m << ";\n  { const u32 l = lbase + " << m * nws << "u;";
+                o << " const u32 idx = " << g * G * w << "u + (l < " << nstr << "u ? l : 0u), j = idx / " << w
+                  << "u, s = idx - j * " << w << "u;";
+                o << " sp" << g << "_" << m << " = a.in[j] + s * a.S + a.off + " << CH << "u * lq; }\n";
+            }
+        }
+        o << "  auto produce = [&](u32 u2) {\n";
+        o << "    const u32 it2 = u2 / NG, g2 = u2 - it2 * NG;\n";
+        o << "    const u32 t2 = blockIdx.x + it2 * gridDim.x;\n";
+        o << "    if (t2 >= ntiles) return;\n";
+        o << "    const u32 sl = u2 % NSLOT, ph = (u2 / NSLOT) & 1u;\n";
+        o << "    mbar_wait(EMPTY(sl), ph ^ 1u);\n";
+        o << "    const u32 b2 = t2 / tpb, tt2 = t2 - b2 * tpb;\n";
+        o << "    const u64 uoff = b2 * a.ibp + (u64)tt2 * TILE;\n";
         o << "    const u64 rem = a.len - (u64)tt2 * TILE;\n";
         o << "    const u32 vb = (u32)(rem < TILE ? rem : TILE);\n";
-        o << "    const u32 lq = lane % " << lps << "u, lsub = lane / " << lps << "u;\n";
+        o << "    const u32 d0 = sbase + BAR_BYTES + sl * SLOT_BYTES + lbase * TILE + " << CH << "u * lq;\n";
         for (std::uint32_t c = 0; c < cpl; ++c)
-            o << "    const u32 n" << c << " = " << CH << "u * (lq + " << c * lps << "u) < vb ? " << CH << "u : 0u;\n";
-        o << "#pragma unroll 1\n";
-        o << "    for (u32 l = warp * " << spw << "u + lsub; l < nstr; l += " << nw * spw << "u) {\n";
-        o << "      const u32 idx = j0 * " << w << "u + l, j = idx / " << w << "u, s = idx - j * " << w << "u;\n";
-        o << "      const u8* src = a.in[j] + b2 * a.ibp + s * a.S + o + " << CH << "u * lq;\n";
-        o << "      const u32 d = dst + l * TILE + " << CH << "u * lq;\n";
-        for (std::uint32_t c = 0; c < cpl; ++c)
-            o << "      cpa" << CH << "(d + " << CH * c * lps << "u, n" << c << " ? src + " << CH * c * lps
-              << "u : a.in[0] + a.off, n" << c << ");\n";
+            o << "    const bool n" << c << " = " << CH << "u * (lq + " << c * lps << "u) < vb;\n";
+        o << "    switch (g2) {\n";
+        for (std::uint32_t g = 0; g < groups; ++g) {
+            const std::uint32_t nstr = (std::min(k, (g + 1) * G) - g * G) * w;
+            o << "    case " << g << "u:\n";
+            for (std::uint32_t m = 0; m < per_group[g]; ++m) {
+                const bool tail = (m + 1) * nws > nstr; // some threads have no strip m
+                o << "      " << (tail ? "if (lbase + " + std::to_string(m * nws) + "u < " + std::to_string(nstr) + "u) " : "")
+                  << "{ const u8* src = sp" << g << "_" << m << " + uoff;";
+                for (std::uint32_t c = 0; c < cpl; ++c)
+                    o << " if (n" << c << ") cpa" << CH << "(d0 + " << (m * nws * TILE + CH * c * lps) << "u, src + "
+                      << CH * c * lps << "u, " << CH << "u);";
+                o << " }\n";
+            }
+            o << "      break;\n";
+        }
         o << "    }\n";
         o << "    cpa_arrive(FULL(sl));\n";
     } else {
+        o << "  auto produce = [&](u32 u2) {\n";
+        o << "    const u32 it2 = u2 / NG, g2 = u2 - it2 * NG;\n";
+        o << "    const u32 t2 = blockIdx.x + it2 * gridDim.x;\n";
+        o << "    if (t2 >= ntiles) return;\n";
+        o << "    const u32 sl = u2 % NSLOT, ph = (u2 / NSLOT) & 1u;\n";
+        o << "    mbar_wait(EMPTY(sl), ph ^ 1u);\n";
+        o << "    const u32 b2 = t2 / tpb, tt2 = t2 - b2 * tpb;\n";
+        o << "    const u64 o = a.off + (u64)tt2 * TILE;\n";
+        o << "    const u32 dst = sbase + BAR_BYTES + sl * SLOT_BYTES;\n";
+        o << "    const u32 j0 = g2 * " << G << "u;\n";
+        o << "    const u32 nstr = (g2 + 1u == NG ? " << k << "u - j0 : " << G << "u) * " << w << "u;\n";
         // warp 0: lane 0 posts the byte count, the lanes issue one
         // cp.async.bulk per strip tile
         o << "    const u64 rem = a.len - (u64)tt2 * TILE;\n";
