@@ -133,6 +133,16 @@ def prebuild_kernels(lanes=(100, 1), force=False) -> list[str]:
     return built
 
 
+def build_test_tools(force=False) -> str:
+    """tests/sanitize_check.cpp -> build/sanitize_check (compute-sanitizer driver, test infrastructure)."""
+    src = os.path.join(ROOT, "tests", "sanitize_check.cpp")
+    out = os.path.join(BUILD, "sanitize_check")
+    if force or _stale(out, [src, LIB, os.path.join(ROOT, "include", "pyrit_b200.h")]):
+        _run([NVCC, *ARCH, "-O2", "-std=c++17", f"-I{os.path.join(ROOT, 'include')}", src, "-o", out, f"-L{PKG}",
+              "-lpyrit_b200", "-Xlinker", "-rpath,$ORIGIN/../paper_1709_00178_b200"])
+    return out
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
@@ -140,6 +150,7 @@ def main(argv=None):
     ap.add_argument("--lanes", default="100,1", help="100 = TMA-staged kernel, 1/2/4 = direct")
     a = ap.parse_args(argv)
     build_library(a.force)
+    build_test_tools(a.force)
     if not a.no_prebuild:
         prebuild_kernels(tuple(int(x) for x in a.lanes.split(",")), a.force)
 

@@ -19,3 +19,16 @@ def test_shim_matches_reference(cuda):
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "SHIM CHECK PASSED" in r.stdout
+
+
+SAN = os.path.join(ROOT, "build", "sanitize_check")
+
+
+@pytest.mark.skipif(not os.path.exists(SAN), reason="build/sanitize_check not built")
+def test_sanitize_driver_plain(cuda):
+    """The compute-sanitizer driver (tests/sanitize_check.cpp) passes without the sanitizer:
+    every kernel shape on exact-size buffers matches the host interpreter."""
+    r = subprocess.run([SAN], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "SANITIZE CHECK PASSED" in r.stdout
