@@ -7,7 +7,10 @@
 //
 // Every device buffer is allocated at exactly the size the launch may touch,
 // so an out-of-bounds access is reported; results are compared with the
-// library's host interpreter of the same compiled program.
+// library's host interpreter of the same compiled program.  (compute-sanitizer
+// is closed on the GPU pool used here, so the driver also brackets every
+// buffer with 4 KiB canary regions and checks that no launch wrote outside
+// its buffers: plain runs catch stray stores too.)
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -61,12 +64,23 @@ void run(const Case& c) {
     std::vector<std::vector<unsigned char>> hin(c.k, std::vector<unsigned char>(sym * c.stripes));
     for (auto& v : hin)
         for (auto& x : v) x = static_cast<unsigned char>(rng());
-    std::vector<unsigned char*> din(c.k), dout(c.r);
-    for (unsigned j = 0; j < c.k; ++j) {
-        CK(cudaMalloc(&din[j], sym * c.stripes));
-        CK(cudaMemcpy(din[j], hin[j].data(), sym * c.stripes, cudaMemcpyHostToDevice));
+    // one allocation per buffer: [canary | data | canary]
+    constexpr unsigned long long kGuard = 4096;
+    const unsigned long long bytes = sym * c.stripes;
+    std::vector<unsigned char*> base(c.k + c.r), din(c.k), dout(c.r);
+    std::vector<unsigned char> canary(kGuard);
+    for (unsigned long long i = 0; i < kGuard; ++i) canary[i] = static_cast<unsigned char>(0xA5 ^ (i * 7));
+    for (unsigned s = 0; s < c.k + c.r; ++s) {
+        CK(cudaMalloc(&base[s], bytes + 2 * kGuard));
+        CK(cudaMemcpy(base[s], canary.data(), kGuard, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(base[s] + kGuard + bytes, canary.data(), kGuard, cudaMemcpyHostToDevice));
+        CK(cudaMemset(base[s] + kGuard, 0x5A, bytes));
     }
-    for (unsigned i = 0; i < c.r; ++i) CK(cudaMalloc(&dout[i], sym * c.stripes));
+    for (unsigned j = 0; j < c.k; ++j) {
+        din[j] = base[j] + kGuard;
+        CK(cudaMemcpy(din[j], hin[j].data(), bytes, cudaMemcpyHostToDevice));
+    }
+    for (unsigned i = 0; i < c.r; ++i) dout[i] = base[c.k + i] + kGuard;
     int rc = pyrit_cu_apply_batch(plan, const_cast<const unsigned char* const*>(din.data()), dout.data(), c.strip,
                                   0, c.strip, c.stripes, sym, sym, nullptr);
     CK(cudaDeviceSynchronize());
@@ -87,10 +101,22 @@ void run(const Case& c) {
             ok = std::memcmp(got.data(), want[i].data(), sym) == 0;
         }
     }
-    std::printf("%-34s mode %d %-52s %s\n", c.name, c.mode, kname, ok ? "OK" : "MISMATCH");
-    failures += !ok;
-    for (auto* p : din) CK(cudaFree(p));
-    for (auto* p : dout) CK(cudaFree(p));
+    bool guards = true;
+    std::vector<unsigned char> g(kGuard);
+    for (unsigned s = 0; s < c.k + c.r; ++s)
+        for (unsigned long long at : {0ull, kGuard + bytes}) {
+            CK(cudaMemcpy(g.data(), base[s] + at, kGuard, cudaMemcpyDeviceToHost));
+            guards = guards && std::memcmp(g.data(), canary.data(), kGuard) == 0;
+        }
+    for (unsigned j = 0; guards && j < c.k; ++j) { // inputs are read-only
+        std::vector<unsigned char> back(bytes);
+        CK(cudaMemcpy(back.data(), din[j], bytes, cudaMemcpyDeviceToHost));
+        guards = back == hin[j];
+    }
+    std::printf("%-34s mode %d %-52s %s%s\n", c.name, c.mode, kname, ok ? "OK" : "MISMATCH",
+                guards ? "" : " (STRAY WRITE)");
+    failures += !ok + !guards;
+    for (auto* p : base) CK(cudaFree(p));
     pyrit_plan_destroy(plan);
     pyrit_set_kernel_mode(0);
 }
