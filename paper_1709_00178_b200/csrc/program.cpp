@@ -25,7 +25,7 @@ namespace {
 
 constexpr std::uint32_t kNone = 0xFFFFFFFFu;
 // bump whenever generated code changes for the same program (prebuilt cubins are keyed by name)
-constexpr int kGeneratorVersion = 9;
+constexpr int kGeneratorVersion = 10;
 
 // Greedy pair elimination over XOR targets.  Each target is a set of
 // variable ids; the most frequent pair (ties: smallest ids) becomes a new
@@ -578,6 +578,10 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
       << T << "u); }\n";
     o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n  }\n";
     o << "  __syncthreads();\n";
+    // programmatic dependent launch: everything above overlaps the previous
+    // grid's tail; global memory is touched only after it has completed
+    o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
+    o << "  asm volatile(\"griddepcontrol.launch_dependents;\" ::: \"memory\");\n";
     o << "  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;\n";
     // produce(u2): fill the slot of pipeline unit u2 = (tile it2, fragment group g2)
     o << "  u64 pol = 0;\n";
@@ -774,6 +778,8 @@ std::string generate_cuda(const Program& p, const KernelShape& ks) {
     o << "extern \"C\" __global__ void __launch_bounds__(" << ks.threads << ", " << ks.min_blocks << ") " << name
       << "(const Args a)\n{\n";
     o << "  const u64 S = a.S;\n";
+    o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
+    o << "  asm volatile(\"griddepcontrol.launch_dependents;\" ::: \"memory\");\n";
     o << "  const u32 part = threadIdx.x / " << CPB << "u;\n";
     o << "  const u64 c0 = (u64)blockIdx.x * " << CPB << "u + threadIdx.x % " << CPB << "u;\n";
     auto var = [&](std::uint32_t v, std::uint32_t l) {

@@ -31,6 +31,7 @@ struct Driver {
     CUresult (*occupancy)(int*, CUfunction, int, size_t) = nullptr;
     CUresult (*getErrorString)(CUresult, const char**) = nullptr;
     CUresult (*funcSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
+    CUresult (*launchKernelEx)(const CUlaunchConfig*, CUfunction, void**, void**) = nullptr;
 };
 
 template <class F>
@@ -52,6 +53,7 @@ const Driver& driver() {
         resolve("cuOccupancyMaxActiveBlocksPerMultiprocessor", d.occupancy);
         resolve("cuGetErrorString", d.getErrorString);
         resolve("cuFuncSetAttribute", d.funcSetAttribute);
+        resolve("cuLaunchKernelEx", d.launchKernelEx);
     });
     return d;
 }
@@ -331,9 +333,23 @@ LaunchInfo launch_batch(const Program& p, const std::uint8_t* const* in, std::ui
         tail[7] = stride % nwords;
     }
     void* params[] = {args.data()};
-    check_cu(driver().launchKernel(k.fn, blocks, 1, 1, ks.threads, 1, 1, ks.staged ? ks.smem_bytes : 0,
-                                   reinterpret_cast<CUstream>(stream), params, nullptr),
-             "cuLaunchKernel");
+    // programmatic stream serialisation: the kernel may be scheduled while the
+    // previous work on the stream drains; it waits (griddepcontrol.wait) before
+    // touching global memory, so ordering is unchanged (PYRIT_B200_PDL=0 disables)
+    static const bool pdl = env_int("PYRIT_B200_PDL", 1) != 0;
+    CUlaunchAttribute attr{};
+    attr.id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr.value.programmaticStreamSerializationAllowed = 1;
+    CUlaunchConfig cfg{};
+    cfg.gridDimX = blocks;
+    cfg.gridDimY = cfg.gridDimZ = 1;
+    cfg.blockDimX = ks.threads;
+    cfg.blockDimY = cfg.blockDimZ = 1;
+    cfg.sharedMemBytes = ks.staged ? ks.smem_bytes : 0;
+    cfg.hStream = reinterpret_cast<CUstream>(stream);
+    cfg.attrs = pdl ? &attr : nullptr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    check_cu(driver().launchKernelEx(&cfg, k.fn, params, nullptr), "cuLaunchKernelEx");
     ++g_launches;
     info.lanes = ks.lanes;
     info.threads = ks.threads;
