@@ -152,6 +152,19 @@ LoadedKernel load_kernel(const Program& p, const KernelShape& ks, int device) {
 
 bool aligned(const void* p, std::uint64_t v) { return reinterpret_cast<std::uintptr_t>(p) % v == 0; }
 
+// SM count of the current device (cached per device)
+int sm_count() {
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    int n = cache[dev].load();
+    if (n == 0) {
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+        cache[dev] = n;
+    }
+    return n;
+}
+
 } // namespace
 
 std::uint32_t preferred_lanes() {
@@ -260,7 +273,10 @@ KernelShape choose_shape(const Program& p, const std::uint8_t* const* in, std::u
         const std::uint64_t tiles = ks.staged ? (len + ks.tile - 1) / ks.tile : 0;
         const bool dense = tiles && 2 * len >= tiles * ks.tile;
         const bool fits = tiles * nb < (std::uint64_t(1) << 32);
-        const bool suited = dense && chunk == 16 && p.parts.size() <= 2;
+        // ... and enough tiles for its pipeline to pay for the ring setup (small
+        // launches -- config 1's 6 MiB -- run faster on the direct kernel)
+        const bool big = tiles * nb >= 2ull * static_cast<std::uint64_t>(sm_count());
+        const bool suited = dense && big && chunk == 16 && p.parts.size() <= 2;
         if (ks.staged && fits && (suited || kernel_mode() == 2)) return ks;
     }
     // direct mode: widest vector the alignment of every pointer, the strip
