@@ -6,6 +6,7 @@
 #include "pipeline.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -57,7 +58,11 @@ void run_host(const Program& p, const std::vector<const std::uint8_t*>& host_in,
 
     const std::uint64_t strips = std::uint64_t(p.cols + p.rows) * w;
     std::uint64_t chunk = g_chunk;
-    if (chunk == 0) chunk = (std::uint64_t(96) << 20) / strips; // ~96 MiB of staging per slot
+    if (chunk == 0) {
+        static const char* env = std::getenv("PYRIT_B200_HOST_STAGE_MIB"); // tuning knob
+        const std::uint64_t mib = env ? std::strtoull(env, nullptr, 10) : 96;
+        chunk = ((mib ? mib : 96) << 20) / strips; // ~96 MiB of staging per slot
+    }
     chunk = std::max<std::uint64_t>(chunk, 64 * 1024) & ~std::uint64_t(4095);
     if (strip % 16 == 0) chunk = std::min(chunk, strip);
     else chunk = std::min(chunk, strip & ~std::uint64_t(15)); // tail chunk handled in byte mode
