@@ -60,8 +60,8 @@ void run_host(const Program& p, const std::vector<const std::uint8_t*>& host_in,
     std::uint64_t chunk = g_chunk;
     if (chunk == 0) {
         static const char* env = std::getenv("PYRIT_B200_HOST_STAGE_MIB"); // tuning knob
-        const std::uint64_t mib = env ? std::strtoull(env, nullptr, 10) : 96;
-        chunk = ((mib ? mib : 96) << 20) / strips; // ~96 MiB of staging per slot
+        const std::uint64_t mib = env ? std::strtoull(env, nullptr, 10) : 192;
+        chunk = ((mib ? mib : 192) << 20) / strips; // ~192 MiB of staging per slot
     }
     chunk = std::max<std::uint64_t>(chunk, 64 * 1024) & ~std::uint64_t(4095);
     if (strip % 16 == 0) chunk = std::min(chunk, strip);
@@ -78,23 +78,34 @@ void run_host(const Program& p, const std::vector<const std::uint8_t*>& host_in,
             s.bytes = need;
         }
     }
+    // runs of symbols laid out back to back on the host (SymbolBuffer storage,
+    // codec.hpp:24-73): one 2D copy moves the window of all their strips
+    auto runs = [&](const auto& ptrs) {
+        std::vector<std::pair<std::uint32_t, std::uint32_t>> out; // [first, end)
+        for (std::uint32_t j = 0; j < ptrs.size(); ++j) {
+            if (!out.empty() && ptrs[j] == ptrs[j - 1] + std::uint64_t(w) * strip) ++out.back().second;
+            else out.push_back({j, j + 1});
+        }
+        return out;
+    };
+    const auto in_runs = runs(host_in);
+    const auto out_runs = runs(host_out);
     std::vector<const std::uint8_t*> din(p.cols);
     std::vector<std::uint8_t*> dout(p.rows);
     std::uint64_t c0 = 0;
     for (int c = 0; c0 < strip; ++c) {
         const std::uint64_t len = std::min(chunk, strip - c0);
         Slot& s = ctx.slots[c % kSlots];
-        for (std::uint32_t j = 0; j < p.cols; ++j) {
-            std::uint8_t* d = s.buf + std::uint64_t(j) * w * chunk;
-            check_cuda(cudaMemcpy2DAsync(d, chunk, host_in[j] + c0, strip, len, w, cudaMemcpyHostToDevice, s.stream),
-                       "H2D");
-            din[j] = d;
-        }
+        for (std::uint32_t j = 0; j < p.cols; ++j) din[j] = s.buf + std::uint64_t(j) * w * chunk;
         for (std::uint32_t i = 0; i < p.rows; ++i) dout[i] = s.buf + std::uint64_t(p.cols + i) * w * chunk;
+        for (const auto& [j0, j1] : in_runs)
+            check_cuda(cudaMemcpy2DAsync(const_cast<std::uint8_t*>(din[j0]), chunk, host_in[j0] + c0, strip, len,
+                                         std::size_t(j1 - j0) * w, cudaMemcpyHostToDevice, s.stream),
+                       "H2D");
         launch_program(p, din.data(), dout.data(), chunk, 0, len, s.stream);
-        for (std::uint32_t i = 0; i < p.rows; ++i)
-            check_cuda(cudaMemcpy2DAsync(host_out[i] + c0, strip, dout[i], chunk, len, w, cudaMemcpyDeviceToHost,
-                                         s.stream),
+        for (const auto& [i0, i1] : out_runs)
+            check_cuda(cudaMemcpy2DAsync(host_out[i0] + c0, strip, dout[i0], chunk, len, std::size_t(i1 - i0) * w,
+                                         cudaMemcpyDeviceToHost, s.stream),
                        "D2H");
         c0 += len;
     }
