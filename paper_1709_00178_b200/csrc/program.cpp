@@ -374,25 +374,32 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
         if (!R && env_u("PYRIT_B200_PARTS") > 0) R = static_cast<std::uint32_t>(env_u("PYRIT_B200_PARTS"));
         if (!R && tuned) R = tuned->parts;
         const std::uint32_t acc_rows = emb && !crs ? n : w; // accumulators per output row
+        // Heuristic (measured on the BASELINE codes and the paper's (60,40) /
+        // (60,20) GF(2^6) codes, profiles/r01_s2): the fewest parts -- every
+        // part re-reads all input strips from shared memory -- that keep
+        // <= 128 accumulators per thread; 512-thread CTAs when a part's
+        // accumulators are few (<= 48), else 256 (255 registers); and the
+        // largest fragment group whose slot still lets 3 slots fit in shared
+        // memory, since every (tile, group) unit costs a barrier round trip.
         if (!R) { // a power of two (it must divide the CTA) no larger than e
             R = 1;
-            while (2 * R <= e && (e + R - 1) / R * acc_rows > 64) R *= 2;
+            while (2 * R <= e && (e + R - 1) / R * acc_rows > 128) R *= 2;
         }
         R = std::max<std::uint32_t>(1, std::min(R, e));
+        const std::uint32_t acc = (e + R - 1) / R * acc_rows;
+        if (!p.staged_threads) p.staged_threads = acc <= 48 ? 512 : 256;
         std::uint32_t pg = opt.part_group;
         if (!pg && env_u("PYRIT_B200_PART_GROUP") > 0) pg = static_cast<std::uint32_t>(env_u("PYRIT_B200_PART_GROUP"));
         if (!pg && tuned) pg = tuned->part_group;
-        // ~48 strips per group; ~24 when the rows are split (those programs
-        // also run as direct split kernels, 128 registers per thread)
-        if (!pg) pg = std::max<std::uint32_t>(1, ((R > 1 ? 24 : 48) + w / 2) / w);
+        if (!pg) {
+            const std::uint32_t tile = 4 * (p.staged_threads / R);
+            pg = std::max<std::uint32_t>(1, (226u * 1024 / 3) / (w * tile));
+            pg = std::min(pg, std::max<std::uint32_t>(1, 160 / w));
+        }
         pg = std::max<std::uint32_t>(1, std::min(pg, k));
         int pcse = env_u("PYRIT_B200_PART_CSE");
         if (pcse < 0 && tuned) pcse = tuned->part_cse;
         if (pcse < 0) pcse = 0;
-        if (!p.staged_threads) {
-            const std::uint32_t live = (e + R - 1) / R * acc_rows + pg * w;
-            p.staged_threads = live <= 96 ? 512 : 256;
-        }
         auto build_parts = [&](bool cse) {
             p.parts.clear();
             p.part_row0.clear();

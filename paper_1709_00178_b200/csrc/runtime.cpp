@@ -202,7 +202,15 @@ std::uint64_t kernel_launches() { return g_launches.load(); }
 KernelShape direct_shape(const Program& p, std::uint32_t lanes) {
     KernelShape ks = shape_for(lanes);
     const std::uint32_t R = static_cast<std::uint32_t>(p.parts.size());
-    if (R > 1 && ks.threads % R == 0 && ks.threads / R >= 32) { ks.split = R; ks.min_blocks = 2; }
+    if (R > 1 && ks.threads % R == 0 && ks.threads / R >= 32) {
+        ks.split = R;
+        // two CTAs per SM (128 registers) while a part's accumulators are few
+        const std::uint32_t acc_rows =
+            p.kind == TransformKind::Embedding && !p.crs ? p.field.n : p.field.w;
+        std::uint32_t acc = 0;
+        for (const Program& q : p.parts) acc = std::max(acc, q.rows * acc_rows);
+        ks.min_blocks = acc <= 64 ? 2 : 1;
+    }
     return ks;
 }
 
