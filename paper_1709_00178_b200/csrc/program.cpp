@@ -290,7 +290,18 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
                 std::sort(tg.begin(), tg.end());
                 p.stats.naive_xors += tg.size(); // one XOR per term into the row...
             }
-        if (opt.cse) share_pairs(targets, nvars, cp, opt.max_temps);
+        if (opt.cse) {
+            // pair sharing over windows of cse_window consecutive targets (ring
+            // rows, output by output); 0 = the whole group.  Small windows keep
+            // shared temporaries short-lived (register pressure)
+            const std::size_t win = opt.cse_window ? opt.cse_window : targets.size();
+            for (std::size_t w0 = 0; w0 < targets.size(); w0 += win) {
+                const std::size_t w1 = std::min(targets.size(), w0 + win);
+                std::vector<std::vector<std::uint32_t>> sub(targets.begin() + w0, targets.begin() + w1);
+                share_pairs(sub, nvars, cp, opt.max_temps);
+                std::copy(sub.begin(), sub.end(), targets.begin() + w0);
+            }
+        }
         const std::size_t ntemps = cp.size();
         for (std::size_t r = 0; r < targets.size(); ++r) {
             auto& tg = targets[r];
@@ -413,6 +424,7 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
                 o2.group = pg;
                 o2.cse = cse && opt.cse;
                 if (const char* env = std::getenv("PYRIT_B200_PART_TEMPS")) o2.max_temps = std::atoi(env);
+                if (const char* env = std::getenv("PYRIT_B200_CSE_WINDOW")) o2.cse_window = std::atoi(env);
                 p.parts.push_back(compile_program(f, kind, sub, o2));
                 p.part_row0.push_back(row0);
                 row0 += nrows;

@@ -71,6 +71,7 @@ struct CompileOptions {
     std::uint32_t parts = 0;   // output parts for the staged kernel: 0 auto, 1 = do not split
     std::uint32_t part_group = 0; // fragment group of the parts: 0 auto
     std::uint32_t max_temps = 0;  // cap on shared pair temporaries per group (0 = no cap)
+    std::uint32_t cse_window = 0; // pair sharing within windows of this many targets (0 = whole group)
     std::uint32_t staged_threads = 0; // staged CTA size (0 = tuned table / 256)
 };
 
