@@ -25,7 +25,7 @@ namespace {
 
 constexpr std::uint32_t kNone = 0xFFFFFFFFu;
 // bump whenever generated code changes for the same program (prebuilt cubins are keyed by name)
-constexpr int kGeneratorVersion = 11;
+constexpr int kGeneratorVersion = 10;
 
 // Greedy pair elimination over XOR targets.  Each target is a set of
 // variable ids; the most frequent pair (ties: smallest ids) becomes a new
@@ -365,9 +365,12 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
 
     // Output parts of the staged kernel (see KernelShape).  Knobs, in order
     // of precedence: CompileOptions, PYRIT_B200_PARTS / _PART_GROUP /
-    // _PART_CSE / _THREADS / _WORD, the measured tuning table (tuned.tsv next
-    // to the library), and the heuristic below.  No pair sharing by default:
-    // its temporaries lengthen live ranges (spills, dependency chains).
+    // _PART_CSE / _THREADS, the measured tuning table (tuned.tsv next to the
+    // library), and the heuristic: the fewest parts that keep <= 64 ring-row
+    // accumulators per thread; fragment groups of about 48 strips; no pair
+    // sharing (its temporaries lengthen live ranges and spill); 512 threads
+    // per CTA when a part's live words (accumulators + one group's strips)
+    // fit the 128 registers that allows, else 256.
     if (opt.parts != 1 && e > 0) {
         const auto env_u = [](const char* name) -> int {
             const char* v = std::getenv(name);
@@ -378,7 +381,6 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
         if (!p.staged_threads && env_u("PYRIT_B200_THREADS") > 0)
             p.staged_threads = static_cast<std::uint32_t>(env_u("PYRIT_B200_THREADS"));
         if (!p.staged_threads && tuned) p.staged_threads = tuned->threads;
-        p.staged_word = env_u("PYRIT_B200_WORD") == 8 ? 8 : 4;
         std::uint32_t R = opt.parts;
         if (!R && env_u("PYRIT_B200_PARTS") > 0) R = static_cast<std::uint32_t>(env_u("PYRIT_B200_PARTS"));
         if (!R && tuned) R = tuned->parts;
@@ -401,7 +403,7 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
         if (!pg && env_u("PYRIT_B200_PART_GROUP") > 0) pg = static_cast<std::uint32_t>(env_u("PYRIT_B200_PART_GROUP"));
         if (!pg && tuned) pg = tuned->part_group;
         if (!pg) {
-            const std::uint32_t tile = p.staged_word * (p.staged_threads / R);
+            const std::uint32_t tile = 4 * (p.staged_threads / R);
             pg = std::max<std::uint32_t>(1, (226u * 1024 / 3) / (w * tile));
             pg = std::min(pg, std::max<std::uint32_t>(1, 160 / w));
         }
@@ -467,7 +469,7 @@ std::string kernel_name(const Program& p, const KernelShape& ks) {
        << ',' << p.rows << ',' << p.cols << ',' << p.group << ',' << ks.lanes << ',' << ks.threads << ',' << ks.min_blocks << ','
        << ks.staged << ',' << ks.tile << ',' << ks.stages << ',' << ks.bar_bytes << ',' << p.parts.size() << ','
        << (p.parts.empty() ? 0u : p.parts[0].group) << ',' << ks.copy << ',' << p.cse << ',' << p.crs << ','
-       << ks.chunk << ',' << ks.split << ',' << ks.word << ',';
+       << ks.chunk << ',' << ks.split << ',';
     if (p.crs)
         for (std::uint16_t x : p.matrix) fp << 'c' << x;
     for (const Program& q : p.parts) fp << q.rows << '/' << q.cse << '/' << q.stats.xors << ',';
@@ -504,7 +506,7 @@ KernelShape staged_shape(const Program& p, std::uint32_t smem_limit) {
     if (p.staged_threads && p.staged_threads != 256) choices.insert(choices.begin(), p.staged_threads);
     for (std::uint32_t threads : choices) {
         if (threads % R) continue;
-        const std::uint32_t tile = p.staged_word * (threads / R);
+        const std::uint32_t tile = 4 * (threads / R);
         if (tile < 64) continue;
         const std::uint64_t slot = std::uint64_t(G) * w * tile;
         std::uint32_t slots = 0, bar = 0;
@@ -521,7 +523,6 @@ KernelShape staged_shape(const Program& p, std::uint32_t smem_limit) {
         ks.stages = slots;
         ks.bar_bytes = bar;
         ks.threads = threads;
-        ks.word = p.staged_word;
         ks.smem_bytes = static_cast<std::uint32_t>(bar + slots * slot);
         (void)k;
         return ks;
@@ -542,10 +543,6 @@ std::string generate_staged(const Program& p, const KernelShape& ks) {
     const std::uint32_t groups = (k + G - 1) / G, TILE = ks.tile, NSLOT = ks.stages, T = ks.threads;
     const std::uint32_t R = static_cast<std::uint32_t>(p.parts.size());
     const std::uint32_t cols_per_part = T / R;
-    // bytes per consumer thread per strip: one 32-bit word, or two (u64 XORs,
-    // 8-byte shared loads and stores: twice the tile per CTA)
-    const std::uint32_t WB = ks.word == 8 ? 8 : 4;
-    const std::string WT = WB == 8 ? "u64" : "u32";
     const std::uint32_t slot_bytes = G * w * TILE;
     std::uint64_t part_xors = 0;
     for (const Program& q : p.parts) part_xors += q.stats.xors;
@@ -584,8 +581,6 @@ static __device__ __forceinline__ void cpa_arrive(u32 bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(bar) : "memory"); }
 static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
   asm volatile("st.global.cs.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory"); }
-static __device__ __forceinline__ void st_cs(u8* p, u64 v) {
-  asm volatile("st.global.cs.b64 [%0], %1;" :: "l"(p), "l"(v) : "memory"); }
 )";
     const std::string name = kernel_name(p, ks);
     o << "#define TILE " << TILE << "u\n#define NSLOT " << NSLOT << "u\n#define SLOT_BYTES " << slot_bytes
@@ -704,7 +699,7 @@ static __device__ __forceinline__ void st_cs(u8* p, u64 v) {
         o << "   u32 it = 0;\n";
         o << "   for (u32 t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {\n";
         o << "    const u32 bb = t / tpb, tt = t - bb * tpb;\n";
-        o << "    const u64 rel = (u64)tt * TILE + " << WB << "u * col;\n";
+        o << "    const u64 rel = (u64)tt * TILE + 4u * col;\n";
         o << "    const u64 o = a.off + rel + bb * a.obp;\n";
         o << "    const bool live = rel < a.len;\n";
         std::vector<bool> out_ptr(q.rows, false);
@@ -712,9 +707,9 @@ static __device__ __forceinline__ void st_cs(u8* p, u64 v) {
         auto emit = [&](const Instr& ins) {
             if (ins.op == Instr::Load) {
                 const std::uint32_t local = (ins.sym - (ins.sym / G) * G) * w + ins.strip;
-                o << "    const " << WT << " v" << ins.dst << " = " << cur_sp << "[" << local * (TILE / WB) << "];\n";
+                o << "    const u32 v" << ins.dst << " = " << cur_sp << "[" << local * (TILE / 4) << "];\n";
             } else if (ins.op == Instr::Xor) {
-                o << "    const " << WT << " v" << ins.dst << " = ";
+                o << "    const u32 v" << ins.dst << " = ";
                 emit_xor_list(o, ins.src, "v");
                 o << ";\n";
             } else {
@@ -725,9 +720,9 @@ static __device__ __forceinline__ void st_cs(u8* p, u64 v) {
                 }
                 o << "    if (live) st_cs(q" << row;
                 if (ins.strip) o << " + " << ins.strip << "u * S";
-                o << ", (" << WT << ")(";
+                o << ", ";
                 emit_xor_list(o, ins.src, "v");
-                o << "));\n";
+                o << ");\n";
             }
         };
         for (std::uint32_t g = 0; g < groups; ++g) {
@@ -739,8 +734,8 @@ static __device__ __forceinline__ void st_cs(u8* p, u64 v) {
             else if (r == 0) o << "    if (warp == 0) produce(un" << gs << " + NSLOT - 1u);\n";
             o << "    const u32 sl" << gs << " = un" << gs << " % NSLOT;\n";
             o << "    mbar_wait(FULL(sl" << gs << "), (un" << gs << " / NSLOT) & 1u);\n";
-            o << "    const " << WT << "* sp" << gs << " = reinterpret_cast<const " << WT << "*>(sm + BAR_BYTES + sl"
-              << gs << " * SLOT_BYTES) + col;\n";
+            o << "    const u32* sp" << gs << " = reinterpret_cast<const u32*>(sm + BAR_BYTES + sl" << gs
+              << " * SLOT_BYTES) + col;\n";
             cur_sp = "sp" + gs;
             for (const Instr& x : q.group_loads[g]) emit(x);
             o << "    mbar_arrive(EMPTY(sl" << gs << "));\n";

@@ -60,7 +60,6 @@ struct Program {
     std::vector<Program> parts;
     std::vector<std::uint32_t> part_row0;
     std::uint32_t staged_threads = 0; // staged CTA size override (0 = 256)
-    std::uint32_t staged_word = 4;    // staged: bytes per consumer thread per strip (4 or 8)
     ProgramStats stats;
 };
 
@@ -121,7 +120,6 @@ struct KernelShape {
     std::uint32_t copy = 1;         // staged: 0 = TMA cp.async.bulk by warp 0, 1 = cp.async by every thread
     std::uint32_t chunk = 16;       // staged cp.async: bytes per copy (16; 8 or 4 for less aligned strips)
     std::uint32_t split = 0;        // direct: rows split over p.parts.size() thread groups (0/1 = no split)
-    std::uint32_t word = 4;         // staged: bytes per consumer thread per strip (4 or 8)
 };
 std::string kernel_name(const Program& p, const KernelShape& ks);
 std::string generate_cuda(const Program& p, const KernelShape& ks);
