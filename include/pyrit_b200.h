@@ -15,6 +15,7 @@
  *   schedule_stats       schedule.hpp:216-223       pyrit_plan_get_stats
  *   replay / parallel_replay codec.hpp:118-193      pyrit_cu_apply
  *   encode               codec.hpp:212-220          pyrit_cu_encode   (device buffers)
+ *   encode_crs           codec.hpp:223-231          pyrit_cu_encode_crs
  *                                                    pyrit_encode_host (host buffers)
  *   decode               codec.hpp:241-284          pyrit_cu_decode   (device buffers)
  *                                                    pyrit_decode_host (host buffers)
@@ -144,6 +145,10 @@ int pyrit_cu_prepare(const pyrit_plan* plan);
 /* encode (codec.hpp:212): data[k], parity[r] device symbol pointers */
 int pyrit_cu_encode(const pyrit_code* code, const uint8_t* const* data, uint8_t* const* parity,
                     uint64_t symbol_size, void* stream);
+/* encode_crs (codec.hpp:223-231): the same parity through the plain-field
+ * Cauchy-RS bitmatrix program (compile_crs_schedule) -- the baseline codec */
+int pyrit_cu_encode_crs(const pyrit_code* code, const uint8_t* const* data, uint8_t* const* parity,
+                        uint64_t symbol_size, void* stream);
 /* decode (codec.hpp:241): symbols[k + r] device pointers, repaired in place */
 int pyrit_cu_decode(const pyrit_code* code, uint8_t* const* symbols, const uint32_t* erased, uint32_t n_erased,
                     uint64_t symbol_size, void* stream);
@@ -168,6 +173,9 @@ int pyrit_cu_decode_batch(const pyrit_code* code, uint8_t* const* symbols, const
  * parity: r * symbol_size host bytes.  Synchronous. Pinned buffers overlap. */
 int pyrit_encode_host(const pyrit_code* code, const uint8_t* data, uint8_t* parity, uint64_t symbol_size,
                       int device);
+/* encode_crs (codec.hpp:223-231) with host buffers */
+int pyrit_encode_crs_host(const pyrit_code* code, const uint8_t* data, uint8_t* parity, uint64_t symbol_size,
+                          int device);
 /* symbols: (k + r) * symbol_size host bytes, repaired in place.  Synchronous. */
 int pyrit_decode_host(const pyrit_code* code, uint8_t* symbols, const uint32_t* erased, uint32_t n_erased,
                       uint64_t symbol_size, int device);

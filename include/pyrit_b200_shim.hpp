@@ -61,6 +61,16 @@ inline SymbolBuffer encode(const SymbolBuffer& data, const CodeSpec& code, int d
     return parity;
 }
 
+// codec.hpp:223 encode_crs(): the bitmatrix baseline codec on the GPU, same
+// parity bytes as encode() (host buffers, like encode above).
+inline SymbolBuffer encode_crs(const SymbolBuffer& data, const CodeSpec& code, int device = 0) {
+    check_data_shape(data, code);
+    SymbolBuffer parity(code.r, data.symbol_size(), code.field);
+    const pyrit_code c = to_c(code);
+    if (code.r) check(pyrit_encode_crs_host(&c, data.symbol(0), parity.symbol(0), data.symbol_size(), device));
+    return parity;
+}
+
 // codec.hpp:241 decode(): in-place repair of the listed symbols from any k
 // survivors (lowest index first), one fused pass on the GPU.
 inline void decode(SymbolBuffer& symbols, const std::vector<unsigned>& erased, const CodeSpec& code,

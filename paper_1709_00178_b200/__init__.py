@@ -24,7 +24,7 @@ __all__ = [
     "sparse_transform", "fold_table", "cauchy_parity_matrix", "decode_matrix", "repair_matrix", "encode",
     "decode", "encode_host", "decode_host", "fill", "digest", "choose_transform", "encode_batch", "decode_batch",
     "ShardHeader", "crc32", "serialize_header", "parse_header", "field_id", "field_from_id", "shard_path",
-    "encode_file", "decode_file", "HEADER_SIZE",
+    "encode_file", "decode_file", "HEADER_SIZE", "encode_crs",
 ]
 
 
@@ -276,6 +276,18 @@ def encode(data, code: CodeSpec):
     parity = torch.empty((code.r, data.shape[1]), dtype=torch.uint8, device=data.device)
     L.check(_clib().pyrit_cu_encode(C.byref(code.c()), _ptr_array(_rows(data)), _ptr_array(_rows(parity)),
                                    data.shape[1], _stream_of(data)))
+    return parity
+
+
+def encode_crs(data, code: CodeSpec):
+    """encode_crs (codec.hpp:223-231): the Cauchy-RS bitmatrix baseline on the GPU; same parity bytes."""
+    import torch
+    if data.dim() != 2 or data.shape[0] != code.k or data.dtype != torch.uint8 or not data.is_cuda:
+        raise PyritError(4, "data buffer does not match the code")
+    data = data.contiguous()
+    parity = torch.empty((code.r, data.shape[1]), dtype=torch.uint8, device=data.device)
+    L.check(_clib().pyrit_cu_encode_crs(C.byref(code.c()), _ptr_array(_rows(data)), _ptr_array(_rows(parity)),
+                                       data.shape[1], _stream_of(data)))
     return parity
 
 

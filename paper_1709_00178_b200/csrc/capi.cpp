@@ -332,6 +332,21 @@ int pyrit_cu_encode(const pyrit_code* code, const uint8_t* const* data, uint8_t*
     });
 }
 
+int pyrit_cu_encode_crs(const pyrit_code* code, const uint8_t* const* data, uint8_t* const* parity,
+                        uint64_t symbol_size, void* stream) {
+    return guarded([&] {
+        check_code(code);
+        const std::uint64_t strip = strip_of(code, symbol_size);
+        if (!data || (!parity && code->r)) raise(Errc::InvalidArgument, "null symbol array");
+        if (code->r == 0) return;
+        CodeParams cp = params_of(code);
+        cp.kind = TransformKind::Embedding; // encode_crs ignores the transform (codec.hpp:223-231)
+        cp.crs = true;
+        auto p = encode_program(cp);
+        launch_program(*p, data, parity, strip, 0, strip, static_cast<cudaStream_t>(stream));
+    });
+}
+
 int pyrit_cu_decode(const pyrit_code* code, uint8_t* const* symbols, const uint32_t* erased, uint32_t n_erased,
                     uint64_t symbol_size, void* stream) {
     return guarded([&] {
@@ -397,6 +412,25 @@ int pyrit_encode_host(const pyrit_code* code, const uint8_t* data, uint8_t* pari
         if (!data || (!parity && code->r)) raise(Errc::InvalidArgument, "null buffer");
         if (code->r == 0) return;
         auto p = encode_program(code);
+        std::vector<const uint8_t*> in;
+        std::vector<uint8_t*> out;
+        for (uint32_t j = 0; j < code->k; ++j) in.push_back(data + std::uint64_t(j) * symbol_size);
+        for (uint32_t i = 0; i < code->r; ++i) out.push_back(parity + std::uint64_t(i) * symbol_size);
+        run_host(*p, in, out, strip, device);
+    });
+}
+
+int pyrit_encode_crs_host(const pyrit_code* code, const uint8_t* data, uint8_t* parity, uint64_t symbol_size,
+                          int device) {
+    return guarded([&] {
+        check_code(code);
+        const std::uint64_t strip = strip_of(code, symbol_size);
+        if (!data || (!parity && code->r)) raise(Errc::InvalidArgument, "null buffer");
+        if (code->r == 0) return;
+        CodeParams cp = params_of(code);
+        cp.kind = TransformKind::Embedding;
+        cp.crs = true;
+        auto p = encode_program(cp);
         std::vector<const uint8_t*> in;
         std::vector<uint8_t*> out;
         for (uint32_t j = 0; j < code->k; ++j) in.push_back(data + std::uint64_t(j) * symbol_size);

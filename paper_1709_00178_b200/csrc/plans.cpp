@@ -44,7 +44,7 @@ PlanCache& cache() {
 std::string code_key(const CodeParams& c) {
     std::ostringstream s;
     s << c.k << ',' << c.r << ',' << c.field.w << ',' << c.field.n << ',' << int(c.field.kind) << ',' << c.field.s
-      << ',' << c.field.r_esp << ',' << c.field.modulus << ',' << int(c.kind);
+      << ',' << c.field.r_esp << ',' << c.field.modulus << ',' << int(c.kind) << ',' << c.crs;
     return s.str();
 }
 
@@ -53,8 +53,10 @@ std::string code_key(const CodeParams& c) {
 std::shared_ptr<const Program> encode_program(const CodeParams& c) {
     const std::string key = "E" + code_key(c);
     if (auto p = cache().get(key)) return p;
+    CompileOptions opt;
+    opt.crs = c.crs;
     auto p = std::make_shared<const Program>(
-        compile_program(c.field, c.kind, cauchy_parity_matrix(c.k, c.r, c.field), CompileOptions{}));
+        compile_program(c.field, c.kind, cauchy_parity_matrix(c.k, c.r, c.field), opt));
     cache().put(key, p);
     return p;
 }

@@ -17,6 +17,7 @@ struct CodeParams {
     std::uint32_t k = 0, r = 0;
     Field field;
     TransformKind kind = TransformKind::Embedding;
+    bool crs = false; // plain-field bitmatrix program (encode_crs, codec.hpp:223-231)
 };
 
 std::shared_ptr<const Program> encode_program(const CodeParams& c);

@@ -48,7 +48,7 @@ int main() {
         fill(data, c.k * 1000 + c.r);
         const SymbolBuffer want = c.ring_ok ? encode(data, code, 4) : encode_crs(data, code, 4);
         const SymbolBuffer got = pyrit::cuda::encode(data, code);
-        const bool enc_ok = same(got, want);
+        const bool enc_ok = same(got, want) && same(pyrit::cuda::encode_crs(data, code), want);
         // decode: erase r symbols (data and parity mixed), repair in place
         SymbolBuffer full(c.k + c.r, c.symbol_size, c.f);
         std::memcpy(full.symbol(0), data.symbol(0), c.k * c.symbol_size);

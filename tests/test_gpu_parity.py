@@ -296,3 +296,19 @@ def test_large_codes_split_rows(cuda, mode, k, r, kind, ss):
         np.testing.assert_array_equal(dev_decode(cuda, code, work, erased), full)
     finally:
         L.check(lib.pyrit_set_kernel_mode(0))
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 5])
+def test_encode_crs_top_level(cuda, cfg):
+    """encode_crs (codec.hpp:223-231) on the GPU == encode() == the field oracle."""
+    import torch
+    wl = WORKLOADS[cfg]
+    f = wl.fld
+    ss = f.w * (1024 + 16 * 3)
+    data = seeded_symbols(wl.k, ss, f.w, wl.seed)
+    d = torch.from_numpy(data).to(cuda)
+    got = P.encode_crs(d, wl.code)
+    ring = P.encode(d, wl.code)
+    torch.cuda.synchronize()
+    assert torch.equal(got, ring)
+    np.testing.assert_array_equal(got.cpu().numpy(), oracle_encode(f, P.cauchy_parity_matrix(wl.code), data))
