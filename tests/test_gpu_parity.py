@@ -312,3 +312,48 @@ def test_encode_crs_top_level(cuda, cfg):
     torch.cuda.synchronize()
     assert torch.equal(got, ring)
     np.testing.assert_array_equal(got.cpu().numpy(), oracle_encode(f, P.cauchy_parity_matrix(wl.code), data))
+
+
+def test_random_codes_windows_and_batches(cuda):
+    """Seeded random sweep (property style, test_schedule.cpp:104-136 generalised):
+    random field, (k, r), transform, window [off, off+len), stripe batch and kernel mode;
+    the device result on every window equals the oracle's ring replay of that window and
+    bytes outside the window are untouched."""
+    import torch
+    rng = random.Random(20261020)
+    fields = [G16, G64, G256, G1024, G4096]
+    for case in range(40):
+        f = rng.choice(fields)
+        k = rng.randint(1, min(24, f.field_size() - 1))
+        r = rng.randint(1, min(12, f.field_size() - k))
+        kind = rng.choice([0, 0, 1])
+        strip = 16 * rng.randint(1, 300) + rng.choice([0, 0, 4, 8])
+        off = rng.choice([0, 4 * rng.randint(0, strip // 8)])
+        length = rng.randint(1, strip - off)
+        nb = rng.choice([1, 1, 3])
+        mode = rng.choice([0, 1, 2])
+        code = P.CodeSpec(k, r, f, P.TransformKind(kind))
+        m = P.cauchy_parity_matrix(code)
+        plan = P.Plan.create(f, m, P.TransformKind(kind))
+        sym = f.w * strip
+        data = rand_symbols(nb * k, sym, case).reshape(nb, k, sym)
+        d = torch.from_numpy(data).to(cuda)
+        out = torch.full((nb, r, sym), 0x77, dtype=torch.uint8, device=cuda)
+        lib = L.load()
+        L.check(lib.pyrit_set_kernel_mode(mode))
+        try:
+            plan.apply_batch([d[0, j].data_ptr() for j in range(k)], [out[0, i].data_ptr() for i in range(r)], strip,
+                             nb, k * sym, r * sym, off=off, length=length,
+                             stream=torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+        finally:
+            L.check(lib.pyrit_set_kernel_mode(0))
+        got = out.cpu().numpy()
+        for b in range(nb):
+            want = np.full((r, sym), 0x77, np.uint8)
+            outs = [want[i] for i in range(r)]
+            O.ring_replay(O.Field(f.w, f.n, f.kind, f.s, f.r_esp, f.modulus), m, [data[b, j].copy() for j in range(k)],
+                          strip, kind=kind, off=off, length=length, outs=outs)
+            np.testing.assert_array_equal(got[b], want, err_msg=f"case {case}: {f} k{k} r{r} kind{kind} strip{strip} "
+                                                               f"off{off} len{length} nb{nb} mode{mode} b{b}")
+        plan.close()
