@@ -134,16 +134,23 @@ int pyrit_field_validate(const pyrit_field* f) {
 }
 
 int pyrit_gf_mul(const pyrit_field* f, uint32_t a, uint32_t b, uint32_t* out) {
-    return guarded([&] { *out = gf_mul(a, b, to_field(f)); });
+    return guarded([&] {
+        if (!out) raise(Errc::InvalidArgument, "null argument");
+        *out = gf_mul(a, b, to_field(f));
+    });
 }
 
 int pyrit_gf_inv(const pyrit_field* f, uint32_t a, uint32_t* out) {
-    return guarded([&] { *out = gf_inv(a, to_field(f)); });
+    return guarded([&] {
+        if (!out) raise(Errc::InvalidArgument, "null argument");
+        *out = gf_inv(a, to_field(f));
+    });
 }
 
 int pyrit_sparse_transform(const pyrit_field* f, uint32_t u, uint32_t* rep) {
     return guarded([&] {
         const Field x = to_field(f);
+        if (!rep) raise(Errc::InvalidArgument, "null argument");
         if (u >= x.field_size()) raise(Errc::InvalidArgument, "element outside the field");
         *rep = sparse_transform(u, x);
     });
@@ -152,6 +159,7 @@ int pyrit_sparse_transform(const pyrit_field* f, uint32_t u, uint32_t* rep) {
 int pyrit_fold_table(const pyrit_field* f, uint32_t* fold) {
     return guarded([&] {
         const auto t = fold_table(to_field(f));
+        if (!fold) raise(Errc::InvalidArgument, "null argument");
         std::memcpy(fold, t.data(), t.size() * sizeof(uint32_t));
     });
 }
@@ -159,6 +167,7 @@ int pyrit_fold_table(const pyrit_field* f, uint32_t* fold) {
 int pyrit_cauchy_parity_matrix(const pyrit_code* code, uint16_t* out) {
     return guarded([&] {
         check_code(code);
+        if (!out) raise(Errc::InvalidArgument, "null argument");
         const Matrix m = cauchy_parity_matrix(code->k, code->r, to_field(&code->field));
         std::memcpy(out, m.e.data(), m.e.size() * sizeof(uint16_t));
     });
@@ -167,6 +176,7 @@ int pyrit_cauchy_parity_matrix(const pyrit_code* code, uint16_t* out) {
 int pyrit_decode_matrix(const pyrit_code* code, const uint32_t* survivors, uint16_t* out, uint32_t* rows) {
     return guarded([&] {
         check_code(code);
+        if (!survivors || !out || !rows) raise(Errc::InvalidArgument, "null argument");
         const Field f = to_field(&code->field);
         const Matrix c = cauchy_parity_matrix(code->k, code->r, f);
         const Matrix dm =
@@ -180,6 +190,8 @@ int pyrit_repair_matrix(const pyrit_code* code, const uint32_t* erased, uint32_t
                         uint32_t* outputs, uint16_t* matrix) {
     return guarded([&] {
         check_code(code);
+        if ((!erased && n_erased) || !survivors || (n_erased && (!outputs || !matrix)))
+            raise(Errc::InvalidArgument, "null argument");
         const RepairPlan rp = repair_matrix(code->k, code->r, to_field(&code->field),
                                             std::vector<uint32_t>(erased, erased + n_erased));
         std::memcpy(survivors, rp.survivors.data(), rp.survivors.size() * sizeof(uint32_t));

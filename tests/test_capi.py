@@ -96,3 +96,23 @@ def test_tuned_table_entries_match_current_plan_keys():
         plan = P.Plan.encode(wl.code) if wl.op == "encode" else P.Plan.decode(wl.code, wl.erased)
         current.add(plan.key())
     assert keys <= current, keys - current  # no stale rows (representatives changed)
+
+
+def test_null_arguments_are_errors_not_crashes():
+    """Every host entry point reports InvalidArgument (1 + Errc) for null outputs."""
+    lib = L.load()
+    f = P.FieldSpec.gf16_aop().c()
+    code = P.CodeSpec(4, 2, P.FieldSpec.gf16_aop()).c()
+    inv = 11  # 1 + Errc::InvalidArgument
+    assert lib.pyrit_gf_mul(C.byref(f), 2, 3, None) == inv
+    assert lib.pyrit_gf_inv(C.byref(f), 2, None) == inv
+    assert lib.pyrit_sparse_transform(C.byref(f), 2, None) == inv
+    assert lib.pyrit_fold_table(C.byref(f), None) == inv
+    assert lib.pyrit_cauchy_parity_matrix(C.byref(code), None) == inv
+    assert lib.pyrit_decode_matrix(C.byref(code), None, None, None) == inv
+    assert lib.pyrit_repair_matrix(C.byref(code), None, 1, None, None, None) == inv
+    assert lib.pyrit_header_parse(None, 29, None) == inv
+    assert lib.pyrit_encode_file(None, b"x", b"y", 16, 0) == inv
+    assert lib.pyrit_decode_file(None, 1, b"out", 0) == inv
+    assert lib.pyrit_cu_apply(None, None, None, 16, 0, 16, None) == inv
+    assert lib.pyrit_cu_apply_batch(None, None, None, 16, 0, 16, 1, 0, 0, None) == inv
