@@ -25,7 +25,7 @@ namespace {
 
 constexpr std::uint32_t kNone = 0xFFFFFFFFu;
 // bump whenever generated code changes for the same program (prebuilt cubins are keyed by name)
-constexpr int kGeneratorVersion = 10;
+constexpr int kGeneratorVersion = 11;
 
 // Greedy pair elimination over XOR targets.  Each target is a set of
 // variable ids; the most frequent pair (ties: smallest ids) becomes a new
@@ -469,7 +469,7 @@ std::string kernel_name(const Program& p, const KernelShape& ks) {
        << ',' << p.rows << ',' << p.cols << ',' << p.group << ',' << ks.lanes << ',' << ks.threads << ',' << ks.min_blocks << ','
        << ks.staged << ',' << ks.tile << ',' << ks.stages << ',' << ks.bar_bytes << ',' << p.parts.size() << ','
        << (p.parts.empty() ? 0u : p.parts[0].group) << ',' << ks.copy << ',' << p.cse << ',' << p.crs << ','
-       << ks.chunk << ',' << ks.split << ',';
+       << ks.chunk << ',' << ks.split << ',' << ks.half << ',';
     if (p.crs)
         for (std::uint16_t x : p.matrix) fp << 'c' << x;
     for (const Program& q : p.parts) fp << q.rows << '/' << q.cse << '/' << q.stats.xors << ',';
@@ -482,8 +482,8 @@ std::string kernel_name(const Program& p, const KernelShape& ks) {
                       ks.tile, ks.stages,
                       static_cast<unsigned long long>(fnv1a(fp.str())));
     else
-        std::snprintf(name, sizeof name, "pyrit_ring_k%u_e%u_w%u_n%u_L%u%s_%016llx", p.cols, p.rows, p.field.w,
-                      p.field.n, ks.lanes, ks.split > 1 ? ("p" + std::to_string(ks.split)).c_str() : "",
+        std::snprintf(name, sizeof name, "pyrit_ring_k%u_e%u_w%u_n%u_%s%u%s_%016llx", p.cols, p.rows, p.field.w,
+                      p.field.n, ks.half ? "H" : "L", ks.lanes, ks.split > 1 ? ("p" + std::to_string(ks.split)).c_str() : "",
                       static_cast<unsigned long long>(fnv1a(fp.str())));
     return name;
 }
@@ -753,8 +753,8 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
 std::string generate_cuda(const Program& p, const KernelShape& ks) {
     if (ks.staged) return generate_staged(p, ks);
     const std::uint32_t L = ks.lanes == 0 ? 1 : ks.lanes;
-    const bool bytes = ks.lanes == 0;
-    const std::uint32_t V = bytes ? 1 : 4 * L; // bytes per thread per strip
+    const bool bytes = ks.lanes == 0; // sub-word mode: one u8 (or u16 when ks.half) per thread per strip
+    const std::uint32_t V = bytes ? (ks.half ? 2 : 1) : 4 * L; // bytes per thread per strip
     // split: the output rows are divided over R thread groups (p.parts) that
     // walk the same column words; every group loads all input strips, the
     // first touch of a line fills L1 and the other groups hit it, so HBM
@@ -777,8 +777,9 @@ std::string generate_cuda(const Program& p, const KernelShape& ks) {
     // split, the other row groups re-read the line; stores: evict-first
     const std::string l1 = R > 1 ? "" : ".L1::no_allocate";
     if (bytes) {
-        o << "#define LD(v, p) asm(\"ld.global.nc" << l1 << ".u8 %0, [%1];\" : \"=r\"(v) : \"l\"(p))\n";
-        o << "#define ST(p, v) asm volatile(\"st.global.cs.u8 [%0], %1;\" :: \"l\"(p), \"r\"(v) : \"memory\")\n";
+        const char* ty = ks.half ? "u16" : "u8";
+        o << "#define LD(v, p) asm(\"ld.global.nc" << l1 << "." << ty << " %0, [%1];\" : \"=r\"(v) : \"l\"(p))\n";
+        o << "#define ST(p, v) asm volatile(\"st.global.cs." << ty << " [%0], %1;\" :: \"l\"(p), \"r\"(v) : \"memory\")\n";
     } else if (L == 1) {
         o << "#define LD(v, p) asm(\"ld.global.nc" << l1 << ".b32 %0, [%1];\" : \"=r\"(v##_0) : \"l\"(p))\n";
         o << "#define ST(p, v) asm volatile(\"st.global.cs.b32 [%0], %1;\" :: \"l\"(p), \"r\"(v##_0) : \"memory\")\n";

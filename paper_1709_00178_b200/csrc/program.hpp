@@ -120,6 +120,7 @@ struct KernelShape {
     std::uint32_t copy = 1;         // staged: 0 = TMA cp.async.bulk by warp 0, 1 = cp.async by every thread
     std::uint32_t chunk = 16;       // staged cp.async: bytes per copy (16; 8 or 4 for less aligned strips)
     std::uint32_t split = 0;        // direct: rows split over p.parts.size() thread groups (0/1 = no split)
+    std::uint32_t half = 0;         // direct sub-word mode: 1 = 2-byte elements (u16), 0 = bytes
 };
 std::string kernel_name(const Program& p, const KernelShape& ks);
 std::string generate_cuda(const Program& p, const KernelShape& ks);

@@ -297,7 +297,9 @@ KernelShape choose_shape(const Program& p, const std::uint8_t* const* in, std::u
             lanes = l;
             break;
         }
-    return direct_shape(p, lanes);
+    KernelShape ks = direct_shape(p, lanes);
+    if (lanes == 0 && all_aligned(2)) ks.half = 1; // e.g. GF(2^12) symbols of 24k bytes: 2-byte strips
+    return ks;
 }
 
 std::string prepare_program(const Program& p, std::uint32_t lanes) {
@@ -345,7 +347,7 @@ LaunchInfo launch_batch(const Program& p, const std::uint8_t* const* in, std::ui
         tail[2] = len; // bytes; tiles of ks.tile bytes per strip
         want = (len + ks.tile - 1) / ks.tile * nb;
     } else {
-        const std::uint64_t vbytes = ks.lanes ? 4ull * ks.lanes : 1ull;
+        const std::uint64_t vbytes = ks.lanes ? 4ull * ks.lanes : ks.half ? 2ull : 1ull;
         nwords = len / vbytes;
         tail[2] = nwords;
         want = (nwords * nb + cpb - 1) / cpb;

@@ -132,10 +132,15 @@ def test_odd_strip_sizes_byte_mode(cuda):
     """Strips that are not word multiples (SymbolBuffer allows any multiple of lcm(w, 8))."""
     for spec, k, r in [(G16, 4, 2), (G64, 5, 3), (G256, 10, 4), (G4096, 16, 4)]:
         code = P.CodeSpec(k, r, spec)
-        ss = int(np.lcm(spec.w, 8)) * 3  # strip of 6, 12, 3, 6 bytes
-        data = rand_symbols(k, ss, 5)
-        np.testing.assert_array_equal(dev_encode(cuda, code, data),
-                                      oracle_encode(spec, P.cauchy_parity_matrix(code), data))
+        for mult in (3, 171):  # strips of 6/12/3/6 bytes and 342/684/171/342 (u8 / u16 elements)
+            ss = int(np.lcm(spec.w, 8)) * mult
+            data = rand_symbols(k, ss, 5)
+            np.testing.assert_array_equal(dev_encode(cuda, code, data),
+                                          oracle_encode(spec, P.cauchy_parity_matrix(code), data))
+    # the 2-byte element kernel is the one a 342-byte strip takes
+    code = P.CodeSpec(16, 4, G4096)
+    dev_encode(cuda, code, rand_symbols(16, 4104, 6))
+    assert "_H0" in P.Plan.last_launch()["kernel"]
 
 
 def test_empty_and_degenerate(cuda):
