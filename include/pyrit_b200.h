@@ -173,6 +173,13 @@ int pyrit_cu_decode_batch(const pyrit_code* code, uint8_t* const* symbols, const
  * parity: r * symbol_size host bytes.  Synchronous. Pinned buffers overlap. */
 int pyrit_encode_host(const pyrit_code* code, const uint8_t* data, uint8_t* parity, uint64_t symbol_size,
                       int device);
+/* the same over several GPUs of one process: every strip is split into
+ * byte-offset shards (16-byte aligned), one per listed device, processed
+ * concurrently with no exchange; a device may repeat */
+int pyrit_encode_host_devices(const pyrit_code* code, const uint8_t* data, uint8_t* parity, uint64_t symbol_size,
+                              const int* devices, uint32_t n_devices);
+int pyrit_decode_host_devices(const pyrit_code* code, uint8_t* symbols, const uint32_t* erased, uint32_t n_erased,
+                              uint64_t symbol_size, const int* devices, uint32_t n_devices);
 /* encode_crs (codec.hpp:223-231) with host buffers */
 int pyrit_encode_crs_host(const pyrit_code* code, const uint8_t* data, uint8_t* parity, uint64_t symbol_size,
                           int device);

@@ -301,24 +301,38 @@ def decode(symbols, erased: Iterable[int], code: CodeSpec) -> None:
                                    symbols.shape[1], _stream_of(symbols)))
 
 
-def encode_host(data: np.ndarray, code: CodeSpec, device: int = 0, parity: np.ndarray | None = None) -> np.ndarray:
-    """encode with host buffers (H2D, fused kernel, D2H inside): data (k, symbol_size) uint8."""
+def encode_host(data: np.ndarray, code: CodeSpec, device: int = 0, parity: np.ndarray | None = None,
+                devices: Sequence[int] | None = None) -> np.ndarray:
+    """encode with host buffers (H2D, fused kernel, D2H inside): data (k, symbol_size) uint8.
+    `devices`: byte-offset shards over several GPUs, concurrently."""
     data = np.ascontiguousarray(data, dtype=np.uint8)
     if data.ndim != 2 or data.shape[0] != code.k:
         raise PyritError(4, "data buffer does not match the code")
     if parity is None:
         parity = np.empty((code.r, data.shape[1]), dtype=np.uint8)
-    L.check(_clib().pyrit_encode_host(C.byref(code.c()), data.ctypes.data, parity.ctypes.data, data.shape[1], device))
+    if devices:
+        dv = np.asarray(list(devices), dtype=np.int32)
+        L.check(_clib().pyrit_encode_host_devices(C.byref(code.c()), data.ctypes.data, parity.ctypes.data,
+                                                 data.shape[1], dv.ctypes.data, dv.size))
+    else:
+        L.check(_clib().pyrit_encode_host(C.byref(code.c()), data.ctypes.data, parity.ctypes.data, data.shape[1],
+                                         device))
     return parity
 
 
-def decode_host(symbols: np.ndarray, erased: Iterable[int], code: CodeSpec, device: int = 0) -> None:
+def decode_host(symbols: np.ndarray, erased: Iterable[int], code: CodeSpec, device: int = 0,
+                devices: Sequence[int] | None = None) -> None:
     """decode with host buffers, in place on a (k + r, symbol_size) uint8 array."""
     if symbols.ndim != 2 or symbols.shape[0] != code.k + code.r or not symbols.flags.c_contiguous:
         raise PyritError(4, "symbol buffer does not match the code")
     er = np.asarray(list(erased), dtype=np.uint32)
-    L.check(_clib().pyrit_decode_host(C.byref(code.c()), symbols.ctypes.data, er.ctypes.data, er.size,
-                                     symbols.shape[1], device))
+    if devices:
+        dv = np.asarray(list(devices), dtype=np.int32)
+        L.check(_clib().pyrit_decode_host_devices(C.byref(code.c()), symbols.ctypes.data, er.ctypes.data, er.size,
+                                                 symbols.shape[1], dv.ctypes.data, dv.size))
+    else:
+        L.check(_clib().pyrit_decode_host(C.byref(code.c()), symbols.ctypes.data, er.ctypes.data, er.size,
+                                         symbols.shape[1], device))
 
 
 def fill(t, seed: int, frag: int, begin: int = 0, valid: int | None = None, stream: int | None = None) -> None:

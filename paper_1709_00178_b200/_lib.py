@@ -55,7 +55,8 @@ EXPORTS = (
     "pyrit_cu_last_launch", "pyrit_jit_compiles", "pyrit_kernel_launches", "pyrit_cu_apply_batch",
     "pyrit_cu_encode_batch", "pyrit_cu_decode_batch", "pyrit_crc32", "pyrit_header_serialize", "pyrit_header_parse",
     "pyrit_field_id", "pyrit_field_from_id", "pyrit_shard_path", "pyrit_encode_file", "pyrit_decode_file",
-    "pyrit_set_file_chunk", "pyrit_cu_encode_crs", "pyrit_encode_crs_host",
+    "pyrit_set_file_chunk", "pyrit_cu_encode_crs", "pyrit_encode_crs_host", "pyrit_encode_host_devices",
+    "pyrit_decode_host_devices",
 )
 
 HEADER_SIZE = 29
@@ -96,6 +97,8 @@ def load():
     lib.pyrit_cu_encode.argtypes = [P(pyrit_code), vp, vp, u64, vp]
     lib.pyrit_cu_encode_crs.argtypes = [P(pyrit_code), vp, vp, u64, vp]
     lib.pyrit_encode_crs_host.argtypes = [P(pyrit_code), vp, vp, u64, i32]
+    lib.pyrit_encode_host_devices.argtypes = [P(pyrit_code), vp, vp, u64, vp, u32]
+    lib.pyrit_decode_host_devices.argtypes = [P(pyrit_code), vp, vp, u32, u64, vp, u32]
     lib.pyrit_cu_decode.argtypes = [P(pyrit_code), vp, vp, u32, u64, vp]
     lib.pyrit_encode_host.argtypes = [P(pyrit_code), vp, vp, u64, i32]
     lib.pyrit_decode_host.argtypes = [P(pyrit_code), vp, vp, u32, u64, i32]

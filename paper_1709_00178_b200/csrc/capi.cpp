@@ -432,6 +432,38 @@ int pyrit_encode_host(const pyrit_code* code, const uint8_t* data, uint8_t* pari
     });
 }
 
+int pyrit_encode_host_devices(const pyrit_code* code, const uint8_t* data, uint8_t* parity, uint64_t symbol_size,
+                              const int* devices, uint32_t n_devices) {
+    return guarded([&] {
+        check_code(code);
+        const std::uint64_t strip = strip_of(code, symbol_size);
+        if (!data || (!parity && code->r) || !devices || !n_devices) raise(Errc::InvalidArgument, "null argument");
+        if (code->r == 0) return;
+        auto p = encode_program(code);
+        std::vector<const uint8_t*> in;
+        std::vector<uint8_t*> out;
+        for (uint32_t j = 0; j < code->k; ++j) in.push_back(data + std::uint64_t(j) * symbol_size);
+        for (uint32_t i = 0; i < code->r; ++i) out.push_back(parity + std::uint64_t(i) * symbol_size);
+        run_host_devices(*p, in, out, strip, std::vector<int>(devices, devices + n_devices));
+    });
+}
+
+int pyrit_decode_host_devices(const pyrit_code* code, uint8_t* symbols, const uint32_t* erased, uint32_t n_erased,
+                              uint64_t symbol_size, const int* devices, uint32_t n_devices) {
+    return guarded([&] {
+        check_code(code);
+        const std::uint64_t strip = strip_of(code, symbol_size);
+        if (!symbols || (!erased && n_erased) || !devices || !n_devices) raise(Errc::InvalidArgument, "null argument");
+        const DecodeProgram d = decode_program(code, std::vector<uint32_t>(erased, erased + n_erased));
+        if (!d.prog) return;
+        std::vector<const uint8_t*> in;
+        std::vector<uint8_t*> out;
+        for (uint32_t s : d.repair.survivors) in.push_back(symbols + std::uint64_t(s) * symbol_size);
+        for (uint32_t o : d.repair.outputs) out.push_back(symbols + std::uint64_t(o) * symbol_size);
+        run_host_devices(*d.prog, in, out, strip, std::vector<int>(devices, devices + n_devices));
+    });
+}
+
 int pyrit_encode_crs_host(const pyrit_code* code, const uint8_t* data, uint8_t* parity, uint64_t symbol_size,
                           int device) {
     return guarded([&] {

@@ -10,6 +10,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <thread>
 
 namespace pyrit_b200 {
 
@@ -49,9 +50,42 @@ void set_host_chunk(std::uint64_t bytes) { g_chunk = bytes; }
 
 void run_host(const Program& p, const std::vector<const std::uint8_t*>& host_in,
               const std::vector<std::uint8_t*>& host_out, std::uint64_t strip, int device) {
+    run_host_window(p, host_in, host_out, strip, 0, strip, device);
+}
+
+void run_host_devices(const Program& p, const std::vector<const std::uint8_t*>& host_in,
+                      const std::vector<std::uint8_t*>& host_out, std::uint64_t strip,
+                      const std::vector<int>& devices) {
+    if (devices.empty()) raise(Errc::InvalidArgument, "no devices");
+    // byte-offset shards of every strip: device d owns
+    // [floor(d S / N), floor((d+1) S / N)) rounded down to 16 bytes, the last
+    // one takes the tail; the shards are independent, one host thread each
+    const std::size_t n = devices.size();
+    std::vector<std::exception_ptr> errs(n);
+    std::vector<std::thread> th;
+    for (std::size_t d = 0; d < n; ++d) {
+        const std::uint64_t lo = strip * d / n / 16 * 16;
+        const std::uint64_t hi = d + 1 == n ? strip : strip * (d + 1) / n / 16 * 16;
+        th.emplace_back([&, d, lo, hi] {
+            try {
+                run_host_window(p, host_in, host_out, strip, lo, hi - lo, devices[d]);
+            } catch (...) {
+                errs[d] = std::current_exception();
+            }
+        });
+    }
+    for (auto& x : th) x.join();
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+}
+
+void run_host_window(const Program& p, const std::vector<const std::uint8_t*>& host_in,
+                     const std::vector<std::uint8_t*>& host_out, std::uint64_t strip, std::uint64_t off,
+                     std::uint64_t win, int device) {
     const std::uint32_t w = p.field.w;
     if (host_in.size() != p.cols || host_out.size() != p.rows) raise(Errc::BufferShape, "symbol count mismatch");
-    if (p.rows == 0 || strip == 0) return;
+    if (off + win > strip) raise(Errc::BufferShape, "column window out of range");
+    if (p.rows == 0 || win == 0) return;
     DeviceCtx& ctx = ctx_for(device);
     std::lock_guard<std::mutex> lk(ctx.mu);
     check_cuda(cudaSetDevice(device), "cudaSetDevice");
@@ -64,9 +98,9 @@ void run_host(const Program& p, const std::vector<const std::uint8_t*>& host_in,
         chunk = ((mib ? mib : 192) << 20) / strips; // ~192 MiB of staging per slot
     }
     chunk = std::max<std::uint64_t>(chunk, 64 * 1024) & ~std::uint64_t(4095);
-    if (strip % 16 == 0) chunk = std::min(chunk, strip);
-    else chunk = std::min(chunk, strip & ~std::uint64_t(15)); // tail chunk handled in byte mode
-    if (chunk == 0) chunk = strip;
+    if (win % 16 == 0) chunk = std::min(chunk, win);
+    else chunk = std::min(chunk, win & ~std::uint64_t(15)); // tail chunk handled in byte mode
+    if (chunk == 0) chunk = win;
     const std::size_t need = static_cast<std::size_t>(strips * chunk);
     for (Slot& s : ctx.slots) {
         if (!s.stream) check_cuda(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "stream");
@@ -92,9 +126,9 @@ void run_host(const Program& p, const std::vector<const std::uint8_t*>& host_in,
     const auto out_runs = runs(host_out);
     std::vector<const std::uint8_t*> din(p.cols);
     std::vector<std::uint8_t*> dout(p.rows);
-    std::uint64_t c0 = 0;
-    for (int c = 0; c0 < strip; ++c) {
-        const std::uint64_t len = std::min(chunk, strip - c0);
+    std::uint64_t c0 = off;
+    for (int c = 0; c0 < off + win; ++c) {
+        const std::uint64_t len = std::min(chunk, off + win - c0);
         Slot& s = ctx.slots[c % kSlots];
         for (std::uint32_t j = 0; j < p.cols; ++j) din[j] = s.buf + std::uint64_t(j) * w * chunk;
         for (std::uint32_t i = 0; i < p.rows; ++i) dout[i] = s.buf + std::uint64_t(p.cols + i) * w * chunk;

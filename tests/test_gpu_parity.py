@@ -216,6 +216,27 @@ def test_host_buffer_path(cuda, cfg):
         L.check(L.load().pyrit_set_host_chunk(0))
 
 
+@pytest.mark.parametrize("cfg", [3, 4, 5])
+def test_host_buffer_path_device_shards(cuda, cfg):
+    """pyrit_encode_host_devices / _decode_host_devices: byte-offset shards processed
+    concurrently (here 3 shards on the one visible device: the sharding and window
+    arithmetic; no shard waits on another) == the single-device path."""
+    import torch
+    wl = WORKLOADS[cfg]
+    ss = wl.fld.w * ((1 << 16) + 16 * 7)  # strip not divisible into equal 16-byte shards
+    data = seeded_symbols(wl.k, ss, wl.fld.w, wl.seed)
+    devs = [0] * 3
+    parity = P.encode_host(data, wl.code, devices=devs)
+    np.testing.assert_array_equal(parity, dev_encode(cuda, wl.code, data))
+    full = np.concatenate([data, parity])
+    erased = list(wl.erased) or [0, 5, wl.k, wl.k + wl.m - 1]
+    work = full.copy()
+    work[erased] = 0
+    P.decode_host(work, erased, wl.code, devices=devs)
+    np.testing.assert_array_equal(work, full)
+    assert torch.cuda.device_count() >= 1
+
+
 @pytest.mark.parametrize("lanes", [1, 2, 4])
 def test_vector_widths(cuda, lanes):
     """The 4/8/16-byte-per-thread variants of the generated kernel agree."""
