@@ -25,7 +25,7 @@ namespace {
 
 constexpr std::uint32_t kNone = 0xFFFFFFFFu;
 // bump whenever generated code changes for the same program (prebuilt cubins are keyed by name)
-constexpr int kGeneratorVersion = 11;
+constexpr int kGeneratorVersion = 12;
 
 // Greedy pair elimination over XOR targets.  Each target is a set of
 // variable ids; the most frequent pair (ties: smallest ids) becomes a new
@@ -600,7 +600,6 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
     // programmatic dependent launch: everything above overlaps the previous
     // grid's tail; global memory is touched only after it has completed
     o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
-    o << "  asm volatile(\"griddepcontrol.launch_dependents;\" ::: \"memory\");\n";
     o << "  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;\n";
     // produce(u2): fill the slot of pipeline unit u2 = (tile it2, fragment group g2)
     o << "  u64 pol = 0;\n";
@@ -744,6 +743,9 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
         for (const Instr& x : q.tail) emit(x);
         o << "   }\n  }\n";
     }
+    // dependents may launch once this CTA has issued all its work: they take
+    // over the SMs freed by the tail without pre-launching during the body
+    o << "  asm volatile(\"griddepcontrol.launch_dependents;\" ::: \"memory\");\n";
     o << "}\n";
     return o.str();
 }
@@ -799,7 +801,6 @@ std::string generate_cuda(const Program& p, const KernelShape& ks) {
       << "(const Args a)\n{\n";
     o << "  const u64 S = a.S;\n";
     o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
-    o << "  asm volatile(\"griddepcontrol.launch_dependents;\" ::: \"memory\");\n";
     o << "  const u32 part = threadIdx.x / " << CPB << "u;\n";
     o << "  const u64 c0 = (u64)blockIdx.x * " << CPB << "u + threadIdx.x % " << CPB << "u;\n";
     auto var = [&](std::uint32_t v, std::uint32_t l) {
@@ -864,6 +865,7 @@ std::string generate_cuda(const Program& p, const KernelShape& ks) {
         o << "    if (cw >= a.nwords) { cw -= a.nwords; ++b; }\n";
         o << "  }\n  }\n";
     }
+    o << "  asm volatile(\"griddepcontrol.launch_dependents;\" ::: \"memory\");\n";
     o << "}\n";
     return o.str();
 }
