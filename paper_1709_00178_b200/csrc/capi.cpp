@@ -2,6 +2,7 @@
 // and maps errors to return codes; nothing throws across the ABI.
 #include "../../include/pyrit_b200.h"
 
+#include <cstdlib>
 #include <cstring>
 #include <list>
 #include <memory>
@@ -289,6 +290,10 @@ int pyrit_plan_source(const pyrit_plan* plan, uint32_t lanes, char* buf, size_t 
             ks = staged_shape(plan->prog, 227 * 1024);
             if (!ks.staged) raise(Errc::BufferShape, "program tiles do not fit in shared memory");
             ks.chunk = lanes == PYRIT_SOURCE_STAGED ? 16 : lanes - PYRIT_SOURCE_STAGED;
+            if (const char* env = std::getenv("PYRIT_B200_COPY")) { // same producer the runtime would pick
+                const int c = std::atoi(env);
+                ks.copy = c == 2 ? 2u : c ? 1u : 0u;
+            }
         }
         const std::string src = generate_cuda(plan->prog, ks);
         const std::string nm = kernel_name(plan->prog, ks);

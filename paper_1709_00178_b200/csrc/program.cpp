@@ -25,7 +25,7 @@ namespace {
 
 constexpr std::uint32_t kNone = 0xFFFFFFFFu;
 // bump whenever generated code changes for the same program (prebuilt cubins are keyed by name)
-constexpr int kGeneratorVersion = 12;
+constexpr int kGeneratorVersion = 13;
 
 // Greedy pair elimination over XOR targets.  Each target is a set of
 // variable ids; the most frequent pair (ties: smallest ids) becomes a new
@@ -478,7 +478,7 @@ std::string kernel_name(const Program& p, const KernelShape& ks) {
     char name[112];
     if (ks.staged)
         std::snprintf(name, sizeof name, "pyrit_ring_k%u_e%u_w%u_n%u_%s%ux%u_%016llx", p.cols, p.rows, p.field.w,
-                      p.field.n, !ks.copy ? "tma" : ks.chunk == 16 ? "cpa" : ks.chunk == 8 ? "cpa8_" : "cpa4_",
+                      p.field.n, ks.copy == 2 ? "tmt" : !ks.copy ? "tma" : ks.chunk == 16 ? "cpa" : ks.chunk == 8 ? "cpa8_" : "cpa4_",
                       ks.tile, ks.stages,
                       static_cast<unsigned long long>(fnv1a(fp.str())));
     else
@@ -547,7 +547,8 @@ std::string generate_staged(const Program& p, const KernelShape& ks) {
     std::uint64_t part_xors = 0;
     for (const Program& q : p.parts) part_xors += q.stats.xors;
     std::ostringstream o;
-    o << "// generated by pyrit_b200 program compiler (staged, " << (ks.copy ? "cp.async" : "TMA cp.async.bulk")
+    o << "// generated by pyrit_b200 program compiler (staged, "
+      << (ks.copy == 2 ? "TMA tensor boxes" : ks.copy ? "cp.async" : "TMA cp.async.bulk")
       << "): field w=" << w << " n=" << p.field.n << " p=0x" << std::hex << p.field.modulus << std::dec << ", "
       << p.rows << "x" << k << " ring matrix in " << R << " output part(s), " << part_xors
       << " XORs per column word (naive ring program " << p.stats.naive_xors << ", reference schedule "
@@ -555,8 +556,11 @@ std::string generate_staged(const Program& p, const KernelShape& ks) {
       << NSLOT << " slots x " << G << " fragment(s)\n";
     o << "typedef unsigned int u32; typedef unsigned long long u64; typedef unsigned char u8;\n";
     // nb stripes of the batch: input j of stripe b at in[j] + b * ibp, output i at out[i] + b * obp
+    if (ks.copy == 2) // one 3D tensor map per input fragment: (column element, strip, stripe)
+        o << "struct alignas(64) TMap { u64 v[16]; };\n";
     o << "struct Args { const u8* in[" << k << "]; u8* out[" << p.rows
-      << "]; u64 S; u64 off; u64 len; u64 nb; u64 ibp; u64 obp; };\n";
+      << "]; u64 S; u64 off; u64 len; u64 nb; u64 ibp; u64 obp;" << (ks.copy == 2 ? " TMap tm[" + std::to_string(k) + "];" : "")
+      << " };\n";
     o << R"(static __device__ __forceinline__ u32 smem_u32(const void* p) {
   u32 r; asm("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(r) : "l"(p)); return r; }
 static __device__ __forceinline__ void mbar_init(u32 bar, u32 count) {
@@ -571,6 +575,9 @@ static __device__ __forceinline__ void mbar_wait(u32 bar, u32 parity) {
 static __device__ __forceinline__ void bulk_g2s(u32 dst, const void* src, u32 bytes, u32 bar, u64 pol) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
                :: "r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory"); }
+static __device__ __forceinline__ void tma3d(u32 dst, const void* map, u32 x, u32 y, u32 z, u32 bar) {
+  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+               :: "r"(dst), "l"(map), "r"(x), "r"(y), "r"(z), "r"(bar) : "memory"); }
 static __device__ __forceinline__ void cpa16(u32 dst, const void* src, u32 n) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(dst), "l"(src), "r"(n) : "memory"); }
 static __device__ __forceinline__ void cpa8(u32 dst, const void* src, u32 n) {
@@ -593,7 +600,7 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
     o << "  const u32 tpb = (u32)((a.len + TILE - 1) / TILE);\n"; // tiles per stripe
     o << "  const u32 ntiles = tpb * (u32)a.nb;\n";
     o << "  if (threadIdx.x == 0) {\n";
-    o << "    for (u32 s = 0; s < NSLOT; ++s) { mbar_init(FULL(s), " << (ks.copy ? T : 1u) << "u); mbar_init(EMPTY(s), "
+    o << "    for (u32 s = 0; s < NSLOT; ++s) { mbar_init(FULL(s), " << (ks.copy == 1 ? T : 1u) << "u); mbar_init(EMPTY(s), "
       << T << "u); }\n";
     o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n  }\n";
     o << "  __syncthreads();\n";
@@ -604,7 +611,26 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
     // produce(u2): fill the slot of pipeline unit u2 = (tile it2, fragment group g2)
     o << "  u64 pol = 0;\n";
     if (!ks.copy) o << "  if (warp == 0) asm volatile(\"createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\" : \"=l\"(pol));\n";
-    if (ks.copy) {
+    if (ks.copy == 2) {
+        // TMA tensor copies: one elected thread posts the unit's byte count and
+        // issues one 3D box (all w strips x TILE bytes of a fragment) per
+        // fragment of the group; no other thread takes part in the copy
+        const std::uint32_t elem = TILE > 1024 ? 8u : 4u;
+        o << "  auto produce = [&](u32 u2) {\n";
+        o << "    const u32 it2 = u2 / NG, g2 = u2 - it2 * NG;\n";
+        o << "    const u32 t2 = blockIdx.x + it2 * gridDim.x;\n";
+        o << "    if (t2 >= ntiles) return;\n";
+        o << "    const u32 sl = u2 % NSLOT, ph = (u2 / NSLOT) & 1u;\n";
+        o << "    mbar_wait(EMPTY(sl), ph ^ 1u);\n";
+        o << "    const u32 b2 = t2 / tpb, tt2 = t2 - b2 * tpb;\n";
+        o << "    const u32 x = (u32)((a.off + (u64)tt2 * TILE) / " << elem << "u);\n";
+        o << "    const u32 dst = sbase + BAR_BYTES + sl * SLOT_BYTES;\n";
+        o << "    const u32 j0 = g2 * " << G << "u;\n";
+        o << "    const u32 nfr = g2 + 1u == NG ? " << k << "u - j0 : " << G << "u;\n";
+        o << "    mbar_expect_tx(FULL(sl), nfr * " << w * TILE << "u);\n";
+        o << "#pragma unroll 1\n";
+        o << "    for (u32 f = 0; f < nfr; ++f) tma3d(dst + f * " << w * TILE << "u, &a.tm[j0 + f], x, 0u, b2, FULL(sl));\n";
+    } else if (ks.copy) {
         // every thread copies CH-byte chunks (16, or 8/4 when the strips are
         // only that aligned; a strip tile is TILE/CH consecutive chunks:
         // coalesced) and arrives on the slot's FULL barrier once its copies
@@ -686,7 +712,7 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
         o << "    }\n";
     }
     o << "  };\n";
-    const std::string who = ks.copy ? "" : "if (warp == 0) ";
+    const std::string who = ks.copy == 1 ? "" : ks.copy == 2 ? "if (threadIdx.x == 0) " : "if (warp == 0) ";
     o << "  " << who << "for (u32 u = 0; u + 1 < NSLOT; ++u) produce(u);\n";
     o << "  const u32 part = threadIdx.x / " << cols_per_part << "u, col = threadIdx.x % " << cols_per_part << "u;\n";
     o << "  const u64 S = a.S;\n";
@@ -729,7 +755,8 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
             // read its strips from shared memory, release the slot, XOR
             const std::string gs = std::to_string(g);
             o << "    const u32 un" << gs << " = it * NG + " << g << "u;\n";
-            if (ks.copy) o << "    produce(un" << gs << " + NSLOT - 1u);\n";
+            if (ks.copy == 1) o << "    produce(un" << gs << " + NSLOT - 1u);\n";
+            else if (ks.copy == 2 && r == 0) o << "    if (threadIdx.x == 0) produce(un" << gs << " + NSLOT - 1u);\n";
             else if (r == 0) o << "    if (warp == 0) produce(un" << gs << " + NSLOT - 1u);\n";
             o << "    const u32 sl" << gs << " = un" << gs << " % NSLOT;\n";
             o << "    mbar_wait(FULL(sl" << gs << "), (un" << gs << " / NSLOT) & 1u);\n";

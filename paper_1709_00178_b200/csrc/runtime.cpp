@@ -5,6 +5,7 @@
 #include <nvrtc.h>
 
 #include <atomic>
+#include <cstring>
 #include <cstdlib>
 #include <fstream>
 #include <iterator>
@@ -32,6 +33,9 @@ struct Driver {
     CUresult (*getErrorString)(CUresult, const char**) = nullptr;
     CUresult (*funcSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
     CUresult (*launchKernelEx)(const CUlaunchConfig*, CUfunction, void**, void**) = nullptr;
+    CUresult (*tensorMapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill) = nullptr;
 };
 
 template <class F>
@@ -54,6 +58,7 @@ const Driver& driver() {
         resolve("cuGetErrorString", d.getErrorString);
         resolve("cuFuncSetAttribute", d.funcSetAttribute);
         resolve("cuLaunchKernelEx", d.launchKernelEx);
+        resolve("cuTensorMapEncodeTiled", d.tensorMapEncodeTiled);
     });
     return d;
 }
@@ -237,7 +242,8 @@ int env_int(const char* name, int dflt) {
 // staged shape for p (PYRIT_B200_COPY=0 selects the TMA bulk-copy producer)
 KernelShape staged_for(const Program& p) {
     KernelShape ks = staged_shape(p, 227 * 1024);
-    ks.copy = env_int("PYRIT_B200_COPY", static_cast<int>(ks.copy)) ? 1u : 0u;
+    const int copy = env_int("PYRIT_B200_COPY", static_cast<int>(ks.copy));
+    ks.copy = copy == 2 ? 2u : copy ? 1u : 0u;
     return ks;
 }
 
@@ -274,7 +280,7 @@ KernelShape choose_shape(const Program& p, const std::uint8_t* const* in, std::u
     if (kernel_mode() != 1 && chunk) {
         KernelShape ks = staged_for(p);
         ks.chunk = chunk;
-        if (!ks.copy && chunk != 16) ks.staged = false;
+        if (ks.copy != 1 && chunk != 16) ks.staged = false; // TMA needs 16-byte alignment
         // auto mode keeps the staged kernel where it measured faster than the
         // direct one (profiles/r01_s2/sizes_*): 16-byte chunks, at most two
         // output parts, and per-stripe windows that fill at least half a tile
@@ -331,7 +337,11 @@ LaunchInfo launch_batch(const Program& p, const std::uint8_t* const* in, std::ui
     const KernelShape ks = choose_shape(p, in, out, strip, off, len, nb, in_pitch, out_pitch);
     const LoadedKernel k = load_kernel(p, ks, dev);
     // Args: in[cols], out[rows], S, off, len|nwords, nb, ibp, obp (, sq, sr)
-    std::vector<std::uint64_t> args(std::size_t(p.cols) + p.rows + 8, 0);
+    // (, tensor maps tm[cols] at the next 64-byte boundary for TMA tensor copies)
+    const std::size_t head = std::size_t(p.cols) + p.rows + 8;
+    const std::size_t tm_off = (8 * (std::size_t(p.cols) + p.rows + 6) + 63) / 64 * 8; // in u64 words
+    const bool tensor = ks.staged && ks.copy == 2;
+    std::vector<std::uint64_t> args(tensor ? tm_off + 16 * std::size_t(p.cols) : head, 0);
     for (std::uint32_t j = 0; j < p.cols; ++j) args[j] = reinterpret_cast<std::uint64_t>(in[j]);
     for (std::uint32_t i = 0; i < p.rows; ++i) args[p.cols + i] = reinterpret_cast<std::uint64_t>(out[i]);
     std::uint64_t* tail = &args[p.cols + p.rows];
@@ -353,6 +363,24 @@ LaunchInfo launch_batch(const Program& p, const std::uint8_t* const* in, std::ui
         want = (nwords * nb + cpb - 1) / cpb;
     }
     const unsigned blocks = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min(want, cap)));
+    if (tensor) {
+        // 3D map per input: (column element, strip, stripe); box = one tile of
+        // all w strips of one stripe; elements of 4 bytes (8 for 2 KiB tiles)
+        const std::uint32_t elem = ks.tile > 1024 ? 8 : 4;
+        for (std::uint32_t j = 0; j < p.cols; ++j) {
+            CUtensorMap m;
+            const cuuint64_t dims[3] = {strip / elem, p.field.w, nb};
+            const cuuint64_t strides[2] = {strip, nb > 1 ? in_pitch : strip * p.field.w};
+            const cuuint32_t box[3] = {ks.tile / elem, p.field.w, 1};
+            const cuuint32_t es[3] = {1, 1, 1};
+            check_cu(driver().tensorMapEncodeTiled(&m, elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32,
+                                                   3, const_cast<std::uint8_t*>(in[j]), dims, strides, box, es,
+                                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+                     "cuTensorMapEncodeTiled");
+            std::memcpy(&args[tm_off + 16 * std::size_t(j)], &m, sizeof m);
+        }
+    }
     if (!ks.staged) {
         const std::uint64_t stride = std::uint64_t(blocks) * cpb;
         tail[6] = stride / nwords;
