@@ -389,7 +389,7 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
         // (60,20) GF(2^6) codes, profiles/r01_s2): the fewest parts -- every
         // part re-reads all input strips from shared memory -- that keep
         // <= 128 accumulators per thread; 512-thread CTAs when a part's
-        // accumulators are few (<= 48), else 256 (255 registers); and the
+        // accumulators are few (<= 64), else 256 (255 registers); and the
         // largest fragment group whose slot still lets 3 slots fit in shared
         // memory, since every (tile, group) unit costs a barrier round trip.
         if (!R) { // a power of two (it must divide the CTA) no larger than e
@@ -398,7 +398,7 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
         }
         R = std::max<std::uint32_t>(1, std::min(R, e));
         const std::uint32_t acc = (e + R - 1) / R * acc_rows;
-        if (!p.staged_threads) p.staged_threads = acc <= 48 ? 512 : 256;
+        if (!p.staged_threads) p.staged_threads = acc <= 64 ? 512 : 256;
         std::uint32_t pg = opt.part_group;
         if (!pg && env_u("PYRIT_B200_PART_GROUP") > 0) pg = static_cast<std::uint32_t>(env_u("PYRIT_B200_PART_GROUP"));
         if (!pg && tuned) pg = tuned->part_group;

@@ -117,7 +117,8 @@ struct KernelShape {
     std::uint32_t stages = 2;       // staged: shared-memory ring depth
     std::uint32_t bar_bytes = 128;  // staged: mbarrier area at the start of shared memory
     std::uint32_t smem_bytes = 0;   // staged: dynamic shared memory per CTA
-    std::uint32_t copy = 1;         // staged: 0 = TMA cp.async.bulk by warp 0, 1 = cp.async by every thread
+    std::uint32_t copy = 2;         // staged producer: 2 = TMA tensor boxes (one elected thread), 1 = cp.async by
+                                    // every thread (any 4/8/16-byte alignment), 0 = TMA 1D bulk copies by warp 0
     std::uint32_t chunk = 16;       // staged cp.async: bytes per copy (16; 8 or 4 for less aligned strips)
     std::uint32_t split = 0;        // direct: rows split over p.parts.size() thread groups (0/1 = no split)
     std::uint32_t half = 0;         // direct sub-word mode: 1 = 2-byte elements (u16), 0 = bytes

@@ -280,7 +280,7 @@ KernelShape choose_shape(const Program& p, const std::uint8_t* const* in, std::u
     if (kernel_mode() != 1 && chunk) {
         KernelShape ks = staged_for(p);
         ks.chunk = chunk;
-        if (ks.copy != 1 && chunk != 16) ks.staged = false; // TMA needs 16-byte alignment
+        if (ks.copy != 1 && chunk != 16) ks.copy = 1; // TMA needs 16-byte alignment: cp.async chunks
         // auto mode keeps the staged kernel where it measured faster than the
         // direct one (profiles/r01_s2/sizes_*): 16-byte chunks, at most two
         // output parts, and per-stripe windows that fill at least half a tile

@@ -76,7 +76,9 @@ def test_plans_describe_themselves():
     st = plan.stats()
     assert (st["rows"], st["cols"], st["ref_region_ops"]) == (4, 16, 2808)
     name, src = plan.source(L.SOURCE_STAGED)
-    assert name.startswith("pyrit_ring_k16_e4_w12_n13_cpa") and "cp.async.cg.shared.global" in src
+    assert name.startswith("pyrit_ring_k16_e4_w12_n13_tmt") and "cp.async.bulk.tensor.3d" in src
+    name8, src8 = plan.source(L.SOURCE_STAGED + 8)  # 8-byte aligned strips: cp.async producer
+    assert "_cpa8_" in name8 and "cp.async.ca.shared.global" in src8
     assert "mbarrier.try_wait.parity" in src and "__grid_constant__" in src
     name1, src1 = plan.source(1)
     assert "_L1_" in name1 and "ld.global.nc" in src1
