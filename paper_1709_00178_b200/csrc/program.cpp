@@ -524,7 +524,16 @@ KernelShape staged_shape(const Program& p, std::uint32_t smem_limit) {
         ks.bar_bytes = bar;
         ks.threads = threads;
         ks.smem_bytes = static_cast<std::uint32_t>(bar + slots * slot);
-        (void)k;
+        // producer (profiles/r01_s2/sizes_*copy*, tune_*_v13_tma): TMA tensor
+        // boxes pay off when a box (all w strips of a fragment tile) is large
+        // and the XOR work per input word is high (the BASELINE codes: 8-24 KB
+        // boxes, 8-14 XORs per input word); light codes (GF(2^4)) and small
+        // boxes (512 B tiles of the split (60,40) code) stream faster with
+        // every thread issuing cp.async
+        std::uint64_t xors = 0;
+        for (const Program& q : p.parts) xors += q.stats.xors;
+        const bool heavy = xors >= 6ull * k * w;
+        ks.copy = (heavy && std::uint64_t(w) * tile >= 6144) ? 2u : 1u;
         return ks;
     }
     ks.staged = false;
