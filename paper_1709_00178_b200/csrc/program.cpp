@@ -532,7 +532,7 @@ KernelShape staged_shape(const Program& p, std::uint32_t smem_limit) {
         // every thread issuing cp.async
         std::uint64_t xors = 0;
         for (const Program& q : p.parts) xors += q.stats.xors;
-        const bool heavy = xors >= 6ull * k * w;
+        const bool heavy = xors >= 8ull * k * w;
         ks.copy = (heavy && std::uint64_t(w) * tile >= 6144) ? 2u : 1u;
         return ks;
     }
