@@ -333,3 +333,37 @@ def test_encode_decode_batch_vs_oracle(cuda, f, k, r, ss, nb):
     P.decode_batch(full, erased, c)
     torch.cuda.synchronize()
     assert torch.equal(full, ref)
+
+
+# ------------------------------------------- file codec validation (no device)
+def test_file_codec_validation_before_any_device_work(tmp_path):
+    """encode_file / decode_file reject bad arguments and damaged shard sets with the
+    reference's error codes before touching a GPU (container.hpp:170-172, :229-275)."""
+    spit(tmp_path / "in.bin", random_bytes(1000, 1))
+    with pytest.raises(P.PyritError) as ei:
+        P.encode_file(tmp_path / "in.bin", tmp_path / "o", code(4, 2, G16), 12)  # not a multiple of 8
+    assert ei.value.code == "BufferShape"
+    with pytest.raises(P.PyritError) as ei:
+        P.encode_file(tmp_path / "in.bin", tmp_path / "o", code(4, 20, G16), 16)  # k + r > 16
+    assert ei.value.code == "TooManySymbols"
+    with pytest.raises(P.PyritError) as ei:
+        P.encode_file(tmp_path / "missing.bin", tmp_path / "o", code(4, 2, G16), 16)
+    assert ei.value.code == "IoError"
+    with pytest.raises(P.PyritError) as ei:
+        P.decode_file([], tmp_path / "out.bin")
+    assert ei.value.code == "InsufficientShards"
+    with pytest.raises(P.PyritError) as ei:
+        P.decode_file([tmp_path / "nope.pyrit"], tmp_path / "out.bin")
+    assert ei.value.code == "IoError"
+    # shard files written by the reference (no GPU involved) feed the validation paths
+    shards = O.encode_file(tmp_path / "in.bin", tmp_path / "ref", 4, 2, O.GF16, 64)
+    bad = tmp_path / "bad.pyrit"
+    b = bytearray(slurp(shards[0]))
+    b[0] = ord("X")
+    bad.write_bytes(bytes(b))
+    with pytest.raises(P.PyritError) as ei:
+        P.decode_file([str(bad)], tmp_path / "out.bin")
+    assert ei.value.code == "BadHeader"
+    with pytest.raises(P.PyritError) as ei:
+        P.decode_file(shards[:3], tmp_path / "out.bin")  # k - 1 distinct shards
+    assert ei.value.code == "InsufficientShards"
