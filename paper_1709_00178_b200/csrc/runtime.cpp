@@ -367,6 +367,8 @@ LaunchInfo launch_batch(const Program& p, const std::uint8_t* const* in, std::ui
         // 3D map per input: (column element, strip, stripe); box = one tile of
         // all w strips of one stripe; elements of 4 bytes (8 for 2 KiB tiles)
         const std::uint32_t elem = ks.tile > 1024 ? 8 : 4;
+        static const int promo_knob = env_int("PYRIT_B200_TMA_PROMO", 3); // tuning: 0 none .. 3 = 256B
+        const CUtensorMapL2promotion promo = static_cast<CUtensorMapL2promotion>(std::min(3, std::max(0, promo_knob)));
         for (std::uint32_t j = 0; j < p.cols; ++j) {
             CUtensorMap m;
             const cuuint64_t dims[3] = {strip / elem, p.field.w, nb};
@@ -375,8 +377,8 @@ LaunchInfo launch_batch(const Program& p, const std::uint8_t* const* in, std::ui
             const cuuint32_t es[3] = {1, 1, 1};
             check_cu(driver().tensorMapEncodeTiled(&m, elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32,
                                                    3, const_cast<std::uint8_t*>(in[j]), dims, strides, box, es,
-                                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+                                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
                      "cuTensorMapEncodeTiled");
             std::memcpy(&args[tm_off + 16 * std::size_t(j)], &m, sizeof m);
         }
