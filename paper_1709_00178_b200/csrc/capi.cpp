@@ -291,6 +291,7 @@ int pyrit_plan_source(const pyrit_plan* plan, uint32_t lanes, char* buf, size_t 
             if (!ks.staged) raise(Errc::BufferShape, "program tiles do not fit in shared memory");
             ks.chunk = lanes == PYRIT_SOURCE_STAGED ? 16 : lanes - PYRIT_SOURCE_STAGED;
             if (ks.chunk != 16) ks.copy = 1; // TMA needs 16-byte alignment
+            if (const char* env = std::getenv("PYRIT_B200_WS")) ks.ws = std::atoi(env) ? 1u : 0u;
             if (const char* env = std::getenv("PYRIT_B200_COPY")) { // same producer the runtime would pick
                 const int c = std::atoi(env);
                 ks.copy = c == 2 ? 2u : c ? 1u : 0u;

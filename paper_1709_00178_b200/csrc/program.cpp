@@ -25,7 +25,7 @@ namespace {
 
 constexpr std::uint32_t kNone = 0xFFFFFFFFu;
 // bump whenever generated code changes for the same program (prebuilt cubins are keyed by name)
-constexpr int kGeneratorVersion = 13;
+constexpr int kGeneratorVersion = 14;
 
 // Greedy pair elimination over XOR targets.  Each target is a set of
 // variable ids; the most frequent pair (ties: smallest ids) becomes a new
@@ -469,7 +469,7 @@ std::string kernel_name(const Program& p, const KernelShape& ks) {
        << ',' << p.rows << ',' << p.cols << ',' << p.group << ',' << ks.lanes << ',' << ks.threads << ',' << ks.min_blocks << ','
        << ks.staged << ',' << ks.tile << ',' << ks.stages << ',' << ks.bar_bytes << ',' << p.parts.size() << ','
        << (p.parts.empty() ? 0u : p.parts[0].group) << ',' << ks.copy << ',' << p.cse << ',' << p.crs << ','
-       << ks.chunk << ',' << ks.split << ',' << ks.half << ',';
+       << ks.chunk << ',' << ks.split << ',' << ks.half << ',' << ks.ws << ',';
     if (p.crs)
         for (std::uint16_t x : p.matrix) fp << 'c' << x;
     for (const Program& q : p.parts) fp << q.rows << '/' << q.cse << '/' << q.stats.xors << ',';
@@ -602,12 +602,14 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
     o << "#define TILE " << TILE << "u\n#define NSLOT " << NSLOT << "u\n#define SLOT_BYTES " << slot_bytes
       << "u\n#define NG " << groups << "u\n#define BAR_BYTES " << ks.bar_bytes << "u\n";
     o << "#define FULL(s) (sbase + 8u * (s))\n#define EMPTY(s) (sbase + 8u * (NSLOT + (s)))\n";
-    o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", 1) " << name
+    const bool ws = ks.copy == 2 && ks.ws; // a dedicated producer warp after the T consumer threads
+    o << "extern \"C\" __global__ void __launch_bounds__(" << T + (ws ? 32u : 0u) << ", 1) " << name
       << "(const __grid_constant__ Args a)\n{\n";
     o << "  extern __shared__ __align__(1024) u8 sm[];\n";
     o << "  const u32 sbase = smem_u32(sm);\n";
     o << "  const u32 tpb = (u32)((a.len + TILE - 1) / TILE);\n"; // tiles per stripe
     o << "  const u32 ntiles = tpb * (u32)a.nb;\n";
+    o << "  auto my_units_tiles = [&]() -> u32 { return blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u; };\n";
     o << "  if (threadIdx.x == 0) {\n";
     o << "    for (u32 s = 0; s < NSLOT; ++s) { mbar_init(FULL(s), " << (ks.copy == 1 ? T : 1u) << "u); mbar_init(EMPTY(s), "
       << T << "u); }\n";
@@ -721,8 +723,16 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
         o << "    }\n";
     }
     o << "  };\n";
-    const std::string who = ks.copy == 1 ? "" : ks.copy == 2 ? "if (threadIdx.x == 0) " : "if (warp == 0) ";
-    o << "  " << who << "for (u32 u = 0; u + 1 < NSLOT; ++u) produce(u);\n";
+    if (ws) {
+        // warp specialisation: the extra warp only feeds the ring (its lane 0
+        // runs ahead until every slot is in flight); consumers never copy
+        o << "  if (threadIdx.x >= " << T << "u) {\n";
+        o << "    if (lane == 0) for (u32 u = 0; u / NG < my_units_tiles(); ++u) produce(u);\n";
+        o << "    return;\n  }\n";
+    } else {
+        const std::string who = ks.copy == 1 ? "" : ks.copy == 2 ? "if (threadIdx.x == 0) " : "if (warp == 0) ";
+        o << "  " << who << "for (u32 u = 0; u + 1 < NSLOT; ++u) produce(u);\n";
+    }
     o << "  const u32 part = threadIdx.x / " << cols_per_part << "u, col = threadIdx.x % " << cols_per_part << "u;\n";
     o << "  const u64 S = a.S;\n";
     // one tile loop per output part: each is its own register-allocation region
@@ -765,7 +775,8 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
             const std::string gs = std::to_string(g);
             o << "    const u32 un" << gs << " = it * NG + " << g << "u;\n";
             if (ks.copy == 1) o << "    produce(un" << gs << " + NSLOT - 1u);\n";
-            else if (ks.copy == 2 && r == 0) o << "    if (threadIdx.x == 0) produce(un" << gs << " + NSLOT - 1u);\n";
+            else if (ks.copy == 2 && !ws && r == 0) o << "    if (threadIdx.x == 0) produce(un" << gs << " + NSLOT - 1u);\n";
+            else if (ks.copy == 2) {}
             else if (r == 0) o << "    if (warp == 0) produce(un" << gs << " + NSLOT - 1u);\n";
             o << "    const u32 sl" << gs << " = un" << gs << " % NSLOT;\n";
             o << "    mbar_wait(FULL(sl" << gs << "), (un" << gs << " / NSLOT) & 1u);\n";

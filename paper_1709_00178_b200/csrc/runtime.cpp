@@ -244,6 +244,7 @@ KernelShape staged_for(const Program& p) {
     KernelShape ks = staged_shape(p, 227 * 1024);
     const int copy = env_int("PYRIT_B200_COPY", static_cast<int>(ks.copy));
     ks.copy = copy == 2 ? 2u : copy ? 1u : 0u;
+    ks.ws = env_int("PYRIT_B200_WS", static_cast<int>(ks.ws)) ? 1u : 0u;
     return ks;
 }
 
@@ -399,7 +400,7 @@ LaunchInfo launch_batch(const Program& p, const std::uint8_t* const* in, std::ui
     CUlaunchConfig cfg{};
     cfg.gridDimX = blocks;
     cfg.gridDimY = cfg.gridDimZ = 1;
-    cfg.blockDimX = ks.threads;
+    cfg.blockDimX = ks.threads + (ks.staged && ks.copy == 2 && ks.ws ? 32u : 0u);
     cfg.blockDimY = cfg.blockDimZ = 1;
     cfg.sharedMemBytes = ks.staged ? ks.smem_bytes : 0;
     cfg.hStream = reinterpret_cast<CUstream>(stream);
