@@ -163,10 +163,12 @@ const TunedEntry* find_tuned(const std::string& key) {
                 while (std::fgets(line, sizeof line, fh)) {
                     if (line[0] == '#' || line[0] == '\n') continue;
                     char k[128];
-                    unsigned parts = 0, pg = 0, threads = 0;
+                    unsigned parts = 0, pg = 0, threads = 0, producer = 0;
                     int cse = -1;
-                    const int got = std::sscanf(line, "%127s %u %u %d %u", k, &parts, &pg, &cse, &threads);
-                    if (got >= 4) g_tuned.push_back(TunedEntry{k, parts, pg, cse, got == 5 ? threads : 0u});
+                    const int got =
+                        std::sscanf(line, "%127s %u %u %d %u %u", k, &parts, &pg, &cse, &threads, &producer);
+                    if (got >= 4)
+                        g_tuned.push_back(TunedEntry{k, parts, pg, cse, got >= 5 ? threads : 0u, got >= 6 ? producer : 0u});
                 }
                 std::fclose(fh);
             }
@@ -381,6 +383,7 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
         if (!p.staged_threads && env_u("PYRIT_B200_THREADS") > 0)
             p.staged_threads = static_cast<std::uint32_t>(env_u("PYRIT_B200_THREADS"));
         if (!p.staged_threads && tuned) p.staged_threads = tuned->threads;
+        if (tuned) p.staged_producer = tuned->producer;
         std::uint32_t R = opt.parts;
         if (!R && env_u("PYRIT_B200_PARTS") > 0) R = static_cast<std::uint32_t>(env_u("PYRIT_B200_PARTS"));
         if (!R && tuned) R = tuned->parts;
@@ -524,16 +527,20 @@ KernelShape staged_shape(const Program& p, std::uint32_t smem_limit) {
         ks.bar_bytes = bar;
         ks.threads = threads;
         ks.smem_bytes = static_cast<std::uint32_t>(bar + slots * slot);
-        // producer (profiles/r01_s2/sizes_*copy*, tune_*_v13_tma): TMA tensor
-        // boxes pay off when a box (all w strips of a fragment tile) is large
-        // and the XOR work per input word is high (the BASELINE codes: 8-24 KB
-        // boxes, 8-14 XORs per input word); light codes (GF(2^4)) and small
-        // boxes (512 B tiles of the split (60,40) code) stream faster with
-        // every thread issuing cp.async
+        // producer (profiles/r01_s2/sizes_*copy*, tune_*_v13_tma, trace_ws):
+        // TMA tensor boxes when a box (all w strips of a fragment tile) is
+        // large (>= 6 KB); heavy codes (>= 8 XORs per input word, the BASELINE
+        // codes) issue them from a consumer thread, light codes (GF(2^4))
+        // from a dedicated producer warp; small boxes (512 B tiles of the
+        // split (60,40) code) stream faster with every thread issuing cp.async
         std::uint64_t xors = 0;
         for (const Program& q : p.parts) xors += q.stats.xors;
         const bool heavy = xors >= 8ull * k * w;
-        ks.copy = (heavy && std::uint64_t(w) * tile >= 6144) ? 2u : 1u;
+        const bool big_box = std::uint64_t(w) * tile >= 6144;
+        std::uint32_t prod = p.staged_producer;
+        if (!prod) prod = big_box ? (heavy ? 2u : 3u) : 1u;
+        ks.copy = prod == 1 ? 1u : 2u;
+        ks.ws = prod == 3 ? 1u : 0u;
         return ks;
     }
     ks.staged = false;

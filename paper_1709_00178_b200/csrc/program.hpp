@@ -60,6 +60,7 @@ struct Program {
     std::vector<Program> parts;
     std::vector<std::uint32_t> part_row0;
     std::uint32_t staged_threads = 0; // staged CTA size override (0 = 256)
+    std::uint32_t staged_producer = 0; // 0 auto, 1 cp.async, 2 TMA tensor, 3 TMA tensor + producer warp
     ProgramStats stats;
 };
 
@@ -82,6 +83,7 @@ struct TunedEntry {
     std::uint32_t parts = 1, part_group = 1;
     int part_cse = 0;
     std::uint32_t threads = 0; // staged CTA size (0 = default)
+    std::uint32_t producer = 0; // 0 auto, 1 cp.async, 2 TMA tensor, 3 TMA tensor + producer warp
 };
 std::string plan_key(const Program& p); // field + transform + ring representatives
 void set_tuned_path(const std::string& path);

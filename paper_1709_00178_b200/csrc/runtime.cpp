@@ -282,6 +282,7 @@ KernelShape choose_shape(const Program& p, const std::uint8_t* const* in, std::u
         KernelShape ks = staged_for(p);
         ks.chunk = chunk;
         if (ks.copy != 1 && chunk != 16) ks.copy = 1; // TMA needs 16-byte alignment: cp.async chunks
+        if (ks.copy != 2) ks.ws = 0;
         // auto mode keeps the staged kernel where it measured faster than the
         // direct one (profiles/r01_s2/sizes_*): 16-byte chunks, at most two
         // output parts, and per-stripe windows that fill at least half a tile
