@@ -347,8 +347,8 @@ def main(argv=None):
                        "l2": "inputs larger than L2" if nsets == 1 else f"{nsets} rotating buffer sets > L2",
                        "launch": "CUDA graph of the K steps" if graph is not None else "per-step launches",
                        "kernel": launch["kernel"], "grid": [launch["blocks"], launch["threads"]],
-                       "xors_per_column_word": st["part_xors"] if ("_cpa" in launch["kernel"] or
-                                                                   "_tma" in launch["kernel"]) else st["xors"],
+                       "xors_per_column_word": st["part_xors"] if ("_cpa" in launch["kernel"] or "_tm" in
+                                                                   launch["kernel"]) else st["xors"],
                        "reference_region_ops": st["ref_region_ops"]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,

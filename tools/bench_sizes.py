@@ -159,8 +159,8 @@ def main():
                        "size": size, "stripes": nb, "gpu_ms": ms, "gpu_src_GBps": src / ms / 1e6,
                        "gpu_ref_GBps": (k + r) * size * nb / ms / 1e6,
                        "gpu_moved_GBps": (k + n_out) * size * nb / ms / 1e6, "kernel": info["kernel"],
-                       "xors_per_word": plan.stats()["part_xors" if ("_cpa" in info["kernel"] or
-                                                                     "_tma" in info["kernel"]) else "xors"]}
+                       "xors_per_word": plan.stats()["part_xors" if ("_cpa" in info["kernel"] or "_tm" in
+                                                                     info["kernel"]) else "xors"]}
                 if a.cpu:
                     dt = cpu_point(f, k, r, a.transform, size, op, codec, threads)
                     if dt:
