@@ -123,9 +123,10 @@ int pyrit_plan_reps(const pyrit_plan* plan, uint32_t* reps /* rows x cols */);
 int pyrit_plan_key(const pyrit_plan* plan, char* buf, size_t cap);
 /* generated CUDA source of the fused kernel; *len receives the full size.
  * lanes: 1/2/4 = direct LDG kernel with that many 32-bit words per thread per
- * strip, 0 = byte mode, PYRIT_SOURCE_STAGED = the staged kernel (16-byte
- * cp.async chunks; PYRIT_SOURCE_STAGED + 8 / + 4 = 8- / 4-byte chunks for
- * strips with only that alignment) */
+ * strip, 0 = byte mode, PYRIT_SOURCE_STAGED = the staged kernel (its
+ * producer as chosen for the plan; PYRIT_SOURCE_STAGED + 1 = the variant for
+ * equally spaced inputs -- one 4D TMA map; + 8 / + 4 = cp.async with 8- / 4-byte
+ * chunks for strips with only that alignment) */
 #define PYRIT_SOURCE_STAGED 100u
 int pyrit_plan_source(const pyrit_plan* plan, uint32_t lanes, char* buf, size_t cap, size_t* len,
                       char* name, size_t name_cap);

@@ -87,7 +87,7 @@ def baseline_programs():
     ]
 
 
-def prebuild_kernels(lanes=(100, 1), force=False) -> list[str]:
+def prebuild_kernels(lanes=(100, 101, 1), force=False) -> list[str]:
     """Generate + nvcc-compile the BASELINE plans' kernels into kernels/*.cubin."""
     sys.path.insert(0, ROOT)
     from paper_1709_00178_b200 import _lib as L  # noqa: E402
@@ -110,7 +110,7 @@ def prebuild_kernels(lanes=(100, 1), force=False) -> list[str]:
                 size = C.c_size_t(0)
                 name = C.create_string_buffer(128)
                 rc = lib.pyrit_plan_source(plan, ln, None, 0, C.byref(size), name, 128)
-                if rc == 4 and ln == L.SOURCE_STAGED:
+                if rc == 4 and ln in (L.SOURCE_STAGED, L.SOURCE_STAGED + 1):
                     continue  # tiles do not fit in shared memory: direct kernel only
                 L.check(rc)
                 buf = C.create_string_buffer(size.value + 1)
@@ -147,7 +147,8 @@ def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--no-prebuild", action="store_true")
-    ap.add_argument("--lanes", default="100,1", help="100 = TMA-staged kernel, 1/2/4 = direct")
+    ap.add_argument("--lanes", default="100,101,1",
+                    help="100 = staged kernel, 101 = staged for equally spaced inputs, 1/2/4 = direct")
     a = ap.parse_args(argv)
     build_library(a.force)
     build_test_tools(a.force)

@@ -282,15 +282,16 @@ int pyrit_plan_source(const pyrit_plan* plan, uint32_t lanes, char* buf, size_t 
                       size_t name_cap) {
     return guarded([&] {
         if (!plan) raise(Errc::InvalidArgument, "null plan");
-        const bool staged = lanes == PYRIT_SOURCE_STAGED || lanes == PYRIT_SOURCE_STAGED + 4 ||
-                            lanes == PYRIT_SOURCE_STAGED + 8;
+        const bool staged = lanes == PYRIT_SOURCE_STAGED || lanes == PYRIT_SOURCE_STAGED + 1 ||
+                            lanes == PYRIT_SOURCE_STAGED + 4 || lanes == PYRIT_SOURCE_STAGED + 8;
         if (lanes != 0 && lanes != 1 && lanes != 2 && lanes != 4 && !staged) raise(Errc::InvalidArgument, "bad lanes");
         KernelShape ks = direct_shape(plan->prog, staged ? 1 : lanes);
         if (staged) {
             ks = staged_shape(plan->prog, 227 * 1024);
             if (!ks.staged) raise(Errc::BufferShape, "program tiles do not fit in shared memory");
-            ks.chunk = lanes == PYRIT_SOURCE_STAGED ? 16 : lanes - PYRIT_SOURCE_STAGED;
+            ks.chunk = lanes <= PYRIT_SOURCE_STAGED + 1 ? 16 : lanes - PYRIT_SOURCE_STAGED;
             if (ks.chunk != 16) ks.copy = 1; // TMA needs 16-byte alignment
+            ks.tmap4 = lanes == PYRIT_SOURCE_STAGED + 1 && ks.copy == 2 ? 1u : 0u;
             if (const char* env = std::getenv("PYRIT_B200_WS")) ks.ws = std::atoi(env) ? 1u : 0u;
             if (const char* env = std::getenv("PYRIT_B200_COPY")) { // same producer the runtime would pick
                 const int c = std::atoi(env);

@@ -25,7 +25,7 @@ namespace {
 
 constexpr std::uint32_t kNone = 0xFFFFFFFFu;
 // bump whenever generated code changes for the same program (prebuilt cubins are keyed by name)
-constexpr int kGeneratorVersion = 14;
+constexpr int kGeneratorVersion = 15;
 
 // Greedy pair elimination over XOR targets.  Each target is a set of
 // variable ids; the most frequent pair (ties: smallest ids) becomes a new
@@ -472,7 +472,7 @@ std::string kernel_name(const Program& p, const KernelShape& ks) {
        << ',' << p.rows << ',' << p.cols << ',' << p.group << ',' << ks.lanes << ',' << ks.threads << ',' << ks.min_blocks << ','
        << ks.staged << ',' << ks.tile << ',' << ks.stages << ',' << ks.bar_bytes << ',' << p.parts.size() << ','
        << (p.parts.empty() ? 0u : p.parts[0].group) << ',' << ks.copy << ',' << p.cse << ',' << p.crs << ','
-       << ks.chunk << ',' << ks.split << ',' << ks.half << ',' << ks.ws << ',';
+       << ks.chunk << ',' << ks.split << ',' << ks.half << ',' << ks.ws << ',' << ks.tmap4 << ',';
     if (p.crs)
         for (std::uint16_t x : p.matrix) fp << 'c' << x;
     for (const Program& q : p.parts) fp << q.rows << '/' << q.cse << '/' << q.stats.xors << ',';
@@ -575,7 +575,8 @@ std::string generate_staged(const Program& p, const KernelShape& ks) {
     if (ks.copy == 2) // one 3D tensor map per input fragment: (column element, strip, stripe)
         o << "struct alignas(64) TMap { u64 v[16]; };\n";
     o << "struct Args { const u8* in[" << k << "]; u8* out[" << p.rows
-      << "]; u64 S; u64 off; u64 len; u64 nb; u64 ibp; u64 obp;" << (ks.copy == 2 ? " TMap tm[" + std::to_string(k) + "];" : "")
+      << "]; u64 S; u64 off; u64 len; u64 nb; u64 ibp; u64 obp;"
+      << (ks.copy == 2 ? " TMap tm[" + std::to_string(ks.tmap4 ? 1u : k) + "];" : "")
       << " };\n";
     o << R"(static __device__ __forceinline__ u32 smem_u32(const void* p) {
   u32 r; asm("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(r) : "l"(p)); return r; }
@@ -591,6 +592,9 @@ static __device__ __forceinline__ void mbar_wait(u32 bar, u32 parity) {
 static __device__ __forceinline__ void bulk_g2s(u32 dst, const void* src, u32 bytes, u32 bar, u64 pol) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
                :: "r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory"); }
+static __device__ __forceinline__ void tma4d(u32 dst, const void* map, u32 x, u32 y, u32 z, u32 q, u32 bar) {
+  asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+               :: "r"(dst), "l"(map), "r"(x), "r"(y), "r"(z), "r"(q), "r"(bar) : "memory"); }
 static __device__ __forceinline__ void tma3d(u32 dst, const void* map, u32 x, u32 y, u32 z, u32 bar) {
   asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
                :: "r"(dst), "l"(map), "r"(x), "r"(y), "r"(z), "r"(bar) : "memory"); }
@@ -645,9 +649,18 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
         o << "    const u32 dst = sbase + BAR_BYTES + sl * SLOT_BYTES;\n";
         o << "    const u32 j0 = g2 * " << G << "u;\n";
         o << "    const u32 nfr = g2 + 1u == NG ? " << k << "u - j0 : " << G << "u;\n";
-        o << "    mbar_expect_tx(FULL(sl), nfr * " << w * TILE << "u);\n";
-        o << "#pragma unroll 1\n";
-        o << "    for (u32 f = 0; f < nfr; ++f) tma3d(dst + f * " << w * TILE << "u, &a.tm[j0 + f], x, 0u, b2, FULL(sl));\n";
+        if (ks.tmap4) {
+            // equally spaced inputs: one 4D box (tile x w strips x G fragments)
+            // per unit; fragments past k are out of bounds and zero-filled, so
+            // the transaction is always the full box
+            o << "    (void)nfr;\n";
+            o << "    mbar_expect_tx(FULL(sl), " << G * w * TILE << "u);\n";
+            o << "    tma4d(dst, &a.tm[0], x, 0u, j0, b2, FULL(sl));\n";
+        } else {
+            o << "    mbar_expect_tx(FULL(sl), nfr * " << w * TILE << "u);\n";
+            o << "#pragma unroll 1\n";
+            o << "    for (u32 f = 0; f < nfr; ++f) tma3d(dst + f * " << w * TILE << "u, &a.tm[j0 + f], x, 0u, b2, FULL(sl));\n";
+        }
     } else if (ks.copy) {
         // every thread copies CH-byte chunks (16, or 8/4 when the strips are
         // only that aligned; a strip tile is TILE/CH consecutive chunks:

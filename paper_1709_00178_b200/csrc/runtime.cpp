@@ -283,6 +283,15 @@ KernelShape choose_shape(const Program& p, const std::uint8_t* const* in, std::u
         ks.chunk = chunk;
         if (ks.copy != 1 && chunk != 16) ks.copy = 1; // TMA needs 16-byte alignment: cp.async chunks
         if (ks.copy != 2) ks.ws = 0;
+        // inputs at a constant 16-byte-multiple spacing (rows of one buffer, the
+        // file layout): one 4D tensor map, one box per unit
+        if (ks.copy == 2 && p.cols > 1 && env_int("PYRIT_B200_TMAP4", 1)) {
+            const std::int64_t d = reinterpret_cast<std::intptr_t>(in[1]) - reinterpret_cast<std::intptr_t>(in[0]);
+            bool uni = d > 0 && d % 16 == 0;
+            for (std::uint32_t j = 2; uni && j < p.cols; ++j)
+                uni = reinterpret_cast<std::intptr_t>(in[j]) - reinterpret_cast<std::intptr_t>(in[j - 1]) == d;
+            ks.tmap4 = uni ? 1u : 0u;
+        }
         // auto mode keeps the staged kernel where it measured faster than the
         // direct one (profiles/r01_s2/sizes_*): 16-byte chunks, at most two
         // output parts, and per-stripe windows that fill at least half a tile
@@ -343,7 +352,8 @@ LaunchInfo launch_batch(const Program& p, const std::uint8_t* const* in, std::ui
     const std::size_t head = std::size_t(p.cols) + p.rows + 8;
     const std::size_t tm_off = (8 * (std::size_t(p.cols) + p.rows + 6) + 63) / 64 * 8; // in u64 words
     const bool tensor = ks.staged && ks.copy == 2;
-    std::vector<std::uint64_t> args(tensor ? tm_off + 16 * std::size_t(p.cols) : head, 0);
+    const std::size_t nmaps = tensor ? (ks.tmap4 ? 1 : p.cols) : 0;
+    std::vector<std::uint64_t> args(tensor ? tm_off + 16 * nmaps : head, 0);
     for (std::uint32_t j = 0; j < p.cols; ++j) args[j] = reinterpret_cast<std::uint64_t>(in[j]);
     for (std::uint32_t i = 0; i < p.rows; ++i) args[p.cols + i] = reinterpret_cast<std::uint64_t>(out[i]);
     std::uint64_t* tail = &args[p.cols + p.rows];
@@ -371,7 +381,23 @@ LaunchInfo launch_batch(const Program& p, const std::uint8_t* const* in, std::ui
         const std::uint32_t elem = ks.tile > 1024 ? 8 : 4;
         static const int promo_knob = env_int("PYRIT_B200_TMA_PROMO", 3); // tuning: 0 none .. 3 = 256B
         const CUtensorMapL2promotion promo = static_cast<CUtensorMapL2promotion>(std::min(3, std::max(0, promo_knob)));
-        for (std::uint32_t j = 0; j < p.cols; ++j) {
+        if (ks.tmap4) {
+            // 4D: (column element, strip, fragment, stripe)
+            CUtensorMap m;
+            const std::uint64_t d = reinterpret_cast<std::uintptr_t>(in[1]) - reinterpret_cast<std::uintptr_t>(in[0]);
+            const std::uint32_t G = p.parts.empty() ? 1 : p.parts[0].group;
+            const cuuint64_t dims[4] = {strip / elem, p.field.w, p.cols, nb};
+            const cuuint64_t strides[3] = {strip, d, nb > 1 ? in_pitch : d * p.cols};
+            const cuuint32_t box[4] = {ks.tile / elem, p.field.w, G, 1};
+            const cuuint32_t es[4] = {1, 1, 1, 1};
+            check_cu(driver().tensorMapEncodeTiled(&m, elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32,
+                                                   4, const_cast<std::uint8_t*>(in[0]), dims, strides, box, es,
+                                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+                     "cuTensorMapEncodeTiled(4D)");
+            std::memcpy(&args[tm_off], &m, sizeof m);
+        }
+        for (std::uint32_t j = 0; !ks.tmap4 && j < p.cols; ++j) {
             CUtensorMap m;
             const cuuint64_t dims[3] = {strip / elem, p.field.w, nb};
             const cuuint64_t strides[2] = {strip, nb > 1 ? in_pitch : strip * p.field.w};
