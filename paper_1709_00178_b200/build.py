@@ -87,7 +87,7 @@ def baseline_programs():
     ]
 
 
-def prebuild_kernels(lanes=(100, 101, 1), force=False) -> list[str]:
+def prebuild_kernels(lanes=(100, 1), force=False) -> list[str]:
     """Generate + nvcc-compile the BASELINE plans' kernels into kernels/*.cubin."""
     sys.path.insert(0, ROOT)
     from paper_1709_00178_b200 import _lib as L  # noqa: E402
@@ -147,7 +147,7 @@ def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--no-prebuild", action="store_true")
-    ap.add_argument("--lanes", default="100,101,1",
+    ap.add_argument("--lanes", default="100,1",
                     help="100 = staged kernel, 101 = staged for equally spaced inputs, 1/2/4 = direct")
     a = ap.parse_args(argv)
     build_library(a.force)

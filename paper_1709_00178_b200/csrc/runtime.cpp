@@ -283,9 +283,10 @@ KernelShape choose_shape(const Program& p, const std::uint8_t* const* in, std::u
         ks.chunk = chunk;
         if (ks.copy != 1 && chunk != 16) ks.copy = 1; // TMA needs 16-byte alignment: cp.async chunks
         if (ks.copy != 2) ks.ws = 0;
-        // inputs at a constant 16-byte-multiple spacing (rows of one buffer, the
-        // file layout): one 4D tensor map, one box per unit
-        if (ks.copy == 2 && p.cols > 1 && env_int("PYRIT_B200_TMAP4", 1)) {
+        // PYRIT_B200_TMAP4=1: inputs at a constant 16-byte-multiple spacing get one
+        // 4D tensor map and one box per unit -- measured slower than a box per
+        // fragment (cfg2 0.894 vs 0.956, cfg3 0.926 vs 1.032), so off by default
+        if (ks.copy == 2 && p.cols > 1 && env_int("PYRIT_B200_TMAP4", 0)) {
             const std::int64_t d = reinterpret_cast<std::intptr_t>(in[1]) - reinterpret_cast<std::intptr_t>(in[0]);
             bool uni = d > 0 && d % 16 == 0;
             for (std::uint32_t j = 2; uni && j < p.cols; ++j)
