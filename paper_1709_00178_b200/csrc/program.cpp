@@ -472,7 +472,7 @@ std::string kernel_name(const Program& p, const KernelShape& ks) {
        << ',' << p.rows << ',' << p.cols << ',' << p.group << ',' << ks.lanes << ',' << ks.threads << ',' << ks.min_blocks << ','
        << ks.staged << ',' << ks.tile << ',' << ks.stages << ',' << ks.bar_bytes << ',' << p.parts.size() << ','
        << (p.parts.empty() ? 0u : p.parts[0].group) << ',' << ks.copy << ',' << p.cse << ',' << p.crs << ','
-       << ks.chunk << ',' << ks.split << ',' << ks.half << ',' << ks.ws << ',' << ks.tmap4 << ',';
+       << ks.chunk << ',' << ks.split << ',' << ks.half << ',' << ks.ws << ',' << ks.tmap4 << ',' << ks.spb << ',';
     if (p.crs)
         for (std::uint16_t x : p.matrix) fp << 'c' << x;
     for (const Program& q : p.parts) fp << q.rows << '/' << q.cse << '/' << q.stats.xors << ',';
@@ -657,9 +657,14 @@ static __device__ __forceinline__ void st_cs(u8* p, u32 v) {
             o << "    mbar_expect_tx(FULL(sl), " << G * w * TILE << "u);\n";
             o << "    tma4d(dst, &a.tm[0], x, 0u, j0, b2, FULL(sl));\n";
         } else {
+            // boxes of ks.spb strips (a divisor of w): several requests per fragment
+            const std::uint32_t spb = ks.spb && w % ks.spb == 0 ? ks.spb : w;
             o << "    mbar_expect_tx(FULL(sl), nfr * " << w * TILE << "u);\n";
             o << "#pragma unroll 1\n";
-            o << "    for (u32 f = 0; f < nfr; ++f) tma3d(dst + f * " << w * TILE << "u, &a.tm[j0 + f], x, 0u, b2, FULL(sl));\n";
+            o << "    for (u32 f = 0; f < nfr; ++f)\n";
+            o << "#pragma unroll\n";
+            o << "      for (u32 s0 = 0; s0 < " << w << "u; s0 += " << spb << "u)\n";
+            o << "        tma3d(dst + f * " << w * TILE << "u + s0 * TILE, &a.tm[j0 + f], x, s0, b2, FULL(sl));\n";
         }
     } else if (ks.copy) {
         // every thread copies CH-byte chunks (16, or 8/4 when the strips are

@@ -126,6 +126,7 @@ struct KernelShape {
     std::uint32_t half = 0;         // direct sub-word mode: 1 = 2-byte elements (u16), 0 = bytes
     std::uint32_t ws = 0;           // staged TMA: 1 = a dedicated producer warp (blockDim = threads + 32)
     std::uint32_t tmap4 = 0;        // staged TMA: 1 = inputs equally spaced, one 4D map / one box per unit
+    std::uint32_t spb = 0;          // staged TMA: strips per box (0 = all w strips of a fragment in one box)
 };
 std::string kernel_name(const Program& p, const KernelShape& ks);
 std::string generate_cuda(const Program& p, const KernelShape& ks);

@@ -245,6 +245,8 @@ KernelShape staged_for(const Program& p) {
     const int copy = env_int("PYRIT_B200_COPY", static_cast<int>(ks.copy));
     ks.copy = copy == 2 ? 2u : copy ? 1u : 0u;
     ks.ws = env_int("PYRIT_B200_WS", static_cast<int>(ks.ws)) ? 1u : 0u;
+    ks.spb = static_cast<std::uint32_t>(env_int("PYRIT_B200_TMA_SPB", static_cast<int>(ks.spb)));
+    if (ks.spb && p.field.w % ks.spb) ks.spb = 0;
     return ks;
 }
 
@@ -402,7 +404,7 @@ LaunchInfo launch_batch(const Program& p, const std::uint8_t* const* in, std::ui
             CUtensorMap m;
             const cuuint64_t dims[3] = {strip / elem, p.field.w, nb};
             const cuuint64_t strides[2] = {strip, nb > 1 ? in_pitch : strip * p.field.w};
-            const cuuint32_t box[3] = {ks.tile / elem, p.field.w, 1};
+            const cuuint32_t box[3] = {ks.tile / elem, ks.spb ? ks.spb : p.field.w, 1};
             const cuuint32_t es[3] = {1, 1, 1};
             check_cu(driver().tensorMapEncodeTiled(&m, elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32,
                                                    3, const_cast<std::uint8_t*>(in[j]), dims, strides, box, es,
