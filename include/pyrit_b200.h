@@ -136,6 +136,30 @@ int pyrit_plan_interpret(const pyrit_plan* plan, const uint8_t* const* in, uint8
                          uint64_t strip_bytes, uint64_t off, uint64_t len);
 void pyrit_plan_destroy(pyrit_plan* plan);
 
+/* ---- plans from a reference schedule (the replay operator) ------------ */
+/* One region op of an XorSchedule, laid out like the reference's XorOp
+ * (schedule.hpp:42-48; mode = OpMode: 0 Copy, 1 Xor, 2 Zero), so a
+ * std::vector<XorOp> can be passed as is. */
+typedef struct pyrit_xor_op {
+    uint16_t src_sym, src_pkt, dst_sym, dst_pkt;
+    uint8_t mode;
+} pyrit_xor_op;
+/* Compiles any XorSchedule -- compile_schedule / compile_crs_schedule output
+ * or hand-written -- into one fused GPU kernel with replay()'s semantics
+ * (codec.hpp:118-157): ops = pre, core, post concatenated in replay order;
+ * sym < k is input slot sym (in_map), sym >= k output slot sym - k
+ * (out_map); packets >= w are workspace scratch, zero at entry (the fresh
+ * Workspace parallel_replay makes, codec.hpp:176-193).  labels (k + outputs
+ * entries, or NULL = all distinct): slots with equal labels share storage
+ * (decode() replays with one SymbolBuffer as in and out), so a write
+ * through one slot is seen by later reads through another.  Output packets
+ * no op writes are left untouched.  Errors as replay: BufferShape for a
+ * slot/packet out of range or a write to an input data packet.
+ * The plan is applied with pyrit_cu_apply / _batch / pyrit_apply_host with
+ * in[k] and out[outputs] indexed by slot. */
+int pyrit_plan_from_schedule(const pyrit_field* f, uint32_t k, uint32_t outputs, const pyrit_xor_op* ops,
+                             size_t n_ops, const uint32_t* labels, pyrit_plan** out);
+
 /* ---- device path ------------------------------------------------------ */
 /* replay (codec.hpp:118): window [off, off+len) of every strip; in[j] /
  * out[i] are device base pointers of the input / output symbols */
@@ -170,6 +194,11 @@ int pyrit_cu_decode_batch(const pyrit_code* code, uint8_t* const* symbols, const
                           uint32_t n_erased, uint64_t symbol_size, uint64_t stripes, uint64_t pitch, void* stream);
 
 /* ---- host-buffer path (end to end: H2D, fused kernel, D2H, pipelined) -- */
+/* parallel_replay / replay (codec.hpp:118-193) on HOST symbols: in[j] /
+ * out[i] are host base pointers (w strips of strip_bytes each), window
+ * [off, off+len) of every strip.  Synchronous. */
+int pyrit_apply_host(const pyrit_plan* plan, const uint8_t* const* in, uint8_t* const* out, uint64_t strip_bytes,
+                     uint64_t off, uint64_t len, int device);
 /* data: k * symbol_size contiguous host bytes (SymbolBuffer layout);
  * parity: r * symbol_size host bytes.  Synchronous. Pinned buffers overlap. */
 int pyrit_encode_host(const pyrit_code* code, const uint8_t* data, uint8_t* parity, uint64_t symbol_size,

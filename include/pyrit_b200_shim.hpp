@@ -9,6 +9,10 @@
 //     -> pyrit::cuda::encode_file(input, out_dir, code, symbol_size, device)
 //   pyrit::decode_file(shard_paths, output)      container.hpp:249-299
 //     -> pyrit::cuda::decode_file(shard_paths, output, device)
+//   pyrit::parallel_replay(sched, in, in_map, out, out_map, threads)  codec.hpp:176-193
+//     -> pyrit::cuda::parallel_replay(sched, in, in_map, out, out_map, device)
+//   pyrit::replay(sched, in, in_map, out, out_map, ws, offset, len)   codec.hpp:118-157
+//     -> pyrit::cuda::replay(sched, in, in_map, out, out_map, offset, len, device)
 //
 // Include after the reference headers (it needs SymbolBuffer, CodeSpec,
 // Error from proj/include/pyrit/) and link libpyrit_b200.so.  Validation and
@@ -20,7 +24,10 @@
 // field oracle oracle_apply / encode_crs).
 #pragma once
 
+#include <algorithm>
+#include <cstddef>
 #include <filesystem>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -106,6 +113,60 @@ inline void decode_file(const std::vector<std::filesystem::path>& shard_paths, c
     std::vector<const char*> ps;
     for (const auto& p : shard_paths) ps.push_back(p.c_str());
     check(pyrit_decode_file(ps.data(), static_cast<std::uint32_t>(ps.size()), output.c_str(), device));
+}
+
+// The operator level: any XorSchedule (compile_schedule, compile_crs_schedule
+// or hand-built) compiled into one fused kernel and replayed over host
+// SymbolBuffers (H2D, kernel, D2H inside).  The reference's XorOp is passed
+// as is (same layout as pyrit_xor_op).  Scratch packets start zeroed, as the
+// fresh Workspace of parallel_replay; slots that name the same symbol of
+// the same buffer share storage, as in the reference's op-by-op replay.
+static_assert(sizeof(XorOp) == sizeof(pyrit_xor_op) && offsetof(XorOp, mode) == offsetof(pyrit_xor_op, mode),
+              "XorOp layout");
+
+inline void replay(const XorSchedule& sched, const SymbolBuffer& in, std::span<const unsigned> in_map,
+                   SymbolBuffer& out, std::span<const unsigned> out_map, std::size_t offset, std::size_t len,
+                   int device = 0) {
+    // codec.hpp:122-127, the reference's own checks
+    if (in_map.size() != sched.k || out_map.size() != sched.outputs)
+        raise(Errc::BufferShape, "replay: slot map sizes do not match schedule");
+    if (!(in.spec() == sched.spec) || !(out.spec() == sched.spec)) raise(Errc::BufferShape, "replay: field mismatch");
+    if (in.packet_size() != out.packet_size() || offset + len > in.packet_size())
+        raise(Errc::BufferShape, "replay: column window out of range");
+    for (unsigned j : in_map)
+        if (j >= in.symbols()) raise(Errc::BufferShape, "replay: input slot maps outside the buffer");
+    for (unsigned i : out_map)
+        if (i >= out.symbols()) raise(Errc::BufferShape, "replay: output slot maps outside the buffer");
+    std::vector<XorOp> ops(sched.pre);
+    ops.insert(ops.end(), sched.core.begin(), sched.core.end());
+    ops.insert(ops.end(), sched.post.begin(), sched.post.end());
+    std::vector<const std::uint8_t*> ip;
+    std::vector<std::uint8_t*> op;
+    for (unsigned j : in_map) ip.push_back(in.symbol(j));
+    for (unsigned i : out_map) op.push_back(out.symbol(i));
+    std::vector<std::uint32_t> labels; // slots naming the same symbol share storage
+    std::vector<const std::uint8_t*> addr(ip.begin(), ip.end());
+    addr.insert(addr.end(), op.begin(), op.end());
+    for (const std::uint8_t* a : addr)
+        labels.push_back(static_cast<std::uint32_t>(std::find(addr.begin(), addr.end(), a) - addr.begin()));
+    pyrit_field f{};
+    f.w = sched.spec.w;
+    f.n = sched.spec.n;
+    f.kind = sched.spec.kind == FieldKind::Esp ? 1u : 0u;
+    f.s = sched.spec.s;
+    f.r_esp = sched.spec.r_esp;
+    f.modulus = sched.spec.modulus;
+    pyrit_plan* plan = nullptr;
+    check(pyrit_plan_from_schedule(&f, sched.k, sched.outputs, reinterpret_cast<const pyrit_xor_op*>(ops.data()),
+                                   ops.size(), labels.data(), &plan));
+    const int rc = pyrit_apply_host(plan, ip.data(), op.data(), in.packet_size(), offset, len, device);
+    pyrit_plan_destroy(plan);
+    check(rc);
+}
+
+inline void parallel_replay(const XorSchedule& sched, const SymbolBuffer& in, std::span<const unsigned> in_map,
+                            SymbolBuffer& out, std::span<const unsigned> out_map, int device = 0) {
+    replay(sched, in, in_map, out, out_map, 0, in.packet_size(), device);
 }
 
 } // namespace pyrit::cuda

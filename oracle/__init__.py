@@ -254,6 +254,49 @@ def digest_np(buf: np.ndarray, word_offset=0) -> int:
         return int(mix64_np(words ^ (q * _DG)).sum(dtype=np.uint64))
 
 
+# XorOp (schedule.hpp:42-48): 4 x uint16 + uint8 mode, 10 bytes
+OP_DTYPE = np.dtype([("src_sym", "<u2"), ("src_pkt", "<u2"), ("dst_sym", "<u2"), ("dst_pkt", "<u2"),
+                     ("mode", "u1")], align=True)
+assert OP_DTYPE.itemsize == 10
+
+
+def _ops_call(fn, *args) -> np.ndarray:
+    n = C.c_uint64(0)
+    rc = fn(*args, None, C.c_uint64(0), C.byref(n))
+    if rc:
+        raise OracleError(rc)
+    ops = np.zeros(n.value, dtype=OP_DTYPE)
+    rc = fn(*args, C.c_void_p(ops.ctypes.data), C.c_uint64(n.value), C.byref(n))
+    if rc:
+        raise OracleError(rc)
+    return ops
+
+
+def compile_schedule(f: Field, m, kind=0, rep=0) -> np.ndarray:
+    """schedule.hpp:94-163 restated: the op list (pre, core, post) as an OP_DTYPE array."""
+    m = np.ascontiguousarray(m, dtype=np.uint16)
+    return _ops_call(lib().or_compile_schedule, f.w, f.n, f.s, f.modulus, kind, m.shape[0], m.shape[1],
+                     m.ctypes.data_as(u16p), rep)
+
+
+def compile_crs_schedule(f: Field, m) -> np.ndarray:
+    """schedule.hpp:168-203 restated."""
+    m = np.ascontiguousarray(m, dtype=np.uint16)
+    return _ops_call(lib().or_compile_crs_schedule, f.w, f.modulus, m.shape[0], m.shape[1], m.ctypes.data_as(u16p))
+
+
+def replay_ops(f: Field, k, outputs, ops, ins, outs, strip, off=0, length=None):
+    """codec.hpp:118-157 restated op by op: ins[j] / outs[i] are the slot symbols (maps applied;
+    the same array object twice = shared storage).  outs are updated in place."""
+    length = strip - off if length is None else length
+    ops = np.ascontiguousarray(ops, dtype=OP_DTYPE)
+    rc = lib().or_replay_ops(f.w, f.n, k, outputs, C.c_void_p(ops.ctypes.data), C.c_uint64(len(ops)), _ptrs(ins),
+                             _ptrs(outs), C.c_uint64(strip), C.c_uint64(off), C.c_uint64(length))
+    if rc:
+        raise OracleError(rc)
+    return outs
+
+
 # ----------------------------------------------------------- the reference
 def ref_cauchy(k, r, f: Field) -> np.ndarray:
     out = np.zeros(max(r, 1) * k, dtype=np.uint16)
@@ -301,6 +344,30 @@ def ref_decode(f: Field, k, r, symbols: np.ndarray, symbol_size, erased, transfo
     er = np.asarray(list(erased), dtype=np.uint32)
     rc = ref().ref_decode(*_fa(f), k, r, transform, symbols.ctypes.data_as(u8p), C.c_uint64(symbol_size),
                           er.ctypes.data_as(u32p), len(er), threads)
+    if rc:
+        raise OracleError(rc)
+
+
+def ref_schedule_ops(f: Field, m, transform=0, crs=0, rep=0) -> np.ndarray:
+    """The reference's own compile_schedule / compile_crs_schedule op list (pre, core, post)."""
+    m = np.ascontiguousarray(m, dtype=np.uint16)
+    return _ops_call(ref().ref_schedule_ops, *_fa(f), m.shape[0], m.shape[1], m.ctypes.data_as(u16p), transform,
+                     crs, rep)
+
+
+def ref_replay_ops(f: Field, k, outputs, ops, inp: np.ndarray | None, in_map, out: np.ndarray, out_map,
+                   symbol_size, threads=1) -> None:
+    """The reference's parallel_replay (codec.hpp:176) of an op list; inp None = in and out are one
+    SymbolBuffer (out).  out is updated in place."""
+    ops = np.ascontiguousarray(ops, dtype=OP_DTYPE)
+    im = np.asarray(in_map, dtype=np.uint32)
+    om = np.asarray(out_map, dtype=np.uint32)
+    same = inp is None
+    src = out if same else inp
+    rc = ref().ref_replay_ops(*_fa(f), k, outputs, C.c_void_p(ops.ctypes.data), C.c_uint64(len(ops)),
+                              src.ctypes.data_as(u8p), src.size // symbol_size, im.ctypes.data_as(u32p),
+                              out.ctypes.data_as(u8p), out.size // symbol_size, om.ctypes.data_as(u32p),
+                              C.c_uint64(symbol_size), int(same), threads)
     if rc:
         raise OracleError(rc)
 

@@ -135,6 +135,60 @@ REF_EXPORT int ref_schedule_stats(unsigned w, unsigned n, unsigned kind, unsigne
     });
 }
 
+// schedule.hpp:94 compile_schedule / :168 compile_crs_schedule: the op list
+// itself (pre, core, post concatenated, XorOp layout); *n_ops = total, ops
+// may be null (count only).  Returns BufferShape + 1 when cap is too small.
+REF_EXPORT int ref_schedule_ops(unsigned w, unsigned n, unsigned kind, unsigned s, unsigned r_esp,
+                                std::uint32_t modulus, unsigned rows, unsigned cols, const std::uint16_t* m,
+                                unsigned transform, unsigned crs, unsigned rep, XorOp* ops, std::uint64_t cap,
+                                std::uint64_t* n_ops) {
+    return guarded([&] {
+        const FieldMatrix fm = make_matrix(make_field(w, n, kind, s, r_esp, modulus), rows, cols, m);
+        const XorSchedule sched =
+            crs ? compile_crs_schedule(fm)
+                : compile_schedule(fm, static_cast<TransformKind>(transform),
+                                   rep ? RingRep::Dense : RingRep::Sparse);
+        std::vector<XorOp> all(sched.pre);
+        all.insert(all.end(), sched.core.begin(), sched.core.end());
+        all.insert(all.end(), sched.post.begin(), sched.post.end());
+        *n_ops = all.size();
+        if (ops) {
+            if (all.size() > cap) raise(Errc::BufferShape, "op buffer too small");
+            std::memcpy(ops, all.data(), all.size() * sizeof(XorOp));
+        }
+    });
+}
+
+// codec.hpp:176 parallel_replay of an arbitrary op list (all in core).
+// in: n_in symbols, out: n_out symbols (symbol_size bytes each, contiguous);
+// same_buffer: in and out are ONE SymbolBuffer (decode()'s in-place replay),
+// held in `out` (n_out symbols).
+REF_EXPORT int ref_replay_ops(unsigned w, unsigned n, unsigned kind, unsigned s, unsigned r_esp,
+                              std::uint32_t modulus, unsigned k, unsigned outputs, const XorOp* ops,
+                              std::uint64_t n_ops, const std::uint8_t* in, unsigned n_in, const unsigned* in_map,
+                              std::uint8_t* out, unsigned n_out, const unsigned* out_map,
+                              std::uint64_t symbol_size, unsigned same_buffer, unsigned threads) {
+    return guarded([&] {
+        const FieldSpec spec = make_field(w, n, kind, s, r_esp, modulus);
+        XorSchedule sched;
+        sched.spec = spec;
+        sched.k = k;
+        sched.outputs = outputs;
+        sched.core.assign(ops, ops + n_ops);
+        SymbolBuffer ob(n_out, symbol_size, spec);
+        std::memcpy(ob.symbol(0), out, std::size_t(n_out) * symbol_size);
+        const std::vector<unsigned> im(in_map, in_map + k), om(out_map, out_map + outputs);
+        if (same_buffer) {
+            parallel_replay(sched, ob, im, ob, om, threads);
+        } else {
+            SymbolBuffer ib(n_in, symbol_size, spec);
+            std::memcpy(ib.symbol(0), in, std::size_t(n_in) * symbol_size);
+            parallel_replay(sched, ib, im, ob, om, threads);
+        }
+        std::memcpy(out, ob.symbol(0), std::size_t(n_out) * symbol_size);
+    });
+}
+
 // codec.hpp:444 oracle_apply over whole symbols (data: cols symbols contiguous)
 REF_EXPORT int ref_oracle_apply(unsigned w, unsigned n, unsigned kind, unsigned s, unsigned r_esp,
                                 std::uint32_t modulus, unsigned transform, unsigned rows,

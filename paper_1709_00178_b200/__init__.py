@@ -24,7 +24,8 @@ __all__ = [
     "sparse_transform", "fold_table", "cauchy_parity_matrix", "decode_matrix", "repair_matrix", "encode",
     "decode", "encode_host", "decode_host", "fill", "digest", "choose_transform", "encode_batch", "decode_batch",
     "ShardHeader", "crc32", "serialize_header", "parse_header", "field_id", "field_from_id", "shard_path",
-    "encode_file", "decode_file", "HEADER_SIZE", "encode_crs",
+    "encode_file", "decode_file", "HEADER_SIZE", "encode_crs", "XorSchedule", "OP_DTYPE", "replay",
+    "parallel_replay",
 ]
 
 
@@ -147,6 +148,25 @@ def repair_matrix(code: CodeSpec, erased: Iterable[int]):
     return surv, outs[: er.size], m[: er.size * code.k].reshape(er.size, code.k)
 
 
+# XorOp (schedule.hpp:42-48): src_sym, src_pkt, dst_sym, dst_pkt (uint16), mode (OpMode, uint8:
+# 0 Copy, 1 Xor, 2 Zero) -- 10 bytes, the reference's own layout
+OP_DTYPE = np.dtype([("src_sym", "<u2"), ("src_pkt", "<u2"), ("dst_sym", "<u2"), ("dst_pkt", "<u2"),
+                     ("mode", "u1")], align=True)
+
+
+@dataclass
+class XorSchedule:
+    """schedule.hpp:50-58: k input slots, `outputs` output slots, and the region ops of the pre, core
+    and post phases concatenated in replay order (an OP_DTYPE array)."""
+    spec: FieldSpec
+    k: int
+    outputs: int
+    ops: np.ndarray
+
+    def __post_init__(self):
+        self.ops = np.ascontiguousarray(self.ops, dtype=OP_DTYPE)
+
+
 def _ptr_array(ptrs):
     return (C.c_void_p * max(len(ptrs), 1))(*ptrs)
 
@@ -166,6 +186,17 @@ class Plan:
         h = C.c_void_p()
         L.check(_clib().pyrit_plan_create(C.byref(f.c()), int(transform), m.ctypes.data, m.shape[0], m.shape[1],
                                          int(rep), group, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_schedule(cls, sched: XorSchedule, labels: Sequence[int] | None = None) -> "Plan":
+        """Any XorSchedule as one fused kernel with replay()'s semantics (codec.hpp:118-157); labels:
+        k + outputs storage labels, equal labels = slots sharing storage (None = all distinct)."""
+        lab = None if labels is None else np.ascontiguousarray(labels, dtype=np.uint32)
+        h = C.c_void_p()
+        L.check(_clib().pyrit_plan_from_schedule(C.byref(sched.spec.c()), sched.k, sched.outputs,
+                                                sched.ops.ctypes.data, len(sched.ops),
+                                                None if lab is None else lab.ctypes.data, C.byref(h)))
         return cls(h)
 
     @classmethod
@@ -227,6 +258,13 @@ class Plan:
         L.check(_clib().pyrit_cu_apply(self._h, _ptr_array(list(in_ptrs)), _ptr_array(list(out_ptrs)), strip, off,
                                       length, stream))
 
+    def apply_host(self, ins: Sequence[np.ndarray], outs: Sequence[np.ndarray], strip: int, off: int = 0,
+                   length: int | None = None, device: int = 0) -> None:
+        """replay over HOST symbols (numpy uint8, w strips each): H2D, kernel, D2H inside; synchronous."""
+        length = strip - off if length is None else length
+        L.check(_clib().pyrit_apply_host(self._h, _ptr_array([a.ctypes.data for a in ins]),
+                                        _ptr_array([a.ctypes.data for a in outs]), strip, off, length, device))
+
     @staticmethod
     def last_launch() -> dict:
         """Kernel name / grid of this thread's most recent launch through the C ABI."""
@@ -265,6 +303,55 @@ def _stream_of(t):
 
 def _rows(t) -> list[int]:
     return [t[i].data_ptr() for i in range(t.shape[0])]
+
+
+def _replay_checks(sched: XorSchedule, inp, in_map, out, out_map, offset, length):
+    # codec.hpp:122-127
+    if len(in_map) != sched.k or len(out_map) != sched.outputs:
+        raise PyritError(4, "replay: slot map sizes do not match schedule")
+    if inp.shape[1] != out.shape[1] or inp.shape[1] % sched.spec.w:
+        raise PyritError(4, "replay: field mismatch")
+    strip = inp.shape[1] // sched.spec.w
+    length = strip - offset if length is None else length
+    if offset + length > strip:
+        raise PyritError(4, "replay: column window out of range")
+    for j in in_map:
+        if not 0 <= j < inp.shape[0]:
+            raise PyritError(4, "replay: input slot maps outside the buffer")
+    for i in out_map:
+        if not 0 <= i < out.shape[0]:
+            raise PyritError(4, "replay: output slot maps outside the buffer")
+    return strip, length
+
+
+def replay(sched: XorSchedule, inp, in_map: Sequence[int], out, out_map: Sequence[int], offset: int = 0,
+           length: int | None = None, device: int = 0) -> None:
+    """replay (codec.hpp:118-157) of any schedule over the column window [offset, offset+length) of every
+    packet, on the GPU: `inp` / `out` are (symbols, symbol_size) uint8 CUDA tensors (asynchronous on the
+    current stream) or numpy arrays (host path, synchronous); they may be the same buffer (decode() style).
+    Workspace scratch starts zeroed, as in parallel_replay."""
+    strip, length = _replay_checks(sched, inp, in_map, out, out_map, offset, length)
+    if hasattr(inp, "data_ptr"):
+        ins = [inp[j].data_ptr() for j in in_map]
+        outs = [out[i].data_ptr() for i in out_map]
+    else:
+        ins = [inp[j].ctypes.data for j in in_map]
+        outs = [out[i].ctypes.data for i in out_map]
+    addr = ins + outs  # slots sharing a symbol share storage
+    labels = [addr.index(a) for a in addr]
+    plan = Plan.from_schedule(sched, labels)
+    if hasattr(inp, "data_ptr"):
+        L.check(_clib().pyrit_cu_apply(plan._h, _ptr_array(ins), _ptr_array(outs), strip, offset, length,
+                                      _stream_of(out)))
+    else:
+        L.check(_clib().pyrit_apply_host(plan._h, _ptr_array(ins), _ptr_array(outs), strip, offset, length, device))
+
+
+def parallel_replay(sched: XorSchedule, inp, in_map: Sequence[int], out, out_map: Sequence[int],
+                    device: int = 0) -> None:
+    """parallel_replay (codec.hpp:176-193): replay over the whole packet (the column windows of the
+    reference's threads are one grid here)."""
+    replay(sched, inp, in_map, out, out_map, 0, None, device)
 
 
 def encode(data, code: CodeSpec):

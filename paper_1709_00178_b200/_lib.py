@@ -56,7 +56,7 @@ EXPORTS = (
     "pyrit_cu_encode_batch", "pyrit_cu_decode_batch", "pyrit_crc32", "pyrit_header_serialize", "pyrit_header_parse",
     "pyrit_field_id", "pyrit_field_from_id", "pyrit_shard_path", "pyrit_encode_file", "pyrit_decode_file",
     "pyrit_set_file_chunk", "pyrit_cu_encode_crs", "pyrit_encode_crs_host", "pyrit_encode_host_devices",
-    "pyrit_decode_host_devices",
+    "pyrit_decode_host_devices", "pyrit_plan_from_schedule", "pyrit_apply_host",
 )
 
 HEADER_SIZE = 29
@@ -133,6 +133,8 @@ def load():
     lib.pyrit_encode_file.argtypes = [P(pyrit_code), C.c_char_p, C.c_char_p, u32, i32]
     lib.pyrit_decode_file.argtypes = [P(C.c_char_p), u32, C.c_char_p, i32]
     lib.pyrit_set_file_chunk.argtypes = [u64]
+    lib.pyrit_plan_from_schedule.argtypes = [P(pyrit_field), u32, u32, vp, C.c_size_t, vp, P(vp)]
+    lib.pyrit_apply_host.argtypes = [vp, vp, vp, u64, u64, u64, i32]
     _lib = lib
     return lib
 

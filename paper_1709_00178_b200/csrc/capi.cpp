@@ -22,7 +22,34 @@ using namespace pyrit_b200;
 
 struct pyrit_plan {
     Program prog;
+    // plans from a schedule (pyrit_plan_from_schedule): kernel input q reads
+    // slot src_slot[q] (>= 0 input slot, < 0 output slot -1-q's prior
+    // contents), kernel output r is output slot dst_slot[r]
+    bool sched = false;
+    std::uint32_t k = 0, outputs = 0;
+    std::vector<std::int32_t> src_slot;
+    std::vector<std::uint32_t> dst_slot;
 };
+
+namespace {
+
+// slot-indexed pointer arrays -> the kernel's input/output arrays
+void kernel_ptrs(const pyrit_plan* plan, const uint8_t* const* in, uint8_t* const* out,
+                 std::vector<const uint8_t*>& kin, std::vector<uint8_t*>& kout) {
+    kin.clear();
+    kout.clear();
+    for (std::int32_t s : plan->src_slot) {
+        const uint8_t* p = s >= 0 ? in[s] : out[-1 - s];
+        if (!p) raise(Errc::InvalidArgument, "null symbol pointer");
+        kin.push_back(p);
+    }
+    for (std::uint32_t i : plan->dst_slot) {
+        if (!out[i]) raise(Errc::InvalidArgument, "null symbol pointer");
+        kout.push_back(out[i]);
+    }
+}
+
+} // namespace
 
 namespace {
 
@@ -219,6 +246,27 @@ int pyrit_plan_create(const pyrit_field* f, uint32_t transform, const uint16_t* 
     });
 }
 
+int pyrit_plan_from_schedule(const pyrit_field* f, uint32_t k, uint32_t outputs, const pyrit_xor_op* ops,
+                             size_t n_ops, const uint32_t* labels, pyrit_plan** out) {
+    return guarded([&] {
+        if (!out || (!ops && n_ops)) raise(Errc::InvalidArgument, "null argument");
+        std::vector<ScheduleOp> v(n_ops);
+        for (size_t i = 0; i < n_ops; ++i)
+            v[i] = ScheduleOp{ops[i].src_sym, ops[i].src_pkt, ops[i].dst_sym, ops[i].dst_pkt, ops[i].mode};
+        std::vector<uint32_t> lab;
+        if (labels) lab.assign(labels, labels + std::size_t(k) + outputs);
+        ScheduleProgram sp = compile_schedule_program(to_field(f), k, outputs, v, lab, CompileOptions{});
+        auto plan = std::make_unique<pyrit_plan>();
+        plan->prog = std::move(sp.prog);
+        plan->sched = true;
+        plan->k = k;
+        plan->outputs = outputs;
+        plan->src_slot = std::move(sp.src_slot);
+        plan->dst_slot = std::move(sp.dst_slot);
+        *out = plan.release();
+    });
+}
+
 int pyrit_plan_encode(const pyrit_code* code, pyrit_plan** out) {
     return guarded([&] {
         check_code(code);
@@ -319,6 +367,22 @@ int pyrit_plan_interpret(const pyrit_plan* plan, const uint8_t* const* in, uint8
     return guarded([&] {
         if (!plan || !in || !out) raise(Errc::InvalidArgument, "null argument");
         if (off + len > strip_bytes) raise(Errc::BufferShape, "column window out of range");
+        if (plan->sched) {
+            if (plan->dst_slot.empty()) return;
+            std::vector<const uint8_t*> kin;
+            std::vector<uint8_t*> kout;
+            kernel_ptrs(plan, in, out, kin, kout);
+            // prior contents of output slots the schedule reads: snapshot the
+            // window first (the interpreter stores as it goes)
+            std::vector<std::vector<uint8_t>> snap;
+            for (std::size_t q = 0; q < kin.size(); ++q)
+                if (plan->src_slot[q] < 0) {
+                    snap.emplace_back(kin[q], kin[q] + std::size_t(plan->prog.field.w) * strip_bytes);
+                    kin[q] = snap.back().data();
+                }
+            interpret_program(plan->prog, kin.data(), kout.data(), strip_bytes, off, len);
+            return;
+        }
         interpret_program(plan->prog, in, out, strip_bytes, off, len);
     });
 }
@@ -329,6 +393,14 @@ int pyrit_cu_apply(const pyrit_plan* plan, const uint8_t* const* in, uint8_t* co
                    uint64_t off, uint64_t len, void* stream) {
     return guarded([&] {
         if (!plan || !in || !out) raise(Errc::InvalidArgument, "null argument");
+        if (plan->sched) {
+            if (plan->dst_slot.empty()) return; // the schedule writes nothing
+            std::vector<const uint8_t*> kin;
+            std::vector<uint8_t*> kout;
+            kernel_ptrs(plan, in, out, kin, kout);
+            launch_program(plan->prog, kin.data(), kout.data(), strip_bytes, off, len, static_cast<cudaStream_t>(stream));
+            return;
+        }
         launch_program(plan->prog, in, out, strip_bytes, off, len, static_cast<cudaStream_t>(stream));
     });
 }
@@ -388,6 +460,18 @@ int pyrit_cu_apply_batch(const pyrit_plan* plan, const uint8_t* const* in, uint8
                          uint64_t out_pitch, void* stream) {
     return guarded([&] {
         if (!plan || !in || !out) raise(Errc::InvalidArgument, "null argument");
+        if (plan->sched) {
+            if (plan->dst_slot.empty()) return;
+            for (std::int32_t s : plan->src_slot)
+                if (s < 0 && in_pitch != out_pitch)
+                    raise(Errc::InvalidArgument, "schedule reads an output slot: in_pitch must equal out_pitch");
+            std::vector<const uint8_t*> kin;
+            std::vector<uint8_t*> kout;
+            kernel_ptrs(plan, in, out, kin, kout);
+            launch_batch(plan->prog, kin.data(), kout.data(), strip_bytes, off, len, stripes, in_pitch, out_pitch,
+                         static_cast<cudaStream_t>(stream));
+            return;
+        }
         launch_batch(plan->prog, in, out, strip_bytes, off, len, stripes, in_pitch, out_pitch,
                      static_cast<cudaStream_t>(stream));
     });
@@ -437,6 +521,28 @@ int pyrit_encode_host(const pyrit_code* code, const uint8_t* data, uint8_t* pari
         for (uint32_t j = 0; j < code->k; ++j) in.push_back(data + std::uint64_t(j) * symbol_size);
         for (uint32_t i = 0; i < code->r; ++i) out.push_back(parity + std::uint64_t(i) * symbol_size);
         run_host(*p, in, out, strip, device);
+    });
+}
+
+int pyrit_apply_host(const pyrit_plan* plan, const uint8_t* const* in, uint8_t* const* out, uint64_t strip_bytes,
+                     uint64_t off, uint64_t len, int device) {
+    return guarded([&] {
+        if (!plan || !in || !out) raise(Errc::InvalidArgument, "null argument");
+        if (off + len > strip_bytes) raise(Errc::BufferShape, "column window out of range");
+        std::vector<const uint8_t*> kin;
+        std::vector<uint8_t*> kout;
+        if (plan->sched) {
+            if (plan->dst_slot.empty()) return;
+            kernel_ptrs(plan, in, out, kin, kout);
+        } else {
+            kin.assign(in, in + plan->prog.cols);
+            kout.assign(out, out + plan->prog.rows);
+            for (const uint8_t* p : kin)
+                if (!p) raise(Errc::InvalidArgument, "null symbol pointer");
+            for (uint8_t* p : kout)
+                if (!p) raise(Errc::InvalidArgument, "null symbol pointer");
+        }
+        run_host_window(plan->prog, kin, kout, strip_bytes, off, len, device);
     });
 }
 

@@ -126,7 +126,22 @@ void run_host_window(const Program& p, const std::vector<const std::uint8_t*>& h
         return out;
     };
     const auto in_runs = runs(host_in);
-    const auto out_runs = runs(host_out);
+    // outputs a schedule program writes only partly (Program::written): only
+    // their written strips come back, the others stay as they are on the host
+    std::vector<std::pair<std::uint32_t, std::uint32_t>> out_runs; // [first, end) of fully written outputs
+    std::vector<std::pair<std::uint32_t, std::uint32_t>> partial;  // (output, strip)
+    for (std::uint32_t i = 0; i < p.rows; ++i) {
+        bool all = true;
+        for (std::uint32_t b = 0; p.sched && b < w; ++b) all = all && p.written[std::size_t(i) * w + b];
+        if (!all) {
+            for (std::uint32_t b = 0; b < w; ++b)
+                if (p.written[std::size_t(i) * w + b]) partial.push_back({i, b});
+        } else if (!out_runs.empty() && out_runs.back().second == i &&
+                   host_out[i] == host_out[i - 1] + std::uint64_t(w) * strip)
+            ++out_runs.back().second;
+        else
+            out_runs.push_back({i, i + 1});
+    }
     std::vector<const std::uint8_t*> din(p.cols);
     std::vector<std::uint8_t*> dout(p.rows);
     std::uint64_t c0 = off;
@@ -143,6 +158,10 @@ void run_host_window(const Program& p, const std::vector<const std::uint8_t*>& h
         for (const auto& [i0, i1] : out_runs)
             check_cuda(cudaMemcpy2DAsync(host_out[i0] + c0, strip, dout[i0], chunk, len, std::size_t(i1 - i0) * w,
                                          cudaMemcpyDeviceToHost, s.stream),
+                       "D2H");
+        for (const auto& [i, b] : partial)
+            check_cuda(cudaMemcpyAsync(host_out[i] + std::uint64_t(b) * strip + c0, dout[i] + std::uint64_t(b) * chunk,
+                                       len, cudaMemcpyDeviceToHost, s.stream),
                        "D2H");
         c0 += len;
     }

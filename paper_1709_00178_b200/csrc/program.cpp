@@ -119,10 +119,14 @@ std::string plan_key(const Program& p) {
     fp << p.field.w << ',' << p.field.n << ',' << p.field.modulus << ',' << int(p.kind) << ',' << p.rows << ','
        << p.cols << ':';
     for (std::uint32_t r : p.reps) fp << r << ',';
-    if (p.crs) // bitmatrix programs depend on the matrix itself, not on representatives
+    if (p.sched) { // schedule programs: the linear map itself
+        for (std::uint32_t b : p.bits) fp << 'b' << b;
+        for (std::uint8_t x : p.written) fp << int(x);
+    } else if (p.crs) // bitmatrix programs depend on the matrix itself, not on representatives
         for (std::uint16_t x : p.matrix) fp << 'c' << x;
     char key[64];
-    std::snprintf(key, sizeof key, "w%un%u_%ux%u%s_%016llx", p.field.w, p.field.n, p.rows, p.cols, p.crs ? "crs" : "",
+    std::snprintf(key, sizeof key, "w%un%u_%ux%u%s_%016llx", p.field.w, p.field.n, p.rows, p.cols,
+                  p.sched ? "sch" : p.crs ? "crs" : "",
                   static_cast<unsigned long long>(fnv1a(fp.str())));
     return key;
 }
@@ -191,7 +195,8 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
     p.group = opt.group ? opt.group : std::max<std::uint32_t>(1, 24 / w);
     p.group = std::min(p.group, k);
     p.cse = opt.cse;
-    p.crs = opt.crs;
+    p.crs = opt.crs || opt.bits;
+    p.sched = opt.bits != nullptr;
     p.matrix = m.e;
     p.fold = fold_table(f);
     p.reps.resize(std::size_t(e) * k);
@@ -203,7 +208,15 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
     // CRS: the w x w bitmatrix of every entry (field_to_bitmatrix, field.hpp:198-207):
     // column c = coefficients of entry * x^c; rows[b] = mask of input strips feeding output strip b
     std::vector<std::uint32_t> bits;
-    if (opt.crs) {
+    if (opt.bits) { // explicit linear map (compile_schedule_program)
+        if (opt.bits->size() != std::size_t(e) * k * w || !opt.written || opt.written->size() != std::size_t(e) * w)
+            raise(Errc::InvalidArgument, "bit matrix shape");
+        bits = *opt.bits;
+        p.bits = bits;
+        p.written = *opt.written;
+        p.stats.matrix_ones = 0;
+        for (std::uint32_t b : bits) p.stats.matrix_ones += std::popcount(b);
+    } else if (opt.crs) {
         if (kind != TransformKind::Embedding) raise(Errc::InvalidArgument, "CRS programs are plain field codes");
         bits.assign(std::size_t(e) * k * w, 0);
         p.stats.matrix_ones = 0;
@@ -219,13 +232,13 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
     }
 
     const bool emb = kind == TransformKind::Embedding;
-    const bool crs = opt.crs;
+    const bool crs = p.crs;
     const std::uint32_t out_rows = emb && !crs ? n : w; // schedule.hpp:132 (CRS: w bit rows)
 
     // reference op count (compile_schedule), generalized post phase
     {
         std::uint64_t ops = 0;
-        if (crs) // compile_crs_schedule (schedule.hpp:186-201): one op per bitmatrix one, Zero for empty rows
+        if (crs && !p.sched) // compile_crs_schedule (schedule.hpp:186-201): one op per bitmatrix one, Zero for empty rows
             for (std::uint32_t i = 0; i < e; ++i)
                 for (std::uint32_t b = 0; b < w; ++b) {
                     std::uint64_t row = 0;
@@ -350,7 +363,8 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
         std::vector<Instr> fold;
         if (opt.cse) share_pairs(targets, nvars, fold);
         const std::size_t ntemps = fold.size();
-        for (std::uint32_t b = 0; b < w; ++b) fold.push_back(Instr{Instr::Store, 0, i, b, targets[b]});
+        for (std::uint32_t b = 0; b < w; ++b)
+            if (!p.sched || p.written[std::size_t(i) * w + b]) fold.push_back(Instr{Instr::Store, 0, i, b, targets[b]});
         lazy_order(fold, ntemps);
         p.code.insert(p.code.end(), fold.begin(), fold.end());
         p.tail.insert(p.tail.end(), fold.begin(), fold.end());
@@ -423,6 +437,16 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
                 for (std::uint32_t i = 0; i < nrows; ++i)
                     for (std::uint32_t j = 0; j < k; ++j) sub.at(i, j) = m.at(row0 + i, j);
                 CompileOptions o2 = opt;
+                std::vector<std::uint32_t> sub_bits;
+                std::vector<std::uint8_t> sub_written;
+                if (opt.bits) {
+                    sub_bits.assign(opt.bits->begin() + std::size_t(row0) * k * w,
+                                    opt.bits->begin() + std::size_t(row0 + nrows) * k * w);
+                    sub_written.assign(opt.written->begin() + std::size_t(row0) * w,
+                                       opt.written->begin() + std::size_t(row0 + nrows) * w);
+                    o2.bits = &sub_bits;
+                    o2.written = &sub_written;
+                }
                 o2.parts = 1;
                 o2.group = pg;
                 o2.cse = cse && opt.cse;
@@ -436,6 +460,121 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
         build_parts(pcse != 0);
     }
     return p;
+}
+
+ScheduleProgram compile_schedule_program(const Field& f, std::uint32_t k, std::uint32_t outputs,
+                                         const std::vector<ScheduleOp>& ops, const std::vector<std::uint32_t>& labels,
+                                         const CompileOptions& opt) {
+    validate_field(f);
+    const std::uint32_t w = f.w, n = f.n, slots = k + outputs;
+    if (k == 0) raise(Errc::InvalidArgument, "schedule has no input slots");
+    if (!labels.empty() && labels.size() != slots) raise(Errc::InvalidArgument, "one storage label per slot");
+    // storage of every slot: distinct labels -> dense ids
+    std::vector<std::uint32_t> store(slots);
+    {
+        std::vector<std::uint32_t> seen;
+        for (std::uint32_t s = 0; s < slots; ++s) {
+            const std::uint32_t lab = labels.empty() ? s : labels[s];
+            auto it = std::find(seen.begin(), seen.end(), lab);
+            store[s] = static_cast<std::uint32_t>(it - seen.begin());
+            if (it == seen.end()) seen.push_back(lab);
+        }
+    }
+    const std::uint32_t nstore = *std::max_element(store.begin(), store.end()) + 1;
+    // GF(2) symbolic replay (codec.hpp:129-156): the value of every packet is
+    // a set of initial packets (storage, strip), one bit each
+    const std::size_t nv = std::size_t(nstore) * w, words = (nv + 63) / 64;
+    using Vec = std::vector<std::uint64_t>;
+    std::vector<Vec> phys(nv, Vec(words, 0)), scratch(std::size_t(slots) * (n - w), Vec(words, 0));
+    for (std::size_t v = 0; v < nv; ++v) phys[v][v / 64] |= 1ull << (v % 64);
+    std::vector<std::uint8_t> wrote(nv, 0);
+    const Vec zero(words, 0);
+    for (const ScheduleOp& op : ops) {
+        if (op.mode > 2) raise(Errc::InvalidArgument, "schedule op mode");
+        if (op.dst_sym >= slots || op.dst_pkt >= n || (op.mode != 2 && (op.src_sym >= slots || op.src_pkt >= n)))
+            raise(Errc::BufferShape, "replay: schedule slot out of range");
+        Vec* dst;
+        if (op.dst_pkt >= w) dst = &scratch[std::size_t(op.dst_sym) * (n - w) + op.dst_pkt - w];
+        else if (op.dst_sym < k) raise(Errc::BufferShape, "replay: schedule writes an input data packet"); // codec.hpp:139-143
+        else {
+            const std::size_t v = std::size_t(store[op.dst_sym]) * w + op.dst_pkt;
+            dst = &phys[v];
+            wrote[v] = 1;
+        }
+        if (op.mode == 2) {
+            *dst = zero;
+            continue;
+        }
+        const Vec& src = op.src_pkt >= w ? scratch[std::size_t(op.src_sym) * (n - w) + op.src_pkt - w]
+                                         : phys[std::size_t(store[op.src_sym]) * w + op.src_pkt];
+        if (op.mode == 0) *dst = src;
+        else
+            for (std::size_t q = 0; q < words; ++q) (*dst)[q] ^= src[q];
+    }
+    // kernel outputs: storages written through an output slot (first slot names it)
+    ScheduleProgram sp;
+    sp.k = k;
+    sp.outputs = outputs;
+    std::vector<std::int32_t> out_of(nstore, -1), src_of(nstore, -1);
+    for (std::uint32_t i = 0; i < outputs; ++i) {
+        const std::uint32_t st = store[k + i];
+        if (out_of[st] >= 0) continue;
+        bool any = false;
+        for (std::uint32_t b = 0; b < w; ++b) any = any || wrote[std::size_t(st) * w + b];
+        if (!any) continue;
+        out_of[st] = static_cast<std::int32_t>(sp.dst_slot.size());
+        sp.dst_slot.push_back(i);
+    }
+    // kernel inputs: storages whose initial packets some stored packet reads
+    std::vector<std::uint8_t> used(nstore, 0);
+    for (std::uint32_t st = 0; st < nstore; ++st)
+        for (std::uint32_t b = 0; out_of[st] >= 0 && b < w; ++b)
+            if (wrote[std::size_t(st) * w + b])
+                for (std::size_t v = 0; v < nv; ++v)
+                    if ((phys[std::size_t(st) * w + b][v / 64] >> (v % 64)) & 1u) used[v / w] = 1;
+    for (std::uint32_t st = 0; st < nstore; ++st) {
+        if (!used[st]) continue;
+        std::int32_t slot = 0;
+        bool found = false;
+        for (std::uint32_t s = 0; s < slots && !found; ++s)
+            if (store[s] == st) {
+                slot = s < k ? static_cast<std::int32_t>(s) : -1 - static_cast<std::int32_t>(s - k);
+                found = true;
+            }
+        src_of[st] = static_cast<std::int32_t>(sp.src_slot.size());
+        sp.src_slot.push_back(slot);
+    }
+    if (sp.src_slot.empty()) sp.src_slot.push_back(0); // only zero stores: a placeholder input nothing reads
+    const std::uint32_t rows = static_cast<std::uint32_t>(sp.dst_slot.size());
+    const std::uint32_t cols = static_cast<std::uint32_t>(sp.src_slot.size());
+    std::vector<std::uint32_t> bits(std::size_t(rows) * cols * w, 0);
+    std::vector<std::uint8_t> written(std::size_t(rows) * w, 0);
+    for (std::uint32_t st = 0; st < nstore; ++st) {
+        if (out_of[st] < 0) continue;
+        const std::uint32_t r = static_cast<std::uint32_t>(out_of[st]);
+        for (std::uint32_t b = 0; b < w; ++b) {
+            const std::size_t v0 = std::size_t(st) * w + b;
+            if (!wrote[v0]) continue;
+            written[std::size_t(r) * w + b] = 1;
+            for (std::size_t v = 0; v < nv; ++v)
+                if ((phys[v0][v / 64] >> (v % 64)) & 1u)
+                    bits[(std::size_t(r) * cols + src_of[v / w]) * w + b] |= 1u << (v % w);
+        }
+    }
+    if (rows) {
+        CompileOptions o = opt;
+        o.bits = &bits;
+        o.written = &written;
+        o.crs = false;
+        o.dense = false;
+        sp.prog = compile_program(f, TransformKind::Embedding, Matrix(rows, cols), o);
+    } else {
+        sp.prog.field = f;
+        sp.prog.sched = true;
+        sp.prog.cols = cols;
+    }
+    sp.prog.stats.ref_region_ops = ops.size();
+    return sp;
 }
 
 void interpret_program(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
@@ -473,7 +612,10 @@ std::string kernel_name(const Program& p, const KernelShape& ks) {
        << ks.staged << ',' << ks.tile << ',' << ks.stages << ',' << ks.bar_bytes << ',' << p.parts.size() << ','
        << (p.parts.empty() ? 0u : p.parts[0].group) << ',' << ks.copy << ',' << p.cse << ',' << p.crs << ','
        << ks.chunk << ',' << ks.split << ',' << ks.half << ',' << ks.ws << ',' << ks.tmap4 << ',' << ks.spb << ',';
-    if (p.crs)
+    if (p.sched) {
+        for (std::uint32_t b : p.bits) fp << 'b' << b;
+        for (std::uint8_t x : p.written) fp << int(x);
+    } else if (p.crs)
         for (std::uint16_t x : p.matrix) fp << 'c' << x;
     for (const Program& q : p.parts) fp << q.rows << '/' << q.cse << '/' << q.stats.xors << ',';
     fp << ':';

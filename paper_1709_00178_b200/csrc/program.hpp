@@ -48,6 +48,10 @@ struct Program {
     std::uint32_t group = 1;          // input fragments whose strips are live together
     bool cse = true;                  // pair sharing applied
     bool crs = false;                 // plain-field bitmatrix program (compile_crs_schedule)
+    bool sched = false;               // compiled from an explicit XorSchedule (bits/written below)
+    std::vector<std::uint32_t> bits;  // sched: rows x cols x w masks, bit c of [(i*cols+j)*w+b] = strip c of input j
+                                      //        feeds strip b of output i
+    std::vector<std::uint8_t> written; // sched: rows x w, strip b of output i is stored (else left untouched)
     std::vector<std::uint32_t> reps;  // rows x cols ring representatives (n-bit masks)
     std::vector<std::uint16_t> matrix; // rows x cols GF(2^w) entries the program was compiled from
     std::vector<std::uint32_t> fold;  // fold[t - w] = x^t mod p
@@ -74,6 +78,10 @@ struct CompileOptions {
     std::uint32_t max_temps = 0;  // cap on shared pair temporaries per group (0 = no cap)
     std::uint32_t cse_window = 0; // pair sharing within windows of this many targets (0 = whole group)
     std::uint32_t staged_threads = 0; // staged CTA size (0 = tuned table / 256)
+    // explicit linear map instead of a matrix (compile_schedule_program): the
+    // matrix passed alongside only gives the shape
+    const std::vector<std::uint32_t>* bits = nullptr;
+    const std::vector<std::uint8_t>* written = nullptr;
 };
 
 // Measured staged-kernel choices for specific programs (tuned.tsv):
@@ -91,6 +99,38 @@ const TunedEntry* find_tuned(const std::string& key);
 
 // compile_schedule analogue: matrix (rows x cols, GF(2^w) entries) -> program
 Program compile_program(const Field& f, TransformKind kind, const Matrix& m, const CompileOptions& opt);
+
+// One region op of a reference XorSchedule (schedule.hpp:40-48); mode is
+// OpMode: 0 Copy, 1 Xor, 2 Zero.
+struct ScheduleOp {
+    std::uint16_t src_sym = 0, src_pkt = 0, dst_sym = 0, dst_pkt = 0;
+    std::uint8_t mode = 0;
+};
+
+// A reference XorSchedule compiled for the GPU: the B200 replacement for
+// replay()/parallel_replay() over an arbitrary schedule (codec.hpp:118-193).
+// The schedule (pre, core, post concatenated in replay order) is evaluated
+// symbolically over GF(2): every output packet it writes is a XOR of
+// initial input packets, which one fused kernel computes column word by
+// column word.  Slots follow replay(): sym < k is input slot sym (in_map),
+// sym >= k output slot sym - k (out_map); packets >= w are workspace
+// scratch, zero at entry (a fresh Workspace, as parallel_replay makes).
+// Slots that share storage (decode() passes one SymbolBuffer as in and out)
+// carry equal labels, so a write through one slot is seen by later reads
+// through another, as in the reference's op-by-op replay.
+//   kernel input q reads slot src_slot[q] (>= 0: input slot; < 0: output
+//   slot -1-src_slot[q], its contents before the call); kernel output r is
+//   output slot dst_slot[r], written only on the strips in prog.written.
+struct ScheduleProgram {
+    Program prog;
+    std::vector<std::int32_t> src_slot;
+    std::vector<std::uint32_t> dst_slot;
+    std::uint32_t k = 0, outputs = 0;
+};
+// labels: k + outputs storage labels (empty = all slots distinct)
+ScheduleProgram compile_schedule_program(const Field& f, std::uint32_t k, std::uint32_t outputs,
+                                         const std::vector<ScheduleOp>& ops, const std::vector<std::uint32_t>& labels,
+                                         const CompileOptions& opt);
 
 // Host interpreter of a compiled program (verification of the compiler on
 // machines without a GPU; never used by the device path).  Window

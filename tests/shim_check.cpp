@@ -62,6 +62,54 @@ int main() {
         std::printf("%-40s encode %s decode %s\n", c.name, enc_ok ? "OK" : "MISMATCH", dec_ok ? "OK" : "MISMATCH");
         failures += !enc_ok + !dec_ok;
     }
+    // operator level: the reference's own schedules replayed by pyrit::cuda::parallel_replay
+    {
+        struct SCase {
+            const char* name;
+            FieldSpec f;
+            unsigned k, r;
+            TransformKind kind;
+            int which; // 0 sparse ring, 1 dense ring, 2 CRS
+        };
+        const SCase sc[] = {
+            {"gf16 k4 r2 sparse", FieldSpec::gf16_aop(), 4, 2, TransformKind::Embedding, 0},
+            {"gf16 k4 r2 dense", FieldSpec::gf16_aop(), 4, 2, TransformKind::Embedding, 1},
+            {"gf64 k5 r3 crs", FieldSpec::gf64_esp(), 5, 3, TransformKind::Embedding, 2},
+            {"gf64 k3 r5 parity", FieldSpec::gf64_esp(), 3, 5, TransformKind::Parity, 0},
+            {"gf4096 k16 r4 sparse", FieldSpec{12, 13, FieldKind::Aop, 1, 12, 0x1FFF}, 16, 4, TransformKind::Embedding, 0},
+        };
+        for (const SCase& c : sc) {
+            const CodeSpec code{c.k, c.r, c.f, c.kind};
+            const FieldMatrix m = cauchy_parity_matrix(code);
+            const XorSchedule sched = c.which == 2 ? compile_crs_schedule(m)
+                                                   : compile_schedule(m, c.kind, c.which ? RingRep::Dense : RingRep::Sparse);
+            const std::size_t ss = std::size_t(c.f.w) * 8 * 777;
+            SymbolBuffer in(c.k + 2, ss, c.f);
+            fill(in, 77 + c.k);
+            std::vector<unsigned> in_map, out_map;
+            for (unsigned j = 0; j < c.k; ++j) in_map.push_back(c.k + 1 - j); // a permutation into k + 2 symbols
+            for (unsigned i = 0; i < c.r; ++i) out_map.push_back(c.r - 1 - i);
+            SymbolBuffer want(c.r, ss, c.f), got(c.r, ss, c.f);
+            fill(want, 9);
+            std::memcpy(got.symbol(0), want.symbol(0), c.r * ss);
+            parallel_replay(sched, in, in_map, want, out_map, 4);
+            pyrit::cuda::parallel_replay(sched, in, in_map, got, out_map);
+            bool ok = same(got, want);
+            // window only (replay) and in place in one buffer, decode()-style
+            SymbolBuffer both(c.k + c.r, ss, c.f), both_ref(c.k + c.r, ss, c.f);
+            fill(both, 5);
+            std::memcpy(both_ref.symbol(0), both.symbol(0), (c.k + c.r) * ss);
+            std::vector<unsigned> im(c.k), om(c.r);
+            for (unsigned j = 0; j < c.k; ++j) im[j] = j;
+            for (unsigned i = 0; i < c.r; ++i) om[i] = c.k + i;
+            Workspace ws(sched, 64);
+            replay(sched, both_ref, im, both_ref, om, ws, 128, 64);
+            pyrit::cuda::replay(sched, both, im, both, om, 128, 64);
+            ok = ok && same(both, both_ref);
+            std::printf("parallel_replay %-28s %s\n", c.name, ok ? "OK" : "MISMATCH");
+            failures += !ok;
+        }
+    }
     // error behaviour mirrors the reference
     try {
         const CodeSpec code{4, 2, FieldSpec::gf16_aop(), TransformKind::Embedding};
