@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--only", type=int, nargs="*", default=None, help="shard counts to run (default 1 2 4 8)")
     a = ap.parse_args()
 
     import torch
@@ -45,7 +46,7 @@ def main():
         plan = P.Plan.decode(wl.code, wl.erased)
         n_in, n_out = wl.k, len(wl.erased)
     base = None
-    for n in (1, 2, 4, 8):
+    for n in a.only or (1, 2, 4, 8):
         lo, hi = shard(wl.strip, 0, n)
         Ls = hi - lo
         sym = w * Ls
