@@ -561,7 +561,36 @@ ScheduleProgram compile_schedule_program(const Field& f, std::uint32_t k, std::u
                     bits[(std::size_t(r) * cols + src_of[v / w]) * w + b] |= 1u << (v % w);
         }
     }
-    if (rows) {
+    // Matrix recovery: when every written output is complete and every
+    // w x w block of the map is multiplication by a field element (true for
+    // any schedule compile_schedule or compile_crs_schedule emits, either
+    // transform: they all implement the plain GF(2^w) code), the schedule
+    // computes M x inputs for that matrix M, and the ring program of M --
+    // sparse representatives, the fold, the tuned kernel shape -- is the
+    // cheapest exact implementation (flattening a ring schedule would give
+    // the bitmatrix's XOR count instead).
+    bool field_map = rows > 0 && std::all_of(written.begin(), written.end(), [](std::uint8_t x) { return x != 0; });
+    Matrix fm(rows, cols);
+    for (std::uint32_t r = 0; field_map && r < rows; ++r)
+        for (std::uint32_t q = 0; field_map && q < cols; ++q) {
+            const std::uint32_t* blk = &bits[(std::size_t(r) * cols + q) * w];
+            std::uint32_t a = 0; // column 0 = the coefficients of a * 1
+            for (std::uint32_t b = 0; b < w; ++b) a |= (blk[b] & 1u) << b;
+            for (std::uint32_t c = 0; field_map && c < w; ++c) {
+                const std::uint32_t prod = gf_mul(a, 1u << c, f);
+                for (std::uint32_t b = 0; b < w; ++b)
+                    if (((blk[b] >> c) & 1u) != ((prod >> b) & 1u)) field_map = false;
+            }
+            fm.at(r, q) = static_cast<std::uint16_t>(a);
+        }
+    if (field_map) {
+        CompileOptions o = opt;
+        o.bits = nullptr;
+        o.written = nullptr;
+        o.crs = false;
+        o.dense = false;
+        sp.prog = compile_program(f, TransformKind::Embedding, fm, o);
+    } else if (rows) {
         CompileOptions o = opt;
         o.bits = &bits;
         o.written = &written;

@@ -232,6 +232,32 @@ def test_schedule_errors():
     assert (o == 7).all()
 
 
+def test_field_schedules_compile_to_the_ring_program():
+    """Matrix recovery: a schedule whose map is a GF(2^w) matrix (every compile_schedule /
+    compile_crs_schedule output for AOP/ESP fields, ring, dense or CRS) compiles to the same ring
+    program as the matrix itself -- same tuning key, same kernel -- so replaying the reference's
+    schedule costs what encode() costs.  R_{2,17} ring schedules from the reference are not field
+    maps (uint16 truncation): they replay as their own bit map, bytes as the reference's."""
+    from paper_1709_00178_b200.workloads import WORKLOADS
+    for c in (1, 3, 5):
+        wl = WORKLOADS[c]
+        of = ofield(wl.fld)
+        m = P.cauchy_parity_matrix(wl.code)
+        enc = P.Plan.encode(wl.code)
+        for ops in (O.compile_schedule(of, m), O.compile_crs_schedule(of, m), O.compile_schedule(of, m, 0, 1)):
+            p = P.Plan.from_schedule(P.XorSchedule(wl.fld, wl.k, wl.m, ops))
+            assert p.key() == enc.key()
+            assert p.source(P._lib.SOURCE_STAGED)[0] == enc.source(P._lib.SOURCE_STAGED)[0]
+            assert p.stats()["ref_region_ops"] == len(ops)
+    wl = WORKLOADS[2]
+    of = ofield(wl.fld)
+    m = P.cauchy_parity_matrix(wl.code)
+    crs = P.Plan.from_schedule(P.XorSchedule(wl.fld, wl.k, wl.m, O.compile_crs_schedule(of, m)))
+    assert crs.key() == P.Plan.encode(wl.code).key()
+    ring = P.Plan.from_schedule(P.XorSchedule(wl.fld, wl.k, wl.m, O.compile_schedule(of, m)))
+    assert "sch" in ring.key()
+
+
 # ------------------------------------------------------------------------- GPU
 def _torch():
     import torch
@@ -267,9 +293,33 @@ def test_gpu_reference_schedules(cuda, f):
                 P.replay(sched, di, in_map, do, out_map)
                 torch.cuda.synchronize()
                 assert np.array_equal(do.cpu().numpy(), want), (k, r, kind, which, strip)
+                assert P.Plan.last_launch()["kernel"].startswith("pyrit_ring_")
                 got = out0.copy()
                 P.replay(sched, inp, in_map, got, out_map)  # host buffers
                 assert np.array_equal(got, want), (k, r, kind, which, strip, "host")
+
+
+@pytest.mark.gpu
+def test_gpu_replay_of_baseline_schedule_uses_the_encode_kernel(cuda):
+    """The reference's compile_schedule output for BASELINE config 5 (strip shrunk), replayed through
+    P.replay, launches the same generated kernel as encode() and gives the same parity."""
+    torch = _torch()
+    from paper_1709_00178_b200.workloads import WORKLOADS
+    wl = WORKLOADS[5]
+    of = ofield(wl.fld)
+    m = P.cauchy_parity_matrix(wl.code)
+    strip = 16 * 65536
+    data = torch.from_numpy(np.random.default_rng(5).integers(0, 256, (wl.k, wl.fld.w * strip),
+                                                               dtype=np.uint8)).to(cuda)
+    parity = P.encode(data, wl.code)
+    torch.cuda.synchronize()
+    enc_kernel = P.Plan.last_launch()["kernel"]
+    out = torch.zeros_like(parity)
+    P.parallel_replay(P.XorSchedule(wl.fld, wl.k, wl.m, O.compile_schedule(of, m)), data, list(range(wl.k)), out,
+                      list(range(wl.m)))
+    torch.cuda.synchronize()
+    assert P.Plan.last_launch()["kernel"] == enc_kernel
+    assert torch.equal(out, parity)
 
 
 @pytest.mark.gpu
