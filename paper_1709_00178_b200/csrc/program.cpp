@@ -484,6 +484,9 @@ ScheduleProgram compile_schedule_program(const Field& f, std::uint32_t k, std::u
     // GF(2) symbolic replay (codec.hpp:129-156): the value of every packet is
     // a set of initial packets (storage, strip), one bit each
     const std::size_t nv = std::size_t(nstore) * w, words = (nv + 63) / 64;
+    // one bit vector per packet and scratch packet: keep the symbolic state bounded
+    if ((nv + std::size_t(slots) * (n - w)) * words * 8 > (std::size_t(1) << 30))
+        raise(Errc::InvalidArgument, "schedule has too many slots for symbolic replay");
     using Vec = std::vector<std::uint64_t>;
     std::vector<Vec> phys(nv, Vec(words, 0)), scratch(std::size_t(slots) * (n - w), Vec(words, 0));
     for (std::size_t v = 0; v < nv; ++v) phys[v][v / 64] |= 1ull << (v % 64);
