@@ -196,6 +196,8 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
     p.group = std::min(p.group, k);
     p.cse = opt.cse;
     p.crs = opt.crs || opt.bits;
+    // (p.cse is revised below for very large programs: greedy pair sharing is
+    // superlinear in the terms per fragment group)
     p.sched = opt.bits != nullptr;
     p.matrix = m.e;
     p.fold = fold_table(f);
@@ -231,6 +233,11 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
             }
     }
 
+    // Pair sharing costs time superlinear in the program size and its
+    // temporaries only serve the unsplit kernels; very large codes (more than
+    // ~200k ring-matrix ones, e.g. k = 100, r = 50 over GF(2^12)) run split
+    // into output parts, which do not share pairs, so skip it there.
+    if (p.stats.matrix_ones > 200000) p.cse = false;
     const bool emb = kind == TransformKind::Embedding;
     const bool crs = p.crs;
     const std::uint32_t out_rows = emb && !crs ? n : w; // schedule.hpp:132 (CRS: w bit rows)
@@ -305,7 +312,7 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
                 std::sort(tg.begin(), tg.end());
                 p.stats.naive_xors += tg.size(); // one XOR per term into the row...
             }
-        if (opt.cse) {
+        if (p.cse) {
             // pair sharing over windows of cse_window consecutive targets (ring
             // rows, output by output); 0 = the whole group.  Small windows keep
             // shared temporaries short-lived (register pressure)
@@ -361,7 +368,7 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
             if (!targets[b].empty() && acc[i * out_rows + b] == kNone) --p.stats.naive_xors;
         }
         std::vector<Instr> fold;
-        if (opt.cse) share_pairs(targets, nvars, fold);
+        if (p.cse) share_pairs(targets, nvars, fold);
         const std::size_t ntemps = fold.size();
         for (std::uint32_t b = 0; b < w; ++b)
             if (!p.sched || p.written[std::size_t(i) * w + b]) fold.push_back(Instr{Instr::Store, 0, i, b, targets[b]});

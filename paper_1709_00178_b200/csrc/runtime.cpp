@@ -3,6 +3,9 @@
 #include <cuda.h>
 #include <dlfcn.h>
 #include <nvrtc.h>
+#include <unistd.h>
+
+#include <filesystem>
 
 #include <atomic>
 #include <cstring>
@@ -99,6 +102,41 @@ std::vector<char> read_file(const std::string& path) {
     return std::vector<char>(std::istreambuf_iterator<char>(f), {});
 }
 
+// Kernels compiled by NVRTC are kept on disk so a program is compiled once
+// per machine, not once per process (large codes take tens of seconds).
+// The kernel name carries the generator version and a hash of the program
+// and shape, so a cached cubin is never stale.  PYRIT_B200_JIT_CACHE = a
+// directory, or "0" / "" to disable; default $XDG_CACHE_HOME/pyrit_b200 or
+// ~/.cache/pyrit_b200.
+std::string jit_cache_dir() {
+    static const std::string dir = [] {
+        if (const char* env = std::getenv("PYRIT_B200_JIT_CACHE"))
+            return std::string(env) == "0" ? std::string() : std::string(env);
+        if (const char* x = std::getenv("XDG_CACHE_HOME"); x && *x) return std::string(x) + "/pyrit_b200";
+        if (const char* h = std::getenv("HOME"); h && *h) return std::string(h) + "/.cache/pyrit_b200";
+        return std::string();
+    }();
+    return dir;
+}
+
+void write_cache(const std::string& dir, const std::string& name, const std::vector<char>& cubin) {
+    std::error_code ec;
+    std::filesystem::create_directories(dir, ec);
+    if (ec) return; // the cache is an optimisation only
+    const std::string tmp = dir + "/." + name + "." + std::to_string(::getpid()) + ".tmp";
+    {
+        std::ofstream f(tmp, std::ios::binary);
+        if (!f) return;
+        f.write(cubin.data(), static_cast<std::streamsize>(cubin.size()));
+        if (!f) {
+            std::filesystem::remove(tmp, ec);
+            return;
+        }
+    }
+    std::filesystem::rename(tmp, dir + "/" + name + ".cubin", ec); // atomic: readers never see a partial file
+    if (ec) std::filesystem::remove(tmp, ec);
+}
+
 std::vector<char> nvrtc_compile(const std::string& src, const std::string& name) {
     nvrtcProgram prog;
     auto chk = [&](nvrtcResult r, const char* what) {
@@ -133,8 +171,14 @@ LoadedKernel load_kernel(const Program& p, const KernelShape& ks, int device) {
         auto it = g_kernels.find(key);
         if (it != g_kernels.end()) return it->second;
     }
+    // prebuilt (next to the library), else the on-disk JIT cache, else NVRTC
     std::vector<char> cubin = read_file(kernel_dir() + "/" + name + ".cubin");
-    if (cubin.empty()) cubin = nvrtc_compile(generate_cuda(p, ks), name);
+    const std::string cache = jit_cache_dir();
+    if (cubin.empty() && !cache.empty()) cubin = read_file(cache + "/" + name + ".cubin");
+    if (cubin.empty()) {
+        cubin = nvrtc_compile(generate_cuda(p, ks), name);
+        if (!cache.empty()) write_cache(cache, name, cubin);
+    }
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_kernels.find(key);
     if (it != g_kernels.end()) return it->second;
