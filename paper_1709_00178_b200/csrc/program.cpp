@@ -434,7 +434,13 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
         pg = std::max<std::uint32_t>(1, std::min(pg, k));
         int pcse = env_u("PYRIT_B200_PART_CSE");
         if (pcse < 0 && tuned) pcse = tuned->part_cse;
-        if (pcse < 0) pcse = 0;
+        // Parity transform: every input's column parities (ring positions
+        // >= w) are XORs of its data strips, so expanded ring rows repeat the
+        // same pairs; sharing them within one output's rows (short-lived
+        // temporaries) pays: (60,20) GF(2^6) parity code 1.57x
+        // (profiles/r01_s3/cse/); for the embedding codes it does not
+        const bool parity_cse = !emb && !crs && pcse < 0;
+        if (pcse < 0) pcse = parity_cse ? 1 : 0;
         auto build_parts = [&](bool cse) {
             p.parts.clear();
             p.part_row0.clear();
@@ -459,6 +465,7 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
                 o2.cse = cse && opt.cse;
                 if (const char* env = std::getenv("PYRIT_B200_PART_TEMPS")) o2.max_temps = std::atoi(env);
                 if (const char* env = std::getenv("PYRIT_B200_CSE_WINDOW")) o2.cse_window = std::atoi(env);
+                else if (parity_cse) o2.cse_window = w; // one output's rows
                 p.parts.push_back(compile_program(f, kind, sub, o2));
                 p.part_row0.push_back(row0);
                 row0 += nrows;

@@ -33,6 +33,8 @@ def main():
     ap.add_argument("--frag", type=int, default=0, help="fragment bytes (overrides the config's; > L2 working set)")
     ap.add_argument("--rounds", type=int, default=3, help="interleaved repeats per variant (median reported)")
     ap.add_argument("--no-graph", action="store_true", help="launch from Python instead of a captured CUDA graph")
+    ap.add_argument("--code", default="", help="k,r,field[,transform]: an encode of this code instead of a config "
+                    "(field gf16|gf64|gf256_r17|aop<w>; transform 0 embedding, 1 parity); needs --frag")
     a = ap.parse_args()
 
     import torch
@@ -43,7 +45,16 @@ def main():
 
     lib = L.load()
     dev = torch.device("cuda", 0)
-    wl = WORKLOADS[a.config]
+    transform = 0
+    if a.code:
+        from paper_1709_00178_b200.workloads import Workload
+        parts = a.code.split(",")
+        fn = parts[2]
+        fld = P.FieldSpec.aop(int(fn[3:])) if fn.startswith("aop") else getattr(P.FieldSpec, fn + ("_aop" if fn == "gf16" else "_esp" if fn == "gf64" else ""))()
+        transform = int(parts[3]) if len(parts) > 3 else 0
+        wl = Workload(0, f"code-{a.code}", "encode", fld, int(parts[0]), int(parts[1]), a.frag, 7)
+    else:
+        wl = WORKLOADS[a.config]
     w = wl.fld.w
     S = (a.frag // w if a.frag else wl.strip // a.scale) // 16 * 16
     sym = w * S
@@ -68,7 +79,7 @@ def main():
         outs = [out[i].data_ptr() for i in range(len(order))]
     moved = (len(ins) + len(outs)) * sym
     ref = None
-    knobs = ("MODE", "COPY", "PARTS", "PART_GROUP", "PART_CSE", "PART_TEMPS", "THREADS", "LANES")
+    knobs = ("MODE", "COPY", "PARTS", "PART_GROUP", "PART_CSE", "PART_TEMPS", "THREADS", "LANES", "CSE_WINDOW")
     specs = a.variants.split(";")
     plans, graphs, times, clocks = {}, {}, {sp: [] for sp in specs}, {}
     for rnd in range(a.rounds):
@@ -82,7 +93,7 @@ def main():
             L.check(lib.pyrit_set_lanes(int(env.get("LANES", 1))))
             try:
                 if spec not in plans:
-                    plans[spec] = P.Plan.create(wl.fld, m)
+                    plans[spec] = P.Plan.create(wl.fld, m, transform=transform)
                 plan = plans[spec]
                 for _ in range(a.warmup):
                     plan.apply(ins, outs, S, stream=stream)
