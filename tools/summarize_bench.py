@@ -1,3 +1,5 @@
+#!/usr/bin/env python
+"""One summary line per bench.py JSON line: python tools/summarize_bench.py profiles/r01_s3/bench_*.jsonl"""
 import json,sys
 for fn in sys.argv[1:]:
     for line in open(fn):

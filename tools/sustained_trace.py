@@ -1,3 +1,14 @@
+#!/usr/bin/env python
+"""Launch-by-launch trace of a BASELINE config's kernel (sustained behaviour).
+
+    CFG=5 N=300 python tools/sustained_trace.py
+
+Launches the encode program N times back to back from Python, records a CUDA event
+after every launch, and prints one JSON line. The line has the mean launch time over
+launches 0-19, 20-99 and 100-end, and every 10th launch time. These traces are the
+sustained_trace_* files under profiles/r01_s2: they compare the TMA and cp.async
+producers, and the torch copy probes.
+"""
 import os, sys, json, time
 sys.path.insert(0, os.getcwd())
 import torch
