@@ -30,7 +30,7 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-HOST_SOURCES = ["algebra.cpp", "program.cpp", "runtime.cpp", "pipeline.cpp", "plans.cpp", "container.cpp", "capi.cpp"]
+HOST_SOURCES = ["algebra.cpp", "program.cpp", "runtime.cpp", "pipeline.cpp", "plans.cpp", "container.cpp", "hostpool.cpp", "capi.cpp"]
 CUDA_SOURCES = ["kernels.cu"]
 HEADERS = ["algebra.hpp", "program.hpp", "runtime.hpp", "pipeline.hpp", "plans.hpp", "container.hpp", "kernels.hpp"]
 

@@ -19,6 +19,7 @@
 #include <memory>
 #include <mutex>
 
+#include "hostpool.hpp"
 #include "plans.hpp"
 #include "runtime.hpp"
 
@@ -118,98 +119,12 @@ void pwritev_full(int fd, std::vector<iovec>& iov, std::uint64_t off, const std:
     }
 }
 
-// ---- host I/O workers: shard files are read and written in parallel ------
-
-class IoPool {
-public:
-    IoPool() {
-        const unsigned n = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-        for (unsigned i = 0; i + 1 < n; ++i) workers_.emplace_back([this] { loop(); });
-    }
-    ~IoPool() {
-        {
-            std::lock_guard<std::mutex> lk(mu_);
-            stop_ = true;
-        }
-        cv_.notify_all();
-        for (auto& th : workers_) th.join();
-    }
-    // f(0..n-1) on the workers and the caller; rethrows the first failure
-    void run(std::size_t n, const std::function<void(std::size_t)>& f) {
-        if (n == 0) return;
-        Job job{&f, n, 0, 0, nullptr};
-        std::unique_lock<std::mutex> lk(mu_);
-        jobs_.push_back(&job);
-        cv_.notify_all();
-        // an item is claimed (next++) under the lock and counted as finished
-        // only after it ran, so the job outlives every worker touching it
-        while (job.next < job.n) {
-            const std::size_t i = job.next++;
-            lk.unlock();
-            execute(job, i);
-            lk.lock();
-        }
-        done_cv_.wait(lk, [&] { return job.finished == job.n; });
-        jobs_.erase(std::remove(jobs_.begin(), jobs_.end(), &job), jobs_.end());
-        if (job.error) std::rethrow_exception(job.error);
-    }
-
-private:
-    struct Job {
-        const std::function<void(std::size_t)>* f;
-        std::size_t n, next, finished;
-        std::exception_ptr error;
-    };
-    // runs item i of job (claimed by the caller) and records completion
-    void execute(Job& job, std::size_t i) {
-        std::exception_ptr err;
-        try {
-            (*job.f)(i);
-        } catch (...) {
-            err = std::current_exception();
-        }
-        std::lock_guard<std::mutex> lk(mu_);
-        if (err && !job.error) job.error = err;
-        if (++job.finished == job.n) done_cv_.notify_all();
-    }
-    void loop() {
-        std::unique_lock<std::mutex> lk(mu_);
-        for (;;) {
-            Job* job = nullptr;
-            cv_.wait(lk, [&] {
-                if (stop_) return true;
-                for (Job* j : jobs_)
-                    if (j->next < j->n) {
-                        job = j;
-                        return true;
-                    }
-                return false;
-            });
-            if (stop_) return;
-            const std::size_t i = job->next++;
-            lk.unlock();
-            execute(*job, i);
-            lk.lock();
-        }
-    }
-    std::mutex mu_;
-    std::condition_variable cv_, done_cv_;
-    std::vector<Job*> jobs_;
-    std::vector<std::thread> workers_;
-    bool stop_ = false;
-};
-
-IoPool& io_pool() {
-    static IoPool pool;
-    return pool;
-}
-
 // pread of [off, off+len) split over the pool; returns the bytes read
 std::size_t pread_parallel(int fd, std::uint8_t* dst, std::size_t len, std::uint64_t off, const std::string& path) {
     constexpr std::size_t kPiece = 8u << 20;
     const std::size_t pieces = (len + kPiece - 1) / kPiece;
     std::vector<std::size_t> got(pieces, 0);
-    io_pool().run(pieces, [&](std::size_t i) {
+    host_pool().run(pieces, [&](std::size_t i) {
         const std::size_t b = i * kPiece, n = std::min(kPiece, len - b);
         got[i] = pread_full(fd, dst + b, n, off + b, path);
     });
@@ -457,7 +372,7 @@ std::vector<std::string> encode_file(const std::string& input, const std::string
             check_cuda(cudaSetDevice(device), "cudaSetDevice");
             check_cuda(cudaStreamSynchronize(sp->stream), "cudaStreamSynchronize");
             const std::uint64_t at_shard = kHeaderSize + s0 * ss;
-            io_pool().run(total, [&](std::size_t i) { // one shard file per task
+            host_pool().run(total, [&](std::size_t i) { // one shard file per task
                 if (i < k) {
                     std::vector<iovec> iov(nb);
                     for (std::uint64_t b = 0; b < nb; ++b) iov[b] = {sp->h_in + b * stripe_bytes + i * ss, ss};
@@ -578,7 +493,7 @@ void decode_file(const std::vector<std::string>& shard_paths, const std::string&
         if (pending[c % kStages].valid()) pending[c % kStages].get();
         const std::uint64_t nb = std::min(B, stripes - s0);
         // survivor-major staging: survivor i's nb symbols are contiguous
-        io_pool().run(surv.size(), [&](std::size_t i) {
+        host_pool().run(surv.size(), [&](std::size_t i) {
             const Loaded& L = byindex[surv[i]];
             const std::size_t want = static_cast<std::size_t>(nb * ss);
             if (pread_full(L.fd.fd, st.h_in + i * nb * ss, want, kHeaderSize + s0 * ss, L.path) != want)
@@ -596,7 +511,7 @@ void decode_file(const std::vector<std::string>& shard_paths, const std::string&
             check_cuda(cudaStreamSynchronize(sp->stream), "cudaStreamSynchronize");
             // the output range of this chunk, written by several tasks (runs of stripes)
             const std::uint64_t pieces = std::min<std::uint64_t>(nb, 16);
-            io_pool().run(pieces, [&](std::size_t q) {
+            host_pool().run(pieces, [&](std::size_t q) {
                 const std::uint64_t b0 = nb * q / pieces, b1 = nb * (q + 1) / pieces;
                 const std::uint64_t at = (s0 + b0) * stripe_bytes;
                 if (at >= length) return;

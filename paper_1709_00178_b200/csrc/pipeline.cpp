@@ -5,6 +5,10 @@
 // D2H copy of chunk c-1 overlap on the two copy engines and the SMs.
 #include "pipeline.hpp"
 
+#include <cstring>
+
+#include "hostpool.hpp"
+
 #include <algorithm>
 #include <cstdlib>
 #include <map>
@@ -22,7 +26,21 @@ struct Slot {
     cudaStream_t stream = nullptr;
     std::uint8_t* buf = nullptr;
     std::size_t bytes = 0;
+    // pageable callers: pinned mirror of buf, and the event after the slot's D2H
+    std::uint8_t* hbuf = nullptr;
+    std::size_t hbytes = 0;
+    cudaEvent_t done = nullptr;
 };
+
+// true when the driver can DMA straight from/to p (page-locked or managed)
+bool dma_capable(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError(); // unregistered pointers can report an error on older drivers
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
 
 struct DeviceCtx {
     std::mutex mu;
@@ -79,6 +97,84 @@ void run_host_devices(const Program& p, const std::vector<const std::uint8_t*>& 
         if (e) std::rethrow_exception(e);
 }
 
+namespace {
+
+// strips of output i that the program stores (all, except for schedule programs)
+bool stores_strip(const Program& p, std::uint32_t i, std::uint32_t b) {
+    return !p.sched || p.written[std::size_t(i) * p.field.w + b];
+}
+
+void run_staged(const Program& p, const std::vector<const std::uint8_t*>& host_in,
+                const std::vector<std::uint8_t*>& host_out, std::uint64_t strip, std::uint64_t off,
+                std::uint64_t win, std::uint64_t chunk, DeviceCtx& ctx) {
+    const std::uint32_t w = p.field.w;
+    const std::uint64_t in_strips = std::uint64_t(p.cols) * w;
+    const std::size_t need = static_cast<std::size_t>(std::uint64_t(p.cols + p.rows) * w * chunk);
+    for (Slot& s : ctx.slots) {
+        if (s.hbytes < need) {
+            if (s.hbuf) check_cuda(cudaFreeHost(s.hbuf), "cudaFreeHost");
+            s.hbuf = nullptr;
+            s.hbytes = 0;
+            check_cuda(cudaHostAlloc(reinterpret_cast<void**>(&s.hbuf), need, cudaHostAllocDefault), "pinned staging");
+            s.hbytes = need;
+        }
+        if (!s.done) check_cuda(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming), "event");
+    }
+    std::vector<std::pair<std::uint32_t, std::uint32_t>> out_strips; // (output, strip) stored
+    for (std::uint32_t i = 0; i < p.rows; ++i)
+        for (std::uint32_t b = 0; b < w; ++b)
+            if (stores_strip(p, i, b)) out_strips.push_back({i, b});
+    struct Pending {
+        bool live = false;
+        std::uint64_t c0 = 0, len = 0;
+    } pend[kSlots];
+    auto unpack = [&](int si) {
+        Slot& s = ctx.slots[si];
+        Pending& pd = pend[si];
+        if (!pd.live) return;
+        check_cuda(cudaEventSynchronize(s.done), "cudaEventSynchronize");
+        const std::uint8_t* h_out = s.hbuf + in_strips * chunk;
+        host_pool().run(out_strips.size(), [&](std::size_t q) {
+            const auto [i, b] = out_strips[q];
+            std::memcpy(host_out[i] + std::uint64_t(b) * strip + pd.c0, h_out + (std::uint64_t(i) * w + b) * chunk,
+                        pd.len);
+        });
+        pd.live = false;
+    };
+    std::vector<const std::uint8_t*> din(p.cols);
+    std::vector<std::uint8_t*> dout(p.rows);
+    std::uint64_t c0 = off;
+    try {
+        for (int c = 0; c0 < off + win; ++c) {
+            const std::uint64_t len = std::min(chunk, off + win - c0);
+            const int si = c % kSlots;
+            Slot& s = ctx.slots[si];
+            unpack(si); // the slot's previous chunk is done (H2D, kernel, D2H)
+            host_pool().run(in_strips, [&](std::size_t q) {
+                const std::uint64_t j = q / w, b = q % w;
+                std::memcpy(s.hbuf + q * chunk, host_in[j] + b * strip + c0, len);
+            });
+            check_cuda(cudaMemcpy2DAsync(s.buf, chunk, s.hbuf, chunk, len, in_strips, cudaMemcpyHostToDevice, s.stream),
+                       "H2D");
+            for (std::uint32_t j = 0; j < p.cols; ++j) din[j] = s.buf + std::uint64_t(j) * w * chunk;
+            for (std::uint32_t i = 0; i < p.rows; ++i) dout[i] = s.buf + std::uint64_t(p.cols + i) * w * chunk;
+            launch_program(p, din.data(), dout.data(), chunk, 0, len, s.stream);
+            check_cuda(cudaMemcpy2DAsync(s.hbuf + in_strips * chunk, chunk, s.buf + in_strips * chunk, chunk, len,
+                                         std::uint64_t(p.rows) * w, cudaMemcpyDeviceToHost, s.stream),
+                       "D2H");
+            check_cuda(cudaEventRecord(s.done, s.stream), "cudaEventRecord");
+            pend[si] = {true, c0, len};
+            c0 += len;
+        }
+        for (int si = 0; si < kSlots; ++si) unpack(si);
+    } catch (...) {
+        for (Slot& s : ctx.slots) (void)cudaStreamSynchronize(s.stream); // no copy may outlive the caller's buffers
+        throw;
+    }
+}
+
+} // namespace
+
 void run_host_window(const Program& p, const std::vector<const std::uint8_t*>& host_in,
                      const std::vector<std::uint8_t*>& host_out, std::uint64_t strip, std::uint64_t off,
                      std::uint64_t win, int device) {
@@ -114,6 +210,19 @@ void run_host_window(const Program& p, const std::vector<const std::uint8_t*>& h
             check_cuda(cudaMalloc(&s.buf, need), "cudaMalloc staging");
             s.bytes = need;
         }
+    }
+    // Pageable symbols (a reference SymbolBuffer is a std::vector): the
+    // driver would stage every copy through its own small pinned buffer,
+    // synchronously and on one thread (measured 8-10 GB/s).  Instead the host
+    // pool packs each chunk's strips into a pinned mirror of the slot (and
+    // unpacks the outputs) while the copy engines and SMs work on the other
+    // slots: pack chunk c | H2D + kernel + D2H of c-1, c-2 | unpack c-3.
+    bool pinned = true;
+    for (const std::uint8_t* q : host_in) pinned = pinned && dma_capable(q);
+    for (std::uint8_t* q : host_out) pinned = pinned && dma_capable(q);
+    if (!pinned) {
+        run_staged(p, host_in, host_out, strip, off, win, chunk, ctx);
+        return;
     }
     // runs of symbols laid out back to back on the host (SymbolBuffer storage,
     // codec.hpp:24-73): one 2D copy moves the window of all their strips
