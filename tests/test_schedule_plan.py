@@ -258,6 +258,26 @@ def test_field_schedules_compile_to_the_ring_program():
     assert "sch" in ring.key()
 
 
+def test_c_abi_argument_errors():
+    """pyrit_plan_from_schedule / pyrit_apply_host validate their arguments before any device work
+    (return codes are 1 + Errc, errors.hpp:12-24)."""
+    import ctypes as C
+    from paper_1709_00178_b200 import _lib as L
+    lib = L.load()
+    f = G16.c()
+    h = C.c_void_p()
+    assert lib.pyrit_plan_from_schedule(C.byref(f), 1, 1, None, 3, None, C.byref(h)) == 11  # InvalidArgument
+    assert lib.pyrit_plan_from_schedule(C.byref(f), 0, 1, None, 0, None, C.byref(h)) == 11  # no input slots
+    ops = np.array([(0, 0, 1, 0, 0)], dtype=P.OP_DTYPE)
+    plan = P.Plan.from_schedule(P.XorSchedule(G16, 1, 1, ops))
+    a = np.zeros(64, dtype=np.uint8)
+    arr = (C.c_void_p * 1)(a.ctypes.data)
+    assert lib.pyrit_apply_host(plan._h, None, arr, 16, 0, 16, 0) == 11
+    assert lib.pyrit_apply_host(plan._h, arr, arr, 16, 8, 16, 0) == 4  # BufferShape: window past the strip
+    nul = (C.c_void_p * 1)(None)
+    assert lib.pyrit_apply_host(plan._h, nul, arr, 16, 0, 16, 0) == 11  # null symbol pointer
+
+
 # ------------------------------------------------------------------------- GPU
 def _torch():
     import torch
