@@ -358,11 +358,13 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
     for (std::uint32_t i = 0; i < e; ++i) {
         std::vector<std::vector<std::uint32_t>> targets(w);
         for (std::uint32_t b = 0; b < w; ++b) {
-            if (acc[i * out_rows + b] != kNone) targets[b].push_back(acc[i * out_rows + b]);
+            // toggle, not append: two ring rows can be the same variable (a row
+            // that is a single input strip aliases the load), and x ^ x = 0
+            if (acc[i * out_rows + b] != kNone) toggle(targets[b], acc[i * out_rows + b]);
             if (emb && !crs)
                 for (std::uint32_t t = w; t < n; ++t)
                     if (((p.fold[t - w] >> b) & 1u) && acc[i * out_rows + t] != kNone) {
-                        targets[b].push_back(acc[i * out_rows + t]);
+                        toggle(targets[b], acc[i * out_rows + t]);
                         ++p.stats.naive_xors;
                     }
             if (!targets[b].empty() && acc[i * out_rows + b] == kNone) --p.stats.naive_xors;
