@@ -383,6 +383,15 @@ int pyrit_plan_interpret(const pyrit_plan* plan, const uint8_t* const* in, uint8
             interpret_program(plan->prog, kin.data(), kout.data(), strip_bytes, off, len);
             return;
         }
+        // PYRIT_B200_INTERPRET_PARTS=1: run the output parts the staged and
+        // split kernels execute (rows part_row0[r] ..) instead of the whole
+        // program, so CPU tests cover the part programs too
+        const char* parts_env = std::getenv("PYRIT_B200_INTERPRET_PARTS");
+        if (parts_env && std::atoi(parts_env) && !plan->prog.parts.empty()) {
+            for (std::size_t r = 0; r < plan->prog.parts.size(); ++r)
+                interpret_program(plan->prog.parts[r], in, out + plan->prog.part_row0[r], strip_bytes, off, len);
+            return;
+        }
         interpret_program(plan->prog, in, out, strip_bytes, off, len);
     });
 }

@@ -72,3 +72,54 @@ def test_representatives_any_field(f):
         best = min(cands, key=lambda c: (bin(c).count("1"), c))
         assert bin(rep).count("1") == bin(best).count("1")
         assert rep == O.sparse_transform(u, ofield(f))
+
+
+AOP_ESP = [P.FieldSpec(2, 3, 0, 1, 2, 0b111), P.FieldSpec.gf16_aop(), P.FieldSpec.gf64_esp(), P.FieldSpec.aop(10),
+           P.FieldSpec.aop(12)]
+KNOBS = ("PARTS", "PART_GROUP", "PART_CSE", "CSE_WINDOW", "PART_TEMPS")
+
+
+@st.composite
+def part_cases(draw):
+    parity = draw(st.booleans())
+    f = draw(st.sampled_from(AOP_ESP if parity else FIELDS))
+    k = draw(st.integers(1, 7))
+    r = draw(st.integers(1, 6))
+    entries = draw(st.lists(st.integers(0, (1 << f.w) - 1), min_size=k * r, max_size=k * r))
+    m = np.array(entries, dtype=np.uint16).reshape(r, k)
+    knobs = {"PARTS": draw(st.integers(1, 4)), "PART_GROUP": draw(st.integers(1, 4)),
+             "PART_CSE": draw(st.integers(0, 1)), "CSE_WINDOW": draw(st.sampled_from([0, 1, 2, 5])),
+             "PART_TEMPS": draw(st.sampled_from([0, 3]))}
+    group = draw(st.integers(0, 3))
+    strip = draw(st.integers(1, 24))
+    return f, int(parity), m, knobs, group, strip, draw(st.integers(0, 2**31))
+
+
+@settings(max_examples=300, deadline=None)
+@given(part_cases())
+def test_output_parts_and_pair_sharing(case):
+    """The programs the kernels actually run -- output parts (the staged kernel's warp groups, the
+    split direct kernel's thread groups) with their fragment groups and windowed pair sharing --
+    interpreted part by part, against the field oracle; both transforms."""
+    import os
+    f, kind, m, knobs, group, strip, seed = case
+    rng = np.random.default_rng(seed)
+    r, k = m.shape
+    ins = [rng.integers(0, 256, f.w * strip, dtype=np.uint8) for _ in range(k)]
+    want = O.apply_columns(ofield(f), m, ins, strip, kind=kind)
+    saved = {n: os.environ.get("PYRIT_B200_" + n) for n in KNOBS + ("INTERPRET_PARTS",)}
+    try:
+        for n, v in knobs.items():
+            os.environ["PYRIT_B200_" + n] = str(v)
+        os.environ["PYRIT_B200_INTERPRET_PARTS"] = "1"
+        plan = P.Plan.create(f, m, transform=P.TransformKind(kind), group=group)
+        assert plan.stats()["parts"] == min(knobs["PARTS"], r)
+        got = plan.interpret(ins, strip, outs=[np.full(f.w * strip, 0xA5, dtype=np.uint8) for _ in range(r)])
+    finally:
+        for n, v in saved.items():
+            if v is None:
+                os.environ.pop("PYRIT_B200_" + n, None)
+            else:
+                os.environ["PYRIT_B200_" + n] = v
+    for a, b in zip(got, want):
+        assert np.array_equal(a, b)
