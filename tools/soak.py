@@ -25,6 +25,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", type=int, default=300)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--knobs", action="store_true",
+                    help="also random matrices, more (w, n, p) fields and random compile knobs (parts, fragment "
+                         "groups, pair sharing windows, CTA size)")
     a = ap.parse_args()
 
     import numpy as np
@@ -39,12 +42,15 @@ def main():
     rng = random.Random(a.seed)
     fields = [P.FieldSpec.gf16_aop(), P.FieldSpec.gf64_esp(), P.FieldSpec.gf256_r17(), P.FieldSpec.aop(10),
               P.FieldSpec.aop(12)]
+    exotic = [P.FieldSpec(2, 3, 0, 1, 2, 0b111), P.FieldSpec(3, 7, 0, 1, 3, 0b1011),
+              P.FieldSpec(4, 15, 0, 1, 4, 0b10011)]
+    knob_names = ("PARTS", "PART_GROUP", "PART_CSE", "CSE_WINDOW", "THREADS")
     fails, t0, kernels = [], time.time(), set()
     for case in range(a.cases):
-        f = rng.choice(fields)
+        f = rng.choice(fields + (exotic if a.knobs else []))
         k = rng.randint(1, min(32, f.field_size() - 1))
         r = rng.randint(1, min(16, f.field_size() - k))
-        kind = rng.choice([0, 0, 0, 1])
+        kind = rng.choice([0, 0, 0, 1]) if f not in exotic else 0
         strip = 16 * rng.randint(1, 2048) + rng.choice([0, 0, 0, 4, 8])
         nb = rng.choice([1, 1, 2, 5])
         mode = rng.choice([0, 2, 2])
@@ -53,7 +59,18 @@ def main():
         os.environ["PYRIT_B200_WS"] = "1" if prod == "3" else "0"
         L.check(lib.pyrit_set_kernel_mode(mode))
         code = P.CodeSpec(k, r, f, P.TransformKind(kind))
-        m = P.cauchy_parity_matrix(code)
+        knobs = {}
+        if a.knobs:
+            knobs = {"PARTS": rng.choice([1, 2, 4]), "PART_GROUP": rng.randint(1, 4), "PART_CSE": rng.randint(0, 1),
+                     "CSE_WINDOW": rng.choice([0, 1, 3, 9]), "THREADS": rng.choice([256, 512])}
+        for n in knob_names:
+            os.environ.pop("PYRIT_B200_" + n, None)
+        for n, v in knobs.items():
+            os.environ["PYRIT_B200_" + n] = str(v)
+        if a.knobs and rng.random() < 0.5:
+            m = np.array([[rng.randrange(f.field_size()) for _ in range(k)] for _ in range(r)], dtype=np.uint16)
+        else:
+            m = P.cauchy_parity_matrix(code)
         plan = P.Plan.create(f, m, P.TransformKind(kind))
         sym = f.w * strip
         data = np.random.default_rng(case).integers(0, 256, (nb, k, sym), dtype=np.uint8)
@@ -70,14 +87,16 @@ def main():
                 want = O.ring_replay(of, m, [data[b, j].copy() for j in range(k)], strip, kind=kind)
                 if not all(np.array_equal(got[b, i], want[i]) for i in range(r)):
                     fails.append({"case": case, "field": [f.w, f.n], "k": k, "r": r, "kind": kind, "strip": strip,
-                                  "nb": nb, "mode": mode, "producer": prod, "stripe": b,
+                                  "nb": nb, "mode": mode, "producer": prod, "stripe": b, "knobs": knobs,
                                   "kernel": P.Plan.last_launch()["kernel"]})
                     break
         except Exception as e:  # report, keep soaking
             fails.append({"case": case, "error": str(e)[:200], "k": k, "r": r, "strip": strip, "producer": prod})
         plan.close()
     L.check(lib.pyrit_set_kernel_mode(0))
-    print(json.dumps({"cases": a.cases, "failures": len(fails), "distinct_kernels": len(kernels),
+    for n in knob_names:
+        os.environ.pop("PYRIT_B200_" + n, None)
+    print(json.dumps({"cases": a.cases, "knobs": a.knobs, "failures": len(fails), "distinct_kernels": len(kernels),
                       "seconds": round(time.time() - t0, 1), "first_failures": fails[:5]}))
     return 1 if fails else 0
 
