@@ -193,9 +193,16 @@ void run_host_window(const Program& p, const std::vector<const std::uint8_t*>& h
         const std::uint64_t mib = env ? std::strtoull(env, nullptr, 10) : 192;
         chunk = ((mib ? mib : 192) << 20) / strips; // ~192 MiB of staging per slot
     }
-    // small calls still get >= 4 chunks (64 KiB per strip at least) so the
-    // D2H of one chunk overlaps the H2D of the next
-    if (g_chunk == 0) chunk = std::min<std::uint64_t>(chunk, std::max<std::uint64_t>(64 * 1024, win / 4));
+    // calls get >= 16 chunks (64 KiB per strip at least) so the D2H of one
+    // chunk overlaps the H2D of the next
+    // (PYRIT_B200_HOST_MIN_CHUNKS, default 16: the first H2D and the last D2H
+    // are the only copies nothing overlaps, so they should be small)
+    static const std::uint64_t min_chunks = [] {
+        const char* e = std::getenv("PYRIT_B200_HOST_MIN_CHUNKS");
+        const long v = e ? std::strtol(e, nullptr, 10) : 16;
+        return static_cast<std::uint64_t>(v > 0 ? v : 16);
+    }();
+    if (g_chunk == 0) chunk = std::min<std::uint64_t>(chunk, std::max<std::uint64_t>(64 * 1024, win / min_chunks));
     chunk = std::max<std::uint64_t>(chunk, 64 * 1024) & ~std::uint64_t(4095);
     if (win % 16 == 0) chunk = std::min(chunk, win);
     else chunk = std::min(chunk, win & ~std::uint64_t(15)); // tail chunk handled in byte mode
