@@ -183,6 +183,36 @@ const TunedEntry* find_tuned(const std::string& key) {
     return nullptr;
 }
 
+namespace {
+
+void hash_instrs(std::uint64_t& h, const std::vector<Instr>& v) {
+    auto mix = [&](std::uint64_t x) {
+        for (int b = 0; b < 8; ++b) {
+            h ^= (x >> (8 * b)) & 0xFF;
+            h *= 1099511628211ull;
+        }
+    };
+    mix(v.size());
+    for (const Instr& in : v) {
+        mix((std::uint64_t(in.op) << 56) ^ (std::uint64_t(in.dst) << 24) ^ (std::uint64_t(in.sym) << 8) ^ in.strip);
+        mix(in.src.size());
+        for (std::uint32_t x : in.src) mix(x);
+    }
+}
+
+std::uint64_t ir_hash_of(const Program& p) {
+    std::uint64_t h = 1469598103934665603ull;
+    hash_instrs(h, p.code);
+    for (const Program& q : p.parts) {
+        for (const auto& g : q.group_loads) hash_instrs(h, g);
+        for (const auto& g : q.group_compute) hash_instrs(h, g);
+        hash_instrs(h, q.tail);
+    }
+    return h;
+}
+
+} // namespace
+
 Program compile_program(const Field& f, TransformKind kind, const Matrix& m, const CompileOptions& opt) {
     validate_field(f);
     if (m.cols == 0) raise(Errc::InvalidArgument, "matrix has no columns");
@@ -475,6 +505,7 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
         };
         build_parts(pcse != 0);
     }
+    p.ir_hash = ir_hash_of(p);
     return p;
 }
 
@@ -666,6 +697,7 @@ std::string kernel_name(const Program& p, const KernelShape& ks) {
     } else if (p.crs)
         for (std::uint16_t x : p.matrix) fp << 'c' << x;
     for (const Program& q : p.parts) fp << q.rows << '/' << q.cse << '/' << q.stats.xors << ',';
+    fp << 'h' << p.ir_hash << ',';
     fp << ':';
     for (std::uint32_t r : p.reps) fp << r << ',';
     char name[112];
