@@ -5,6 +5,8 @@
 // D2H copy of chunk c-1 overlap on the two copy engines and the SMs.
 #include "pipeline.hpp"
 
+#include <immintrin.h>
+
 #include <cstring>
 
 #include "hostpool.hpp"
@@ -99,6 +101,37 @@ void run_host_devices(const Program& p, const std::vector<const std::uint8_t*>& 
 
 namespace {
 
+// Large host copies for the pageable staging: non-temporal (streaming)
+// stores skip the read-for-ownership of the destination lines, one of the
+// three memory passes of a plain memcpy (PYRIT_B200_NT_COPY=0 disables).
+__attribute__((target("avx512f"))) void copy_nt512(std::uint8_t* dst, const std::uint8_t* src, std::size_t n) {
+    const std::size_t head = (64 - (reinterpret_cast<std::uintptr_t>(dst) & 63)) & 63;
+    std::memcpy(dst, src, head);
+    dst += head;
+    src += head;
+    n -= head;
+    std::size_t i = 0;
+    for (; i + 256 <= n; i += 256) {
+        const __m512i a = _mm512_loadu_si512(src + i), b = _mm512_loadu_si512(src + i + 64);
+        const __m512i c = _mm512_loadu_si512(src + i + 128), d = _mm512_loadu_si512(src + i + 192);
+        _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + i), a);
+        _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + i + 64), b);
+        _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + i + 128), c);
+        _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + i + 192), d);
+    }
+    std::memcpy(dst + i, src + i, n - i);
+    _mm_sfence();
+}
+
+void host_copy(std::uint8_t* dst, const std::uint8_t* src, std::size_t n) {
+    static const bool nt = [] {
+        const char* e = std::getenv("PYRIT_B200_NT_COPY");
+        return (!e || std::atoi(e) != 0) && __builtin_cpu_supports("avx512f");
+    }();
+    if (nt && n >= (64u << 10)) copy_nt512(dst, src, n);
+    else std::memcpy(dst, src, n);
+}
+
 // strips of output i that the program stores (all, except for schedule programs)
 bool stores_strip(const Program& p, std::uint32_t i, std::uint32_t b) {
     return !p.sched || p.written[std::size_t(i) * p.field.w + b];
@@ -136,8 +169,8 @@ void run_staged(const Program& p, const std::vector<const std::uint8_t*>& host_i
         const std::uint8_t* h_out = s.hbuf + in_strips * chunk;
         host_pool().run(out_strips.size(), [&](std::size_t q) {
             const auto [i, b] = out_strips[q];
-            std::memcpy(host_out[i] + std::uint64_t(b) * strip + pd.c0, h_out + (std::uint64_t(i) * w + b) * chunk,
-                        pd.len);
+            host_copy(host_out[i] + std::uint64_t(b) * strip + pd.c0, h_out + (std::uint64_t(i) * w + b) * chunk,
+                      pd.len);
         });
         pd.live = false;
     };
@@ -152,7 +185,7 @@ void run_staged(const Program& p, const std::vector<const std::uint8_t*>& host_i
             unpack(si); // the slot's previous chunk is done (H2D, kernel, D2H)
             host_pool().run(in_strips, [&](std::size_t q) {
                 const std::uint64_t j = q / w, b = q % w;
-                std::memcpy(s.hbuf + q * chunk, host_in[j] + b * strip + c0, len);
+                host_copy(s.hbuf + q * chunk, host_in[j] + b * strip + c0, len);
             });
             check_cuda(cudaMemcpy2DAsync(s.buf, chunk, s.hbuf, chunk, len, in_strips, cudaMemcpyHostToDevice, s.stream),
                        "H2D");
