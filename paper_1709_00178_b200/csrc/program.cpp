@@ -471,8 +471,9 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
         // same pairs; sharing them within one output's rows (short-lived
         // temporaries) pays: (60,20) GF(2^6) parity code 1.57x
         // (profiles/r01_s3/cse/); for the embedding codes it does not
-        const bool parity_cse = !emb && !crs && pcse < 0;
-        if (pcse < 0) pcse = parity_cse ? 1 : 0;
+        const bool parity = !emb && !crs;
+        if (pcse < 0) pcse = parity ? 1 : 0;
+        const bool parity_cse = parity && pcse;
         auto build_parts = [&](bool cse) {
             p.parts.clear();
             p.part_row0.clear();

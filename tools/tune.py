@@ -79,7 +79,7 @@ def main():
         outs = [out[i].data_ptr() for i in range(len(order))]
     moved = (len(ins) + len(outs)) * sym
     ref = None
-    knobs = ("MODE", "COPY", "PARTS", "PART_GROUP", "PART_CSE", "PART_TEMPS", "THREADS", "LANES", "CSE_WINDOW")
+    knobs = ("MODE", "COPY", "PARTS", "PART_GROUP", "PART_CSE", "PART_TEMPS", "THREADS", "LANES", "CSE_WINDOW", "WS")
     specs = a.variants.split(";")
     plans, graphs, times, clocks = {}, {}, {sp: [] for sp in specs}, {}
     for rnd in range(a.rounds):
