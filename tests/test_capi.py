@@ -97,6 +97,9 @@ def test_tuned_table_entries_match_current_plan_keys():
         wl = WORKLOADS[cfg]
         plan = P.Plan.encode(wl.code) if wl.op == "encode" else P.Plan.decode(wl.code, wl.erased)
         current.add(plan.key())
+    # the paper's large GF(2^6) codes (Fig. 2/3): (60,40) embedding and (60,20) parity
+    for k, r, t in ((40, 20, 0), (20, 40, 1)):
+        current.add(P.Plan.encode(P.CodeSpec(k, r, P.FieldSpec.gf64_esp(), P.TransformKind(t))).key())
     assert keys <= current, keys - current  # no stale rows (representatives changed)
 
 
