@@ -66,3 +66,29 @@ def test_large_code_encode_and_repair(cuda):
     P.decode(full, erased, code)
     torch.cuda.synchronize()
     assert torch.equal(full, ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("f,k,r,kind", [
+    (P.FieldSpec.gf16_aop(), 12, 4, 0), (P.FieldSpec.gf16_aop(), 8, 8, 0), (P.FieldSpec.gf16_aop(), 4, 12, 1),
+    (P.FieldSpec.gf64_esp(), 48, 16, 0), (P.FieldSpec.gf64_esp(), 16, 48, 1)])
+def test_maximum_length_codes(cuda, f, k, r, kind):
+    """k + r = 2^w, the largest code each field admits (matrix.hpp:27-30): encode, and decode of r
+    erasures spread over data and parity."""
+    import torch
+    code = P.CodeSpec(k, r, f, P.TransformKind(kind))
+    strip = 16 * 300
+    data = np.random.default_rng(k * 100 + r).integers(0, 256, (k, f.w * strip), dtype=np.uint8)
+    m = P.cauchy_parity_matrix(code)
+    want = np.stack(O.ring_replay(ofield(f), m, list(data), strip, kind=kind))
+    d = torch.from_numpy(data).to(cuda)
+    parity = P.encode(d, code)
+    torch.cuda.synchronize()
+    assert np.array_equal(parity.cpu().numpy(), want)
+    full = torch.cat([d, parity])
+    ref = full.clone()
+    erased = sorted(np.random.default_rng(r).choice(k + r, size=r, replace=False).tolist())
+    full[erased] = 0
+    P.decode(full, erased, code)
+    torch.cuda.synchronize()
+    assert torch.equal(full, ref)
