@@ -266,6 +266,8 @@ int pyrit_set_kernel_dir(const char* dir);
 /* name and geometry of this thread's most recent generated-kernel launch */
 int pyrit_cu_last_launch(char* kernel, size_t cap, uint32_t* blocks, uint32_t* threads);
 uint64_t pyrit_jit_compiles(void);
+/* which NVRTC compiles kernels that are not prebuilt: "nvrtc 12.9 (<file>)" */
+int pyrit_jit_info(char* buf, size_t cap);
 uint64_t pyrit_kernel_launches(void);
 
 #if defined(__GNUC__)

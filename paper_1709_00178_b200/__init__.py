@@ -167,6 +167,13 @@ class XorSchedule:
         self.ops = np.ascontiguousarray(self.ops, dtype=OP_DTYPE)
 
 
+def jit_info() -> str:
+    """Which NVRTC compiles kernels that are not prebuilt, e.g. 'nvrtc 12.9 (/usr/local/cuda/lib64/libnvrtc.so.12)'."""
+    buf = C.create_string_buffer(512)
+    L.check(_clib().pyrit_jit_info(buf, 512))
+    return buf.value.decode()
+
+
 def _ptr_array(ptrs):
     return (C.c_void_p * max(len(ptrs), 1))(*ptrs)
 

@@ -56,7 +56,7 @@ EXPORTS = (
     "pyrit_cu_encode_batch", "pyrit_cu_decode_batch", "pyrit_crc32", "pyrit_header_serialize", "pyrit_header_parse",
     "pyrit_field_id", "pyrit_field_from_id", "pyrit_shard_path", "pyrit_encode_file", "pyrit_decode_file",
     "pyrit_set_file_chunk", "pyrit_cu_encode_crs", "pyrit_encode_crs_host", "pyrit_encode_host_devices",
-    "pyrit_decode_host_devices", "pyrit_plan_from_schedule", "pyrit_apply_host",
+    "pyrit_decode_host_devices", "pyrit_plan_from_schedule", "pyrit_apply_host", "pyrit_jit_info",
 )
 
 HEADER_SIZE = 29
@@ -135,6 +135,7 @@ def load():
     lib.pyrit_set_file_chunk.argtypes = [u64]
     lib.pyrit_plan_from_schedule.argtypes = [P(pyrit_field), u32, u32, vp, C.c_size_t, vp, P(vp)]
     lib.pyrit_apply_host.argtypes = [vp, vp, vp, u64, u64, u64, i32]
+    lib.pyrit_jit_info.argtypes = [vp, C.c_size_t]
     _lib = lib
     return lib
 

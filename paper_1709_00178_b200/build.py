@@ -56,7 +56,7 @@ def build_library(force=False) -> str:
         o = os.path.join(BUILD, src + ".o")
         if force or _stale(o, [s] + hdrs):
             _run(["g++", "-std=c++20", "-O2", "-g", "-fPIC", "-fvisibility=hidden", "-Wall", "-Wextra",
-                  f"-I{CUDA}/include", "-c", s, "-o", o])
+                  f"-I{CUDA}/include", f'-DPYRIT_NVRTC_PATH="{CUDA}/lib64/libnvrtc.so.12"', "-c", s, "-o", o])
         objs.append(o)
     for src in CUDA_SOURCES:
         s = os.path.join(CSRC, src)
@@ -66,8 +66,8 @@ def build_library(force=False) -> str:
                   "-Xptxas", "-v", "-c", s, "-o", o])
         objs.append(o)
     if force or _stale(LIB, objs):
-        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static", f"-L{CUDA}/lib64", "-lnvrtc",
-              "-Xlinker", f"-rpath,{CUDA}/lib64", "-Xlinker", "--exclude-libs,ALL", "-ldl", "-lpthread", "-lrt"])
+        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static", f"-L{CUDA}/lib64",
+              "-Xlinker", "--exclude-libs,ALL", "-ldl", "-lpthread", "-lrt"])
     return LIB
 
 

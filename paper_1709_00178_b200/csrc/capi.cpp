@@ -749,6 +749,16 @@ int pyrit_cu_last_launch(char* kernel, size_t cap, uint32_t* blocks, uint32_t* t
     });
 }
 
+int pyrit_jit_info(char* buf, size_t cap) {
+    return guarded([&] {
+        if (!buf || !cap) raise(Errc::InvalidArgument, "null buffer");
+        const std::string s = jit_info();
+        const size_t n = std::min(cap - 1, s.size());
+        std::memcpy(buf, s.data(), n);
+        buf[n] = 0;
+    });
+}
+
 uint64_t pyrit_jit_compiles(void) { return jit_compiles(); }
 uint64_t pyrit_kernel_launches(void) { return kernel_launches(); }
 

@@ -14,6 +14,7 @@
 #include <iterator>
 #include <mutex>
 #include <unordered_map>
+#include <type_traits>
 #include <vector>
 
 namespace pyrit_b200 {
@@ -137,28 +138,99 @@ void write_cache(const std::string& dir, const std::string& name, const std::vec
     if (ec) std::filesystem::remove(tmp, ec);
 }
 
+// NVRTC, loaded by path from the toolkit the library was built with.  A
+// process resolves the soname libnvrtc.so.12 to whichever copy was loaded
+// first -- in a torch process that is torch's bundled (older) NVRTC, whose
+// code measured 4.5% slower on config 4 than the toolkit's
+// (profiles/r01_s3/jit/).  Opening the toolkit's file explicitly
+// (RTLD_LOCAL | RTLD_DEEPBIND) gives the same compiler as the prebuilt
+// kernels in every process; PYRIT_B200_NVRTC names another file, and the
+// plain soname is the fallback.
+struct Nvrtc {
+    void* handle = nullptr;
+    std::string path;
+    nvrtcResult (*create)(nvrtcProgram*, const char*, const char*, int, const char* const*, const char* const*) = nullptr;
+    nvrtcResult (*compile)(nvrtcProgram, int, const char* const*) = nullptr;
+    nvrtcResult (*log_size)(nvrtcProgram, size_t*) = nullptr;
+    nvrtcResult (*log)(nvrtcProgram, char*) = nullptr;
+    nvrtcResult (*cubin_size)(nvrtcProgram, size_t*) = nullptr;
+    nvrtcResult (*cubin)(nvrtcProgram, char*) = nullptr;
+    nvrtcResult (*destroy)(nvrtcProgram*) = nullptr;
+    const char* (*error)(nvrtcResult) = nullptr;
+    nvrtcResult (*version)(int*, int*) = nullptr;
+};
+
+#ifndef PYRIT_NVRTC_PATH
+#define PYRIT_NVRTC_PATH "libnvrtc.so.12"
+#endif
+
+const Nvrtc& nvrtc() {
+    static std::once_flag once;
+    static Nvrtc n;
+    std::call_once(once, [] {
+        std::vector<std::string> tries;
+        if (const char* e = std::getenv("PYRIT_B200_NVRTC"); e && *e) tries.emplace_back(e);
+        tries.emplace_back(PYRIT_NVRTC_PATH);
+        tries.emplace_back("libnvrtc.so.12");
+        for (const std::string& t : tries) {
+            n.handle = dlopen(t.c_str(), RTLD_NOW | RTLD_LOCAL | RTLD_DEEPBIND);
+            if (n.handle) {
+                n.path = t;
+                break;
+            }
+        }
+        if (!n.handle) return;
+        auto sym = [&](const char* name, auto& fn) { fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(n.handle, name)); };
+        sym("nvrtcCreateProgram", n.create);
+        sym("nvrtcCompileProgram", n.compile);
+        sym("nvrtcGetProgramLogSize", n.log_size);
+        sym("nvrtcGetProgramLog", n.log);
+        sym("nvrtcGetCUBINSize", n.cubin_size);
+        sym("nvrtcGetCUBIN", n.cubin);
+        sym("nvrtcDestroyProgram", n.destroy);
+        sym("nvrtcGetErrorString", n.error);
+        sym("nvrtcVersion", n.version);
+    });
+    if (!n.handle || !n.create || !n.compile || !n.cubin || !n.cubin_size || !n.destroy || !n.error)
+        throw CudaFailure(-1000, "NVRTC (libnvrtc.so.12) could not be loaded: kernels that are not prebuilt cannot be "
+                                 "compiled");
+    return n;
+}
+
+// "nvrtc12.9": the compiler version in cache file names
+std::string nvrtc_tag() {
+    static const std::string tag = [] {
+        const Nvrtc& n = nvrtc();
+        int major = 0, minor = 0;
+        if (n.version) n.version(&major, &minor);
+        return "nvrtc" + std::to_string(major) + "." + std::to_string(minor);
+    }();
+    return tag;
+}
+
 std::vector<char> nvrtc_compile(const std::string& src, const std::string& name) {
+    const Nvrtc& rt = nvrtc();
     nvrtcProgram prog;
     auto chk = [&](nvrtcResult r, const char* what) {
         if (r != NVRTC_SUCCESS)
-            throw CudaFailure(-1000 - static_cast<int>(r), std::string(what) + ": " + nvrtcGetErrorString(r));
+            throw CudaFailure(-1000 - static_cast<int>(r), std::string(what) + ": " + rt.error(r));
     };
-    chk(nvrtcCreateProgram(&prog, src.c_str(), (name + ".cu").c_str(), 0, nullptr, nullptr), "nvrtcCreateProgram");
+    chk(rt.create(&prog, src.c_str(), (name + ".cu").c_str(), 0, nullptr, nullptr), "nvrtcCreateProgram");
     const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "-DNDEBUG"};
-    const nvrtcResult rc = nvrtcCompileProgram(prog, 4, opts);
+    const nvrtcResult rc = rt.compile(prog, 4, opts);
     if (rc != NVRTC_SUCCESS) {
         size_t n = 0;
-        nvrtcGetProgramLogSize(prog, &n);
+        rt.log_size(prog, &n);
         std::string log(n, '\0');
-        nvrtcGetProgramLog(prog, log.data());
-        nvrtcDestroyProgram(&prog);
+        rt.log(prog, log.data());
+        rt.destroy(&prog);
         throw CudaFailure(-1000 - static_cast<int>(rc), "NVRTC failed for " + name + ":\n" + log);
     }
     size_t n = 0;
-    chk(nvrtcGetCUBINSize(prog, &n), "nvrtcGetCUBINSize");
+    chk(rt.cubin_size(prog, &n), "nvrtcGetCUBINSize");
     std::vector<char> cubin(n);
-    chk(nvrtcGetCUBIN(prog, cubin.data()), "nvrtcGetCUBIN");
-    nvrtcDestroyProgram(&prog);
+    chk(rt.cubin(prog, cubin.data()), "nvrtcGetCUBIN");
+    rt.destroy(&prog);
     ++g_jit;
     return cubin;
 }
@@ -174,10 +246,12 @@ LoadedKernel load_kernel(const Program& p, const KernelShape& ks, int device) {
     // prebuilt (next to the library), else the on-disk JIT cache, else NVRTC
     std::vector<char> cubin = read_file(kernel_dir() + "/" + name + ".cubin");
     const std::string cache = jit_cache_dir();
-    if (cubin.empty() && !cache.empty()) cubin = read_file(cache + "/" + name + ".cubin");
+    // cached cubins are keyed by the compiler too: one from another NVRTC is not reused
+    const std::string cname = cache.empty() || !cubin.empty() ? std::string() : name + "." + nvrtc_tag();
+    if (cubin.empty() && !cache.empty()) cubin = read_file(cache + "/" + cname + ".cubin");
     if (cubin.empty()) {
         cubin = nvrtc_compile(generate_cuda(p, ks), name);
-        if (!cache.empty()) write_cache(cache, name, cubin);
+        if (!cache.empty()) write_cache(cache, cname, cubin);
     }
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_kernels.find(key);
@@ -243,6 +317,13 @@ std::string kernel_dir() {
         g_kernel_dir = env ? env : default_kernel_dir();
     }
     return g_kernel_dir;
+}
+
+std::string jit_info() {
+    const Nvrtc& n = nvrtc();
+    int major = 0, minor = 0;
+    if (n.version) n.version(&major, &minor);
+    return "nvrtc " + std::to_string(major) + "." + std::to_string(minor) + " (" + n.path + ")";
 }
 
 std::uint64_t jit_compiles() { return g_jit.load(); }

@@ -121,3 +121,17 @@ def test_null_arguments_are_errors_not_crashes():
     assert lib.pyrit_decode_file(None, 1, b"out", 0) == inv
     assert lib.pyrit_cu_apply(None, None, None, 16, 0, 16, None) == inv
     assert lib.pyrit_cu_apply_batch(None, None, None, 16, 0, 16, 1, 0, 0, None) == inv
+
+
+def test_jit_uses_the_toolkit_nvrtc_even_after_another_was_loaded():
+    """A torch process may already hold its own (older) libnvrtc.so.12; kernels that are not prebuilt
+    must still be compiled by the toolkit NVRTC the prebuilt ones came from (profiles/r01_s3/jit/)."""
+    import glob
+    import subprocess
+    import sys
+    others = [p for p in glob.glob(os.path.join(os.path.dirname(np.__file__), "..", "nvidia", "cuda_nvrtc", "lib",
+                                                "libnvrtc.so.12"))]
+    pre = f"import ctypes; ctypes.CDLL({others[0]!r}, mode=ctypes.RTLD_GLOBAL); " if others else ""
+    code = pre + "import paper_1709_00178_b200 as P; print(P.jit_info())"
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT, check=True).stdout
+    assert out.startswith("nvrtc 12.") and "/usr/local/cuda" in out, out
