@@ -140,6 +140,13 @@ def cpu_baseline(wl, steps=None, warmup=1, budget_s=12.0, sample_frag=None):
             break
         if steps is None and (time.perf_counter() - t_start > budget_s or n >= 50):
             break
+    # one thread as well (T = hardware threads and T = 1), a few runs
+    t1 = []
+    if steps is None:
+        for _ in range(3):
+            t0 = time.perf_counter()
+            plan.run(1)
+            t1.append(time.perf_counter() - t0)
     plan.close()
     src = wl.k * frag
     t = statistics.median(times)
@@ -147,7 +154,8 @@ def cpu_baseline(wl, steps=None, warmup=1, budget_s=12.0, sample_frag=None):
              1: "CRS bitmatrix schedule (compile_crs_schedule + parallel_replay)",
              2: "decode_matrix + CRS parallel_replay, then CRS parity rows (decode() restated)",
              3: "decode_matrix + ring parallel_replay, then ring parity rows (decode())"}
-    return {"value": src / t / 1e9, "unit": "GB/s", "cores": threads, "kind": kind,
+    extra = {"value_1_thread": src / min(t1) / 1e9} if t1 else {}
+    return {"value": src / t / 1e9, "unit": "GB/s", "cores": threads, "kind": kind, **extra,
             "sample": f"{wl.k}x{frag}-byte fragments ({src / 2**20:.0f} MiB source) of the {wl.name} shape, "
                       f"{names[mode]}, {threads} threads, median of {len(times)} runs",
             "times_s": [round(x, 5) for x in times]}
