@@ -155,6 +155,8 @@ def cpu_baseline(wl, steps=None, warmup=1, budget_s=12.0, sample_frag=None):
              2: "decode_matrix + CRS parallel_replay, then CRS parity rows (decode() restated)",
              3: "decode_matrix + ring parallel_replay, then ring parity rows (decode())"}
     extra = {"value_1_thread": src / min(t1) / 1e9} if t1 else {}
+    # the reference bench's own convention counts (k + r) * F bytes (bench.hpp:205-207)
+    extra["value_kr_convention"] = (wl.k + wl.m) * frag / t / 1e9
     return {"value": src / t / 1e9, "unit": "GB/s", "cores": threads, "kind": kind, **extra,
             "sample": f"{wl.k}x{frag}-byte fragments ({src / 2**20:.0f} MiB source) of the {wl.name} shape, "
                       f"{names[mode]}, {threads} threads, median of {len(times)} runs",
