@@ -135,3 +135,16 @@ def test_jit_uses_the_toolkit_nvrtc_even_after_another_was_loaded():
     code = pre + "import paper_1709_00178_b200 as P; print(P.jit_info())"
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT, check=True).stdout
     assert out.startswith("nvrtc 12.") and "/usr/local/cuda" in out, out
+
+
+def test_header_is_plain_c(tmp_path):
+    """include/pyrit_b200.h compiles as C11 with warnings as errors, and a C program links and runs
+    against the library (host-side entry points only)."""
+    exe = tmp_path / "c_header_check"
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "c_header_check.c"), "-o", str(exe),
+                    "-L", os.path.dirname(L.LIB_PATH), "-lpyrit_b200", f"-Wl,-rpath,{os.path.dirname(L.LIB_PATH)}"],
+                   check=True, capture_output=True, text=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0, (out.returncode, out.stderr)
+    assert "sm_100a" in out.stdout
