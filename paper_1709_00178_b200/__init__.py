@@ -183,6 +183,7 @@ class Plan:
 
     def __init__(self, handle: C.c_void_p, survivors=None, outputs=None):
         self._h = handle
+        self.slots = None
         self.survivors = survivors
         self.outputs = outputs
 
@@ -204,7 +205,9 @@ class Plan:
         L.check(_clib().pyrit_plan_from_schedule(C.byref(sched.spec.c()), sched.k, sched.outputs,
                                                 sched.ops.ctypes.data, len(sched.ops),
                                                 None if lab is None else lab.ctypes.data, C.byref(h)))
-        return cls(h)
+        plan = cls(h)
+        plan.slots = (sched.k, sched.outputs)  # in[] / out[] are indexed by slot for these plans
+        return plan
 
     @classmethod
     def encode(cls, code: CodeSpec) -> "Plan":
@@ -252,15 +255,31 @@ class Plan:
         """Run the compiled program on host arrays (compiler verification only)."""
         st = self.stats()
         length = strip - off if length is None else length
+        n_in, n_out = getattr(self, "slots", None) or (st["cols"], st["rows"])
+        if len(ins) < n_in:
+            raise PyritError(4, f"{n_in} input symbols expected")
         if outs is None:
-            outs = [np.zeros(len(ins[0]), dtype=np.uint8) for _ in range(st["rows"])]
+            outs = [np.zeros(len(ins[0]), dtype=np.uint8) for _ in range(n_out)]
+        if len(outs) < n_out:
+            raise PyritError(4, f"{n_out} output symbols expected")
         L.check(_clib().pyrit_plan_interpret(self._h, _ptr_array([a.ctypes.data for a in ins]),
                                             _ptr_array([a.ctypes.data for a in outs]), strip, off, length))
         return list(outs)
 
+    def _counts(self, ins, outs) -> None:
+        """The C ABI reads in[]/out[] by slot count: refuse short pointer lists here."""
+        if self.slots is None:
+            st = self.stats()
+            n_in, n_out = st["cols"], st["rows"]
+        else:
+            n_in, n_out = self.slots
+        if len(ins) < n_in or len(outs) < n_out:
+            raise PyritError(4, f"{n_in} input and {n_out} output symbols expected")
+
     def apply(self, in_ptrs: Sequence[int], out_ptrs: Sequence[int], strip: int, off: int = 0,
               length: int | None = None, stream: int | None = None) -> None:
         """replay (codec.hpp:118) over device pointers, asynchronously on `stream`."""
+        self._counts(in_ptrs, out_ptrs)
         length = strip - off if length is None else length
         L.check(_clib().pyrit_cu_apply(self._h, _ptr_array(list(in_ptrs)), _ptr_array(list(out_ptrs)), strip, off,
                                       length, stream))
@@ -268,6 +287,7 @@ class Plan:
     def apply_host(self, ins: Sequence[np.ndarray], outs: Sequence[np.ndarray], strip: int, off: int = 0,
                    length: int | None = None, device: int = 0) -> None:
         """replay over HOST symbols (numpy uint8, w strips each): H2D, kernel, D2H inside; synchronous."""
+        self._counts(ins, outs)
         length = strip - off if length is None else length
         L.check(_clib().pyrit_apply_host(self._h, _ptr_array([a.ctypes.data for a in ins]),
                                         _ptr_array([a.ctypes.data for a in outs]), strip, off, length, device))
@@ -284,6 +304,7 @@ class Plan:
                     in_pitch: int, out_pitch: int, off: int = 0, length: int | None = None,
                     stream: int | None = None) -> None:
         """`stripes` stripes in one launch: input j of stripe b at in_ptrs[j] + b * in_pitch."""
+        self._counts(in_ptrs, out_ptrs)
         length = strip - off if length is None else length
         L.check(_clib().pyrit_cu_apply_batch(self._h, _ptr_array(list(in_ptrs)), _ptr_array(list(out_ptrs)), strip,
                                             off, length, stripes, in_pitch, out_pitch, stream))
