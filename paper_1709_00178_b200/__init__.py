@@ -339,6 +339,10 @@ def _replay_checks(sched: XorSchedule, inp, in_map, out, out_map, offset, length
         raise PyritError(4, "replay: slot map sizes do not match schedule")
     if inp.shape[1] != out.shape[1] or inp.shape[1] % sched.spec.w:
         raise PyritError(4, "replay: field mismatch")
+    for t in (inp, out):  # every symbol's strips must be contiguous bytes (SymbolBuffer layout)
+        unit = t.stride(1) if hasattr(t, "stride") and callable(t.stride) else t.strides[1]
+        if unit != 1 or str(t.dtype) not in ("torch.uint8", "uint8"):
+            raise PyritError(4, "replay: symbols must be uint8 rows with contiguous bytes")
     strip = inp.shape[1] // sched.spec.w
     length = strip - offset if length is None else length
     if offset + length > strip:
@@ -411,6 +415,8 @@ def decode(symbols, erased: Iterable[int], code: CodeSpec) -> None:
     import torch
     if symbols.dim() != 2 or symbols.shape[0] != code.k + code.r or symbols.dtype != torch.uint8:
         raise PyritError(4, "symbol buffer does not match the code")
+    if not symbols.is_cuda or symbols.stride(1) != 1:
+        raise PyritError(4, "symbols must be CUDA rows with contiguous bytes (repaired in place)")
     er = np.asarray(list(erased), dtype=np.uint32)
     L.check(_clib().pyrit_cu_decode(C.byref(code.c()), _ptr_array(_rows(symbols)), er.ctypes.data, er.size,
                                    symbols.shape[1], _stream_of(symbols)))
@@ -425,6 +431,8 @@ def encode_host(data: np.ndarray, code: CodeSpec, device: int = 0, parity: np.nd
         raise PyritError(4, "data buffer does not match the code")
     if parity is None:
         parity = np.empty((code.r, data.shape[1]), dtype=np.uint8)
+    elif parity.shape != (code.r, data.shape[1]) or parity.dtype != np.uint8 or not parity.flags.c_contiguous:
+        raise PyritError(4, "parity buffer does not match the code")
     if devices:
         dv = np.asarray(list(devices), dtype=np.int32)
         L.check(_clib().pyrit_encode_host_devices(C.byref(code.c()), data.ctypes.data, parity.ctypes.data,
