@@ -2,17 +2,19 @@
 // top-level calls, written against the reference's OWN types.
 //
 //   pyrit::encode(data, code, threads)          codec.hpp:212-220
-//     -> pyrit::cuda::encode(data, code, device)
+//     -> pyrit::cuda::encode(data, code, threads)   (or (data, code, Device{id}))
 //   pyrit::decode(symbols, erased, code, threads) codec.hpp:241-284
-//     -> pyrit::cuda::decode(symbols, erased, code, device)
+//     -> pyrit::cuda::decode(symbols, erased, code, threads)
 //   pyrit::encode_file(input, out_dir, code, symbol_size) container.hpp:168-222
-//     -> pyrit::cuda::encode_file(input, out_dir, code, symbol_size, device)
+//     -> pyrit::cuda::encode_file(input, out_dir, code, symbol_size)
 //   pyrit::decode_file(shard_paths, output)      container.hpp:249-299
-//     -> pyrit::cuda::decode_file(shard_paths, output, device)
+//     -> pyrit::cuda::decode_file(shard_paths, output)
 //   pyrit::parallel_replay(sched, in, in_map, out, out_map, threads)  codec.hpp:176-193
-//     -> pyrit::cuda::parallel_replay(sched, in, in_map, out, out_map, device)
+//     -> pyrit::cuda::parallel_replay(sched, in, in_map, out, out_map, threads)
 //   pyrit::replay(sched, in, in_map, out, out_map, ws, offset, len)   codec.hpp:118-157
-//     -> pyrit::cuda::replay(sched, in, in_map, out, out_map, offset, len, device)
+//     -> pyrit::cuda::replay(sched, in, in_map, out, out_map, ws, offset, len)
+// Same arguments with the same meaning: switching is a namespace change.  The
+// device is pyrit::cuda::set_device(id) (default 0) or a trailing Device{id}.
 //
 // Include after the reference headers (it needs SymbolBuffer, CodeSpec,
 // Error from proj/include/pyrit/) and link libpyrit_b200.so.  Validation and
@@ -37,6 +39,20 @@
 
 namespace pyrit::cuda {
 
+// Device selection.  The drop-ins keep the reference's signatures exactly --
+// including the trailing `unsigned threads` of encode/decode/parallel_replay,
+// which the GPU path accepts and ignores -- so the device comes from
+// set_device() (per host thread, default 0) or from an explicit Device{id}
+// argument in the overloads that take one.
+struct Device {
+    int id = 0;
+};
+inline int& current_device() {
+    static thread_local int d = 0;
+    return d;
+}
+inline void set_device(int id) { current_device() = id; }
+
 inline pyrit_code to_c(const CodeSpec& code) {
     pyrit_code c{};
     c.k = code.k;
@@ -60,44 +76,54 @@ inline void check(int rc) {
 
 // codec.hpp:212 encode(): parity = C * data, on the GPU (host buffers in,
 // host buffers out; H2D, fused ring kernel and D2H are pipelined inside).
-inline SymbolBuffer encode(const SymbolBuffer& data, const CodeSpec& code, int device = 0) {
+inline SymbolBuffer encode(const SymbolBuffer& data, const CodeSpec& code, Device device) {
     check_data_shape(data, code); // codec.hpp:205-209, the reference's own validation
     SymbolBuffer parity(code.r, data.symbol_size(), code.field);
     const pyrit_code c = to_c(code);
-    if (code.r) check(pyrit_encode_host(&c, data.symbol(0), parity.symbol(0), data.symbol_size(), device));
+    if (code.r) check(pyrit_encode_host(&c, data.symbol(0), parity.symbol(0), data.symbol_size(), device.id));
     return parity;
+}
+inline SymbolBuffer encode(const SymbolBuffer& data, const CodeSpec& code, unsigned /*threads*/ = 1) {
+    return encode(data, code, Device{current_device()});
 }
 
 // codec.hpp:223 encode_crs(): the bitmatrix baseline codec on the GPU, same
 // parity bytes as encode() (host buffers, like encode above).
-inline SymbolBuffer encode_crs(const SymbolBuffer& data, const CodeSpec& code, int device = 0) {
+inline SymbolBuffer encode_crs(const SymbolBuffer& data, const CodeSpec& code, Device device) {
     check_data_shape(data, code);
     SymbolBuffer parity(code.r, data.symbol_size(), code.field);
     const pyrit_code c = to_c(code);
-    if (code.r) check(pyrit_encode_crs_host(&c, data.symbol(0), parity.symbol(0), data.symbol_size(), device));
+    if (code.r) check(pyrit_encode_crs_host(&c, data.symbol(0), parity.symbol(0), data.symbol_size(), device.id));
     return parity;
+}
+inline SymbolBuffer encode_crs(const SymbolBuffer& data, const CodeSpec& code, unsigned /*threads*/ = 1) {
+    return encode_crs(data, code, Device{current_device()});
 }
 
 // codec.hpp:241 decode(): in-place repair of the listed symbols from any k
 // survivors (lowest index first), one fused pass on the GPU.
 inline void decode(SymbolBuffer& symbols, const std::vector<unsigned>& erased, const CodeSpec& code,
-                   int device = 0) {
+                   Device device) {
     validate_code(code);
     if (!(symbols.spec() == code.field) || symbols.symbols() != code.k + code.r)
         raise(Errc::BufferShape, "symbol buffer does not match the code");
     const pyrit_code c = to_c(code);
     std::vector<std::uint32_t> er(erased.begin(), erased.end());
     check(pyrit_decode_host(&c, symbols.symbol(0), er.data(), static_cast<std::uint32_t>(er.size()),
-                            symbols.symbol_size(), device));
+                            symbols.symbol_size(), device.id));
+}
+inline void decode(SymbolBuffer& symbols, const std::vector<unsigned>& erased, const CodeSpec& code,
+                   unsigned /*threads*/ = 1) {
+    decode(symbols, erased, code, Device{current_device()});
 }
 
 // container.hpp:168 encode_file(): same shard files (names, 29-byte headers,
 // stripe layout) as the reference; stripes go through the GPU in batches.
 inline std::vector<std::filesystem::path> encode_file(const std::filesystem::path& input,
                                                       const std::filesystem::path& out_dir, const CodeSpec& code,
-                                                      std::uint32_t symbol_size, int device = 0) {
+                                                      std::uint32_t symbol_size, Device device = Device{current_device()}) {
     const pyrit_code c = to_c(code);
-    check(pyrit_encode_file(&c, input.c_str(), out_dir.c_str(), symbol_size, device));
+    check(pyrit_encode_file(&c, input.c_str(), out_dir.c_str(), symbol_size, device.id));
     std::vector<std::filesystem::path> paths;
     char buf[4096];
     for (unsigned i = 0; i < code.k + code.r; ++i) {
@@ -109,10 +135,10 @@ inline std::vector<std::filesystem::path> encode_file(const std::filesystem::pat
 
 // container.hpp:249 decode_file(): rebuild the original file from any k shards.
 inline void decode_file(const std::vector<std::filesystem::path>& shard_paths, const std::filesystem::path& output,
-                        int device = 0) {
+                        Device device = Device{current_device()}) {
     std::vector<const char*> ps;
     for (const auto& p : shard_paths) ps.push_back(p.c_str());
-    check(pyrit_decode_file(ps.data(), static_cast<std::uint32_t>(ps.size()), output.c_str(), device));
+    check(pyrit_decode_file(ps.data(), static_cast<std::uint32_t>(ps.size()), output.c_str(), device.id));
 }
 
 // The operator level: any XorSchedule (compile_schedule, compile_crs_schedule
@@ -126,7 +152,7 @@ static_assert(sizeof(XorOp) == sizeof(pyrit_xor_op) && offsetof(XorOp, mode) == 
 
 inline void replay(const XorSchedule& sched, const SymbolBuffer& in, std::span<const unsigned> in_map,
                    SymbolBuffer& out, std::span<const unsigned> out_map, std::size_t offset, std::size_t len,
-                   int device = 0) {
+                   Device device) {
     // codec.hpp:122-127, the reference's own checks
     if (in_map.size() != sched.k || out_map.size() != sched.outputs)
         raise(Errc::BufferShape, "replay: slot map sizes do not match schedule");
@@ -159,13 +185,27 @@ inline void replay(const XorSchedule& sched, const SymbolBuffer& in, std::span<c
     pyrit_plan* plan = nullptr;
     check(pyrit_plan_from_schedule(&f, sched.k, sched.outputs, reinterpret_cast<const pyrit_xor_op*>(ops.data()),
                                    ops.size(), labels.data(), &plan));
-    const int rc = pyrit_apply_host(plan, ip.data(), op.data(), in.packet_size(), offset, len, device);
+    const int rc = pyrit_apply_host(plan, ip.data(), op.data(), in.packet_size(), offset, len, device.id);
     pyrit_plan_destroy(plan);
     check(rc);
 }
 
+// codec.hpp:118 signature: the Workspace is accepted for drop-in compatibility;
+// on the GPU the scratch packets live in registers and start at zero for every
+// call (the reference's schedules never read scratch before writing it)
+inline void replay(const XorSchedule& sched, const SymbolBuffer& in, std::span<const unsigned> in_map,
+                   SymbolBuffer& out, std::span<const unsigned> out_map, Workspace& /*ws*/, std::size_t offset,
+                   std::size_t len) {
+    replay(sched, in, in_map, out, out_map, offset, len, Device{current_device()});
+}
+
+// codec.hpp:176 signature (threads: the reference's host threads, unused here)
 inline void parallel_replay(const XorSchedule& sched, const SymbolBuffer& in, std::span<const unsigned> in_map,
-                            SymbolBuffer& out, std::span<const unsigned> out_map, int device = 0) {
+                            SymbolBuffer& out, std::span<const unsigned> out_map, unsigned /*threads*/ = 1) {
+    replay(sched, in, in_map, out, out_map, 0, in.packet_size(), Device{current_device()});
+}
+inline void parallel_replay(const XorSchedule& sched, const SymbolBuffer& in, std::span<const unsigned> in_map,
+                            SymbolBuffer& out, std::span<const unsigned> out_map, Device device) {
     replay(sched, in, in_map, out, out_map, 0, in.packet_size(), device);
 }
 

@@ -48,7 +48,11 @@ int main() {
         fill(data, c.k * 1000 + c.r);
         const SymbolBuffer want = c.ring_ok ? encode(data, code, 4) : encode_crs(data, code, 4);
         const SymbolBuffer got = pyrit::cuda::encode(data, code);
-        const bool enc_ok = same(got, want) && same(pyrit::cuda::encode_crs(data, code), want);
+        // the reference's own argument lists: (data, code, threads) -- threads is a host-thread count,
+        // not a device; and an explicit device
+        const bool enc_ok = same(got, want) && same(pyrit::cuda::encode_crs(data, code), want) &&
+                            same(pyrit::cuda::encode(data, code, 4u), want) &&
+                            same(pyrit::cuda::encode(data, code, pyrit::cuda::Device{0}), want);
         // decode: erase r symbols (data and parity mixed), repair in place
         SymbolBuffer full(c.k + c.r, c.symbol_size, c.f);
         std::memcpy(full.symbol(0), data.symbol(0), c.k * c.symbol_size);
@@ -57,7 +61,7 @@ int main() {
         std::vector<unsigned> erased;
         for (unsigned i = 0; i < c.r; ++i) erased.push_back((i * 5 + 1) % (c.k + c.r));
         for (unsigned e : erased) std::memset(work.symbol(e), 0xAA, c.symbol_size);
-        pyrit::cuda::decode(work, erased, code);
+        pyrit::cuda::decode(work, erased, code, 8u);
         const bool dec_ok = same(work, full);
         std::printf("%-40s encode %s decode %s\n", c.name, enc_ok ? "OK" : "MISMATCH", dec_ok ? "OK" : "MISMATCH");
         failures += !enc_ok + !dec_ok;
@@ -93,7 +97,7 @@ int main() {
             fill(want, 9);
             std::memcpy(got.symbol(0), want.symbol(0), c.r * ss);
             parallel_replay(sched, in, in_map, want, out_map, 4);
-            pyrit::cuda::parallel_replay(sched, in, in_map, got, out_map);
+            pyrit::cuda::parallel_replay(sched, in, in_map, got, out_map, 4u);
             bool ok = same(got, want);
             // window only (replay) and in place in one buffer, decode()-style
             SymbolBuffer both(c.k + c.r, ss, c.f), both_ref(c.k + c.r, ss, c.f);
@@ -104,7 +108,8 @@ int main() {
             for (unsigned i = 0; i < c.r; ++i) om[i] = c.k + i;
             Workspace ws(sched, 64);
             replay(sched, both_ref, im, both_ref, om, ws, 128, 64);
-            pyrit::cuda::replay(sched, both, im, both, om, 128, 64);
+            Workspace ws_gpu(sched, 64);
+            pyrit::cuda::replay(sched, both, im, both, om, ws_gpu, 128, 64); // codec.hpp:118 argument list
             ok = ok && same(both, both_ref);
             std::printf("parallel_replay %-28s %s\n", c.name, ok ? "OK" : "MISMATCH");
             failures += !ok;
