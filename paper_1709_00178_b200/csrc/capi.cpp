@@ -383,6 +383,26 @@ int pyrit_plan_interpret(const pyrit_plan* plan, const uint8_t* const* in, uint8
             interpret_program(plan->prog, kin.data(), kout.data(), strip_bytes, off, len);
             return;
         }
+        // PYRIT_B200_INTERPRET_GENERIC=1: evaluate the generic kernel's bitmatrix
+        // (Program::field_masks) instead, so CPU tests pin what it computes
+        const char* gen_env = std::getenv("PYRIT_B200_INTERPRET_GENERIC");
+        if (gen_env && std::atoi(gen_env)) {
+            const Program& p = plan->prog;
+            if (p.field_masks.empty()) raise(Errc::InvalidArgument, "no generic bitmatrix for this program");
+            const std::uint32_t w = p.field.w;
+            for (std::uint32_t i = 0; i < p.rows; ++i)
+                for (std::uint32_t b = 0; b < w; ++b) {
+                    std::uint8_t* d = out[i] + std::uint64_t(b) * strip_bytes + off;
+                    std::memset(d, 0, len);
+                    for (std::uint32_t j = 0; j < p.cols; ++j)
+                        for (std::uint32_t c = 0; c < w; ++c)
+                            if ((p.field_masks[(std::size_t(i) * w + b) * p.cols + j] >> c) & 1u) {
+                                const std::uint8_t* src = in[j] + std::uint64_t(c) * strip_bytes + off;
+                                for (std::uint64_t q = 0; q < len; ++q) d[q] ^= src[q];
+                            }
+                }
+            return;
+        }
         // PYRIT_B200_INTERPRET_PARTS=1: run the output parts the staged and
         // split kernels execute (rows part_row0[r] ..) instead of the whole
         // program, so CPU tests cover the part programs too

@@ -93,3 +93,63 @@ cudaError_t launch_digest(const std::uint8_t* src, std::uint64_t len, std::uint6
 }
 
 } // namespace pyrit_b200
+
+namespace pyrit_b200 {
+
+// ---- generic bit-matrix kernel (no per-code compilation) -------------------
+//
+// Output strip b of output i = XOR over inputs j and strips c in mask(i, b, j)
+// of input strip c -- the plain-field bitmatrix form of any code this library
+// compiles (every ring program computes the GF(2^w) code, codec.hpp:444-469).
+// It runs while a code's specialised kernel is still being compiled (tiered
+// compilation, runtime.cpp) and on demand (kernel mode 3).  One 4-byte column
+// word per thread, grid-stride over (stripe, word); the masks are uniform
+// across a warp and come from the constant bank (__grid_constant__).
+__global__ void __launch_bounds__(256) generic_kernel(const __grid_constant__ GenericArgs a) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const std::uint32_t k = a.k, e = a.e, w = a.w;
+    const std::uint64_t S = a.S;
+    std::uint64_t c0 = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+    std::uint64_t b = c0 / a.nwords, cw = c0 - b * a.nwords;
+    while (b < a.nb) {
+        const std::uint64_t o = a.off + cw * 4;
+        const std::uint64_t oi = o + b * a.ibp, oo = o + b * a.obp;
+        for (std::uint32_t i = 0; i < e; ++i)
+            for (std::uint32_t r = 0; r < w; ++r) {
+                const std::uint16_t* row = &a.mask[(i * w + r) * k];
+                std::uint32_t acc = 0;
+                for (std::uint32_t j = 0; j < k; ++j) {
+                    std::uint32_t m = row[j];
+                    const std::uint8_t* p = a.ptr[j] + oi;
+                    while (m) {
+                        const std::uint32_t c = __ffs(m) - 1;
+                        m &= m - 1;
+                        acc ^= __ldg(reinterpret_cast<const std::uint32_t*>(p + c * S));
+                    }
+                }
+                __stcs(reinterpret_cast<unsigned int*>(const_cast<std::uint8_t*>(a.ptr[k + i]) + oo + r * S), acc);
+            }
+        b += a.sq;
+        cw += a.sr;
+        if (cw >= a.nwords) {
+            cw -= a.nwords;
+            ++b;
+        }
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+cudaError_t launch_generic(const GenericArgs& args, unsigned blocks, cudaStream_t stream) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(256);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, generic_kernel, args);
+}
+
+} // namespace pyrit_b200

@@ -506,6 +506,48 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
         };
         build_parts(pcse != 0);
     }
+    // the generic kernel's bitmatrix (field code: every transform computes it)
+    const bool all_written = !p.sched || std::all_of(p.written.begin(), p.written.end(), [](std::uint8_t x) { return x; });
+    if (all_written && w <= 16 && e > 0) {
+        p.field_masks.assign(std::size_t(e) * w * k, 0);
+        if (emb || p.sched) { // the GF(2^w) code itself (embedding == plain field code), or the schedule's map
+            for (std::uint32_t i = 0; i < e; ++i)
+                for (std::uint32_t j = 0; j < k; ++j) {
+                    std::uint32_t prod[16] = {};
+                    if (!p.sched)
+                        for (std::uint32_t c = 0; c < w; ++c) prod[c] = gf_mul(m.at(i, j), 1u << c, f);
+                    for (std::uint32_t b = 0; b < w; ++b) {
+                        std::uint32_t mask = 0;
+                        if (p.sched) mask = p.bits[(std::size_t(i) * k + j) * w + b];
+                        else
+                            for (std::uint32_t c = 0; c < w; ++c) mask |= ((prod[c] >> b) & 1u) << c;
+                        p.field_masks[(std::size_t(i) * w + b) * k + j] = static_cast<std::uint16_t>(mask);
+                    }
+                }
+        } else if (std::uint64_t(p.stats.xors + 1) * k * w <= (std::uint64_t(1) << 26)) {
+            // Parity transform: its own GF(2)-linear map -- read it off the program
+            // with unit inputs, 8 at a time (one per bit of a 1-byte strip)
+            const std::uint32_t units = k * w;
+            std::vector<std::vector<std::uint8_t>> in(k, std::vector<std::uint8_t>(w)), out(e, std::vector<std::uint8_t>(w));
+            std::vector<const std::uint8_t*> ip(k);
+            std::vector<std::uint8_t*> op(e);
+            for (std::uint32_t u0 = 0; u0 < units; u0 += 8) {
+                for (auto& v : in) std::fill(v.begin(), v.end(), 0);
+                for (std::uint32_t t = 0; t < 8 && u0 + t < units; ++t) in[(u0 + t) / w][(u0 + t) % w] |= 1u << t;
+                for (std::uint32_t j = 0; j < k; ++j) ip[j] = in[j].data();
+                for (std::uint32_t i = 0; i < e; ++i) op[i] = out[i].data();
+                interpret_program(p, ip.data(), op.data(), 1, 0, 1);
+                for (std::uint32_t i = 0; i < e; ++i)
+                    for (std::uint32_t b = 0; b < w; ++b)
+                        for (std::uint32_t t = 0; t < 8 && u0 + t < units; ++t)
+                            if ((out[i][b] >> t) & 1u)
+                                p.field_masks[(std::size_t(i) * w + b) * k + (u0 + t) / w] |=
+                                    static_cast<std::uint16_t>(1u << ((u0 + t) % w));
+            }
+        } else {
+            p.field_masks.clear(); // too large to read off: no generic kernel for this program
+        }
+    }
     p.ir_hash = ir_hash_of(p);
     return p;
 }

@@ -66,6 +66,9 @@ struct Program {
     std::uint32_t staged_threads = 0; // staged CTA size override (0 = 256)
     std::uint32_t staged_producer = 0; // 0 auto, 1 cp.async, 2 TMA tensor, 3 TMA tensor + producer warp
     ProgramStats stats;
+    // plain-field bitmatrix of the program for the generic kernel: mask[(i*w + b)*cols + j] = strips of
+    // input j feeding strip b of output i (empty for schedule programs that leave strips unwritten)
+    std::vector<std::uint16_t> field_masks;
     std::uint64_t ir_hash = 0; // hash of every instruction list a kernel is generated from (code, parts):
                                // part of the kernel name, so a cached cubin never outlives its program
 };

@@ -1,5 +1,7 @@
 #include "runtime.hpp"
 
+#include "kernels.hpp"
+
 #include <cuda.h>
 #include <dlfcn.h>
 #include <nvrtc.h>
@@ -8,6 +10,9 @@
 #include <filesystem>
 
 #include <atomic>
+#include <sys/stat.h>
+#include <chrono>
+#include <future>
 #include <cstring>
 #include <cstdlib>
 #include <fstream>
@@ -235,6 +240,45 @@ std::vector<char> nvrtc_compile(const std::string& src, const std::string& name)
     return cubin;
 }
 
+// Tiered compilation: a kernel that is neither loaded, prebuilt nor in the
+// disk cache is compiled in the background while the generic bit-matrix
+// kernel (kernels.cu) serves the launches; load_kernel picks the result up.
+std::mutex g_async_mu;
+std::unordered_map<std::string, std::shared_future<std::vector<char>>> g_async;
+
+std::string cache_name(const std::string& name) { return name + "." + nvrtc_tag(); }
+
+bool file_exists(const std::string& path) {
+    struct stat sb {};
+    return ::stat(path.c_str(), &sb) == 0;
+}
+
+// true when load_kernel would not have to compile (or wait for) this kernel
+bool kernel_ready(const std::string& name, int device) {
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (g_kernels.count(name + "@" + std::to_string(device))) return true;
+    }
+    if (file_exists(kernel_dir() + "/" + name + ".cubin")) return true;
+    const std::string cache = jit_cache_dir();
+    if (!cache.empty() && file_exists(cache + "/" + cache_name(name) + ".cubin")) return true;
+    std::lock_guard<std::mutex> lk(g_async_mu);
+    auto it = g_async.find(name);
+    return it != g_async.end() && it->second.wait_for(std::chrono::seconds(0)) == std::future_status::ready;
+}
+
+void start_async_compile(const Program& p, const KernelShape& ks, const std::string& name) {
+    std::lock_guard<std::mutex> lk(g_async_mu);
+    if (g_async.count(name)) return;
+    std::string src = generate_cuda(p, ks); // the program need not outlive this call
+    const std::string cache = jit_cache_dir();
+    g_async[name] = std::async(std::launch::async, [src = std::move(src), name, cache] {
+                        std::vector<char> cubin = nvrtc_compile(src, name);
+                        if (!cache.empty()) write_cache(cache, cache_name(name), cubin);
+                        return cubin;
+                    }).share();
+}
+
 LoadedKernel load_kernel(const Program& p, const KernelShape& ks, int device) {
     const std::string name = kernel_name(p, ks);
     const std::string key = name + "@" + std::to_string(device);
@@ -249,9 +293,19 @@ LoadedKernel load_kernel(const Program& p, const KernelShape& ks, int device) {
     // cached cubins are keyed by the compiler too: one from another NVRTC is not reused
     const std::string cname = cache.empty() || !cubin.empty() ? std::string() : name + "." + nvrtc_tag();
     if (cubin.empty() && !cache.empty()) cubin = read_file(cache + "/" + cname + ".cubin");
-    if (cubin.empty()) {
-        cubin = nvrtc_compile(generate_cuda(p, ks), name);
-        if (!cache.empty()) write_cache(cache, cname, cubin);
+    if (cubin.empty()) { // a background compile of it, else compile now
+        std::shared_future<std::vector<char>> pending;
+        {
+            std::lock_guard<std::mutex> lk(g_async_mu);
+            auto it = g_async.find(name);
+            if (it != g_async.end()) pending = it->second;
+        }
+        if (pending.valid()) {
+            cubin = pending.get();
+        } else {
+            cubin = nvrtc_compile(generate_cuda(p, ks), name);
+            if (!cache.empty()) write_cache(cache, cname, cubin);
+        }
     }
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_kernels.find(key);
@@ -381,14 +435,15 @@ int kernel_mode() {
     int m = g_mode.load();
     if (m < 0) {
         m = env_int("PYRIT_B200_MODE", 0);
-        if (m < 0 || m > 2) m = 0;
+        if (m < 0 || m > 3) m = 0;
         g_mode = m;
     }
     return m;
 }
 
 void set_kernel_mode(int mode) {
-    if (mode < 0 || mode > 2) raise(Errc::InvalidArgument, "mode must be 0 (auto), 1 (direct) or 2 (staged)");
+    if (mode < 0 || mode > 3)
+        raise(Errc::InvalidArgument, "mode must be 0 (auto), 1 (direct), 2 (staged) or 3 (generic)");
     g_mode = mode;
 }
 
@@ -447,6 +502,61 @@ KernelShape choose_shape(const Program& p, const std::uint8_t* const* in, std::u
     return ks;
 }
 
+namespace {
+
+// PYRIT_B200_TIERED=0 compiles every new kernel before its first launch
+bool tiered() {
+    static const bool on = env_int("PYRIT_B200_TIERED", 1) != 0;
+    return on;
+}
+
+bool generic_ok(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out, std::uint64_t strip,
+                std::uint64_t off, std::uint64_t len, std::uint64_t nb, std::uint64_t in_pitch,
+                std::uint64_t out_pitch) {
+    if (p.field_masks.empty() || p.rows == 0 || p.cols + p.rows > kGenericMaxPtrs ||
+        p.field_masks.size() > kGenericMaxMasks)
+        return false;
+    bool ok = strip % 4 == 0 && off % 4 == 0 && len % 4 == 0 && (nb <= 1 || (in_pitch % 4 == 0 && out_pitch % 4 == 0));
+    for (std::uint32_t j = 0; ok && j < p.cols; ++j) ok = aligned(in[j], 4);
+    for (std::uint32_t i = 0; ok && i < p.rows; ++i) ok = aligned(out[i], 4);
+    return ok;
+}
+
+LaunchInfo launch_generic_program(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
+                                  std::uint64_t strip, std::uint64_t off, std::uint64_t len, std::uint64_t nb,
+                                  std::uint64_t in_pitch, std::uint64_t out_pitch, cudaStream_t stream) {
+    thread_local GenericArgs a; // ~27 KB of kernel parameters
+    const std::uint64_t nwords = len / 4;
+    a.S = strip;
+    a.off = off;
+    a.nwords = nwords;
+    a.nb = nb;
+    a.ibp = nb > 1 ? in_pitch : 0;
+    a.obp = nb > 1 ? out_pitch : 0;
+    a.k = p.cols;
+    a.e = p.rows;
+    a.w = p.field.w;
+    for (std::uint32_t j = 0; j < p.cols; ++j) a.ptr[j] = in[j];
+    for (std::uint32_t i = 0; i < p.rows; ++i) a.ptr[p.cols + i] = out[i];
+    std::copy(p.field_masks.begin(), p.field_masks.end(), a.mask);
+    const std::uint64_t want = (nwords * nb + 255) / 256;
+    const unsigned blocks = static_cast<unsigned>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(want, 8ull * sm_count())));
+    const std::uint64_t stride = std::uint64_t(blocks) * 256;
+    a.sq = stride / nwords;
+    a.sr = stride % nwords;
+    check_cuda(launch_generic(a, blocks, stream), "generic kernel launch");
+    ++g_launches;
+    LaunchInfo info;
+    info.kernel = "pyrit_generic_bitmatrix";
+    info.blocks = blocks;
+    info.threads = 256;
+    info.lanes = 1;
+    g_last = info;
+    return info;
+}
+
+} // namespace
+
 std::string prepare_program(const Program& p, std::uint32_t lanes) {
     int dev = 0;
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
@@ -474,6 +584,15 @@ LaunchInfo launch_batch(const Program& p, const std::uint8_t* const* in, std::ui
     int dev = 0;
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
     const KernelShape ks = choose_shape(p, in, out, strip, off, len, nb, in_pitch, out_pitch);
+    const bool gen_ok = generic_ok(p, in, out, strip, off, len, nb, in_pitch, out_pitch);
+    if (gen_ok && kernel_mode() == 3) return launch_generic_program(p, in, out, strip, off, len, nb, in_pitch, out_pitch, stream);
+    if (gen_ok && tiered()) {
+        const std::string name = kernel_name(p, ks);
+        if (!kernel_ready(name, dev)) {
+            start_async_compile(p, ks, name);
+            return launch_generic_program(p, in, out, strip, off, len, nb, in_pitch, out_pitch, stream);
+        }
+    }
     const LoadedKernel k = load_kernel(p, ks, dev);
     // Args: in[cols], out[rows], S, off, len|nwords, nb, ibp, obp (, sq, sr)
     // (, tensor maps tm[cols] at the next 64-byte boundary for TMA tensor copies)

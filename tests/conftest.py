@@ -5,6 +5,9 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+# the tests validate the specialised kernels; the generic stand-in that tiered
+# compilation launches meanwhile is tested on its own (kernel mode 3)
+os.environ.setdefault("PYRIT_B200_TIERED", "0")
 
 
 def pytest_configure(config):

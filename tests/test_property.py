@@ -123,3 +123,25 @@ def test_output_parts_and_pair_sharing(case):
                 os.environ["PYRIT_B200_" + n] = v
     for a, b in zip(got, want):
         assert np.array_equal(a, b)
+
+
+@settings(max_examples=200, deadline=None)
+@given(part_cases())
+def test_generic_kernel_bitmatrix(case):
+    """The generic kernel's bitmatrix (Program::field_masks: the field code for the embedding, read off
+    the program for the Parity transform) computes the same bytes as the oracle, evaluated on the
+    host (PYRIT_B200_INTERPRET_GENERIC)."""
+    import os
+    f, kind, m, _knobs, group, strip, seed = case
+    rng = np.random.default_rng(seed)
+    r, k = m.shape
+    ins = [rng.integers(0, 256, f.w * strip, dtype=np.uint8) for _ in range(k)]
+    want = O.apply_columns(ofield(f), m, ins, strip, kind=kind)
+    plan = P.Plan.create(f, m, transform=P.TransformKind(kind), group=group)
+    os.environ["PYRIT_B200_INTERPRET_GENERIC"] = "1"
+    try:
+        got = plan.interpret(ins, strip, outs=[np.full(f.w * strip, 0x3C, dtype=np.uint8) for _ in range(r)])
+    finally:
+        os.environ.pop("PYRIT_B200_INTERPRET_GENERIC", None)
+    for a, b in zip(got, want):
+        assert np.array_equal(a, b)

@@ -10,6 +10,7 @@ sustained_trace_* files under profiles/r01_s2: they compare the TMA and cp.async
 producers, and the torch copy probes.
 """
 import os, sys, json, time
+os.environ.setdefault("PYRIT_B200_TIERED", "0")  # measure/validate the specialised kernels, never the generic stand-in
 sys.path.insert(0, os.getcwd())
 import torch
 import paper_1709_00178_b200 as P

@@ -15,6 +15,7 @@ import argparse
 import json
 import os
 import sys
+os.environ.setdefault("PYRIT_B200_TIERED", "0")  # measure/validate the specialised kernels, never the generic stand-in
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from bench import ClockSampler  # noqa: E402
