@@ -260,7 +260,9 @@ int pyrit_cu_digest(const uint8_t* src, uint64_t len, uint64_t word_offset, uint
 int pyrit_set_lanes(uint32_t lanes); /* 32-bit words per thread per strip: 1, 2 or 4 */
 /* 0 = auto (TMA-staged kernel whenever pointers/pitch/window are 16-byte
  * aligned and the tiles fit in shared memory), 1 = direct kernel only,
- * 2 = staged whenever possible */
+ * 2 = staged whenever possible, 3 = the generic bit-matrix kernel (no
+ * per-code compilation; 4-byte aligned launches) -- it also serves launches
+ * whose specialised kernel is still compiling (PYRIT_B200_TIERED, default on) */
 int pyrit_set_kernel_mode(int mode);
 int pyrit_set_kernel_dir(const char* dir);
 /* name and geometry of this thread's most recent generated-kernel launch */
