@@ -25,6 +25,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "libpyrit_b200.so")
+HELPER = os.path.join(os.path.dirname(LIB), "pyrit_jit_helper")
 KDIR = os.path.join(PKG, "kernels")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
@@ -65,6 +66,11 @@ def build_library(force=False) -> str:
             _run([NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
                   "-Xptxas", "-v", "-c", s, "-o", o])
         objs.append(o)
+    # the background-compile helper (tiered compilation runs NVRTC in its own process)
+    helper_src = os.path.join(CSRC, "jit_helper.cpp")
+    if force or _stale(HELPER, [helper_src]):
+        _run(["g++", "-std=c++20", "-O2", f"-I{CUDA}/include", f'-DPYRIT_NVRTC_PATH="{CUDA}/lib64/libnvrtc.so.12"',
+              helper_src, "-o", HELPER, "-ldl"])
     if force or _stale(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static", f"-L{CUDA}/lib64",
               "-Xlinker", "--exclude-libs,ALL", "-ldl", "-lpthread", "-lrt"])

@@ -10,6 +10,11 @@
 #include <filesystem>
 
 #include <atomic>
+#include <cstdio>
+#include <cerrno>
+#include <thread>
+#include <sys/wait.h>
+#include <spawn.h>
 #include <sys/stat.h>
 #include <chrono>
 #include <future>
@@ -21,6 +26,8 @@
 #include <unordered_map>
 #include <type_traits>
 #include <vector>
+
+extern char** environ;
 
 namespace pyrit_b200 {
 
@@ -115,13 +122,13 @@ std::vector<char> read_file(const std::string& path) {
 // directory, or "0" / "" to disable; default $XDG_CACHE_HOME/pyrit_b200 or
 // ~/.cache/pyrit_b200.
 std::string jit_cache_dir() {
-    static const std::string dir = [] {
+    static const std::string& dir = *new std::string([] {
         if (const char* env = std::getenv("PYRIT_B200_JIT_CACHE"))
             return std::string(env) == "0" ? std::string() : std::string(env);
         if (const char* x = std::getenv("XDG_CACHE_HOME"); x && *x) return std::string(x) + "/pyrit_b200";
         if (const char* h = std::getenv("HOME"); h && *h) return std::string(h) + "/.cache/pyrit_b200";
         return std::string();
-    }();
+    }());
     return dir;
 }
 
@@ -171,7 +178,7 @@ struct Nvrtc {
 
 const Nvrtc& nvrtc() {
     static std::once_flag once;
-    static Nvrtc n;
+    static Nvrtc& n = *new Nvrtc; // never destroyed (background compiles may outlive exit)
     std::call_once(once, [] {
         std::vector<std::string> tries;
         if (const char* e = std::getenv("PYRIT_B200_NVRTC"); e && *e) tries.emplace_back(e);
@@ -202,14 +209,17 @@ const Nvrtc& nvrtc() {
     return n;
 }
 
+// file the NVRTC in use was loaded from (the helper loads the same one)
+std::string nvrtc_path() { return nvrtc().path; }
+
 // "nvrtc12.9": the compiler version in cache file names
 std::string nvrtc_tag() {
-    static const std::string tag = [] {
+    static const std::string& tag = *new std::string([] {
         const Nvrtc& n = nvrtc();
         int major = 0, minor = 0;
         if (n.version) n.version(&major, &minor);
         return "nvrtc" + std::to_string(major) + "." + std::to_string(minor);
-    }();
+    }());
     return tag;
 }
 
@@ -243,8 +253,11 @@ std::vector<char> nvrtc_compile(const std::string& src, const std::string& name)
 // Tiered compilation: a kernel that is neither loaded, prebuilt nor in the
 // disk cache is compiled in the background while the generic bit-matrix
 // kernel (kernels.cu) serves the launches; load_kernel picks the result up.
-std::mutex g_async_mu;
-std::unordered_map<std::string, std::shared_future<std::vector<char>>> g_async;
+// (heap objects that are never destroyed, so the exit-time waiter below can
+// still use them whatever the destruction order)
+std::mutex& g_async_mu = *new std::mutex;
+std::unordered_map<std::string, std::shared_future<std::vector<char>>>& g_async =
+    *new std::unordered_map<std::string, std::shared_future<std::vector<char>>>;
 
 std::string cache_name(const std::string& name) { return name + "." + nvrtc_tag(); }
 
@@ -267,16 +280,75 @@ bool kernel_ready(const std::string& name, int device) {
     return it != g_async.end() && it->second.wait_for(std::chrono::seconds(0)) == std::future_status::ready;
 }
 
-void start_async_compile(const Program& p, const KernelShape& ks, const std::string& name) {
+// The helper executable next to the library (pyrit_jit_helper, jit_helper.cpp):
+// background compiles run NVRTC in their own process, so the library's
+// process may exit at any moment (an in-process NVRTC compile still running
+// at exit() crashed: its statics were being destroyed under it).
+std::string helper_path() {
+    static const std::string& path = *new std::string([] {
+        Dl_info info{};
+        if (dladdr(reinterpret_cast<void*>(&helper_path), &info) && info.dli_fname) {
+            std::string so = info.dli_fname;
+            const auto slash = so.rfind('/');
+            return (slash == std::string::npos ? std::string(".") : so.substr(0, slash)) + "/pyrit_jit_helper";
+        }
+        return std::string("pyrit_jit_helper");
+    }());
+    return path;
+}
+
+// compile `src` in a helper process into `out` (blocking; runs on a background thread)
+std::vector<char> helper_compile(const std::string& src, const std::string& name, const std::string& out,
+                                 const std::string& lib) {
+    const std::string base = out + ".src" + std::to_string(::getpid()) + "_" +
+                             std::to_string(std::hash<std::thread::id>{}(std::this_thread::get_id()));
+    {
+        std::ofstream f(base, std::ios::binary);
+        f.write(src.data(), static_cast<std::streamsize>(src.size()));
+        if (!f) throw CudaFailure(-1000, "cannot write " + base);
+    }
+    const std::string helper = helper_path();
+    std::vector<char*> argv = {const_cast<char*>(helper.c_str()), const_cast<char*>(base.c_str()),
+                               const_cast<char*>(name.c_str()), const_cast<char*>(out.c_str()),
+                               const_cast<char*>(lib.c_str()), nullptr};
+    pid_t pid = 0;
+    const int rc = posix_spawn(&pid, helper.c_str(), nullptr, nullptr, argv.data(), environ);
+    int status = 0;
+    if (rc == 0)
+        while (::waitpid(pid, &status, 0) < 0 && errno == EINTR) {
+        }
+    std::remove(base.c_str());
+    if (rc != 0 || !WIFEXITED(status) || WEXITSTATUS(status) != 0)
+        throw CudaFailure(-1000, "background compile of " + name + " failed");
+    std::vector<char> cubin = read_file(out);
+    if (cubin.empty()) throw CudaFailure(-1000, "background compile of " + name + " produced nothing");
+    ++g_jit;
+    return cubin;
+}
+
+// false when no helper is available (the caller then compiles synchronously)
+bool start_async_compile(const Program& p, const KernelShape& ks, const std::string& name) {
+    static const bool have_helper = ::access(helper_path().c_str(), X_OK) == 0;
+    if (!have_helper) return false;
     std::lock_guard<std::mutex> lk(g_async_mu);
-    if (g_async.count(name)) return;
+    if (g_async.count(name)) return true;
     std::string src = generate_cuda(p, ks); // the program need not outlive this call
-    const std::string cache = jit_cache_dir();
-    g_async[name] = std::async(std::launch::async, [src = std::move(src), name, cache] {
-                        std::vector<char> cubin = nvrtc_compile(src, name);
-                        if (!cache.empty()) write_cache(cache, cache_name(name), cubin);
+    std::string cache = jit_cache_dir();
+    std::string out;
+    if (!cache.empty()) {
+        std::error_code ec;
+        std::filesystem::create_directories(cache, ec);
+        out = cache + "/" + cache_name(name) + ".cubin";
+    } else {
+        out = (std::filesystem::temp_directory_path() / (name + "." + std::to_string(::getpid()) + ".cubin")).string();
+    }
+    g_async[name] = std::async(std::launch::async, [src = std::move(src), name, out, keep = !cache.empty(),
+                                                    lib = nvrtc_path()] {
+                        std::vector<char> cubin = helper_compile(src, name, out, lib);
+                        if (!keep) std::remove(out.c_str());
                         return cubin;
                     }).share();
+    return true;
 }
 
 LoadedKernel load_kernel(const Program& p, const KernelShape& ks, int device) {
@@ -588,10 +660,8 @@ LaunchInfo launch_batch(const Program& p, const std::uint8_t* const* in, std::ui
     if (gen_ok && kernel_mode() == 3) return launch_generic_program(p, in, out, strip, off, len, nb, in_pitch, out_pitch, stream);
     if (gen_ok && tiered()) {
         const std::string name = kernel_name(p, ks);
-        if (!kernel_ready(name, dev)) {
-            start_async_compile(p, ks, name);
+        if (!kernel_ready(name, dev) && start_async_compile(p, ks, name))
             return launch_generic_program(p, in, out, strip, off, len, nb, in_pitch, out_pitch, stream);
-        }
     }
     const LoadedKernel k = load_kernel(p, ks, dev);
     // Args: in[cols], out[rows], S, off, len|nwords, nb, ibp, obp (, sq, sr)

@@ -163,3 +163,22 @@ def test_tiered_compilation(cuda, tmp_path):
     first, last, ok, jit = r.stdout.split()[-4:]
     assert first == "pyrit_generic_bitmatrix" and last.startswith("pyrit_ring_"), r.stdout
     assert ok == "True" and int(jit) == 1
+
+
+def test_exit_while_compiling(cuda, tmp_path):
+    """A process may exit while a background compile is still running: it must exit cleanly (the
+    compile state is never destroyed under the running thread) and promptly."""
+    script = textwrap.dedent("""
+        import numpy as np, torch
+        import paper_1709_00178_b200 as P
+        code = P.CodeSpec(11, 5, P.FieldSpec.aop(12))
+        d = torch.from_numpy(np.random.default_rng(3).integers(0, 256, (11, 12 * 4096), dtype=np.uint8)).cuda()
+        p = P.encode(d, code)
+        torch.cuda.synchronize()
+        print(P.Plan.last_launch()["kernel"])
+    """)
+    env = dict(os.environ, PYRIT_B200_TIERED="1", PYRIT_B200_JIT_CACHE=str(tmp_path))
+    r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, cwd=ROOT,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.split()[-1] == "pyrit_generic_bitmatrix"
