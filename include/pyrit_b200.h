@@ -271,6 +271,9 @@ int pyrit_cu_last_launch(char* kernel, size_t cap, uint32_t* blocks, uint32_t* t
 uint64_t pyrit_jit_compiles(void);
 /* which NVRTC compiles kernels that are not prebuilt: "nvrtc 12.9 (<file>)" */
 int pyrit_jit_info(char* buf, size_t cap);
+/* wait until every background compile started so far has finished (their
+ * kernels serve the next launches): call it before capturing a CUDA graph */
+int pyrit_jit_wait(void);
 uint64_t pyrit_kernel_launches(void);
 
 #if defined(__GNUC__)

@@ -769,6 +769,10 @@ int pyrit_cu_last_launch(char* kernel, size_t cap, uint32_t* blocks, uint32_t* t
     });
 }
 
+int pyrit_jit_wait(void) {
+    return guarded([&] { jit_wait(); });
+}
+
 int pyrit_jit_info(char* buf, size_t cap) {
     return guarded([&] {
         if (!buf || !cap) raise(Errc::InvalidArgument, "null buffer");

@@ -445,6 +445,15 @@ std::string kernel_dir() {
     return g_kernel_dir;
 }
 
+void jit_wait() {
+    std::vector<std::shared_future<std::vector<char>>> pending;
+    {
+        std::lock_guard<std::mutex> lk(g_async_mu);
+        for (auto& kv : g_async) pending.push_back(kv.second);
+    }
+    for (auto& f : pending) f.get(); // rethrows a failed compile
+}
+
 std::string jit_info() {
     const Nvrtc& n = nvrtc();
     int major = 0, minor = 0;

@@ -57,7 +57,8 @@ std::string kernel_dir();
 
 LaunchInfo last_launch(); // this thread's most recent launch_program
 std::uint64_t jit_compiles(); // number of NVRTC compilations performed so far
-std::string jit_info();       // "nvrtc <major>.<minor> (<library file>)"; throws if NVRTC cannot be loaded
+std::string jit_info();
+void jit_wait(); // wait for every background (tiered) compile started so far       // "nvrtc <major>.<minor> (<library file>)"; throws if NVRTC cannot be loaded
 std::uint64_t kernel_launches(); // number of generated-kernel launches so far
 
 KernelShape shape_for(std::uint32_t lanes);
