@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.hpp"
 
@@ -139,6 +140,42 @@ __global__ void __launch_bounds__(256) generic_kernel(const __grid_constant__ Ge
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// The same with w a compile-time constant: the strips of an input are walked
+// by an unrolled, warp-uniform predicate chain instead of a bit-scan loop.
+template <int W>
+__global__ void __launch_bounds__(256) generic_kernel_w(const __grid_constant__ GenericArgs a) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const std::uint32_t k = a.k, e = a.e;
+    const std::uint64_t S = a.S;
+    std::uint64_t c0 = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+    std::uint64_t b = c0 / a.nwords, cw = c0 - b * a.nwords;
+    while (b < a.nb) {
+        const std::uint64_t o = a.off + cw * 4;
+        const std::uint64_t oi = o + b * a.ibp, oo = o + b * a.obp;
+        for (std::uint32_t i = 0; i < e; ++i)
+#pragma unroll
+            for (int r = 0; r < W; ++r) {
+                const std::uint16_t* row = &a.mask[(i * W + r) * k];
+                std::uint32_t acc = 0;
+                for (std::uint32_t j = 0; j < k; ++j) {
+                    const std::uint32_t m = row[j];
+                    const std::uint8_t* p = a.ptr[j] + oi;
+#pragma unroll
+                    for (int c = 0; c < W; ++c)
+                        if (m & (1u << c)) acc ^= __ldg(reinterpret_cast<const std::uint32_t*>(p + c * S));
+                }
+                __stcs(reinterpret_cast<unsigned int*>(const_cast<std::uint8_t*>(a.ptr[k + i]) + oo + r * S), acc);
+            }
+        b += a.sq;
+        cw += a.sr;
+        if (cw >= a.nwords) {
+            cw -= a.nwords;
+            ++b;
+        }
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 cudaError_t launch_generic(const GenericArgs& args, unsigned blocks, cudaStream_t stream) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(blocks);
@@ -149,6 +186,18 @@ cudaError_t launch_generic(const GenericArgs& args, unsigned blocks, cudaStream_
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    static const bool unrolled = [] {
+        const char* v = std::getenv("PYRIT_B200_GENERIC_UNROLL");
+        return !v || std::atoi(v) != 0;
+    }();
+    if (unrolled) switch (args.w) {
+        case 4: return cudaLaunchKernelEx(&cfg, generic_kernel_w<4>, args);
+        case 6: return cudaLaunchKernelEx(&cfg, generic_kernel_w<6>, args);
+        case 8: return cudaLaunchKernelEx(&cfg, generic_kernel_w<8>, args);
+        case 10: return cudaLaunchKernelEx(&cfg, generic_kernel_w<10>, args);
+        case 12: return cudaLaunchKernelEx(&cfg, generic_kernel_w<12>, args);
+        default: break;
+        }
     return cudaLaunchKernelEx(&cfg, generic_kernel, args);
 }
 
