@@ -16,7 +16,7 @@ import oracle as O
 import paper_1709_00178_b200 as P
 from paper_1709_00178_b200 import _lib as L
 from paper_1709_00178_b200.workloads import WORKLOADS, shard
-from tests.helpers import G16, G64, G256, G1024, G4096, oracle_encode, oracle_ring, rand_symbols, seeded_symbols
+from tests.helpers import G16, G64, G256, G1024, G4096, ofield, oracle_encode, oracle_ring, rand_symbols, seeded_symbols
 
 pytestmark = pytest.mark.gpu
 
@@ -141,6 +141,37 @@ def test_odd_strip_sizes_byte_mode(cuda):
     code = P.CodeSpec(16, 4, G4096)
     dev_encode(cuda, code, rand_symbols(16, 4104, 6))
     assert "_H0" in P.Plan.last_launch()["kernel"]
+
+
+def test_u16_kernel_windows_and_batches(cuda):
+    """The u16-element direct kernel on 2-byte aligned strips, windows and stripe pitches (odd and even
+    u16 counts), against the oracle; nothing outside the outputs is written."""
+    import torch
+    rng = np.random.default_rng(77)
+    for spec, k, r in [(G4096, 16, 4), (G1024, 12, 4), (G256, 10, 4)]:
+        code = P.CodeSpec(k, r, spec)
+        m = P.cauchy_parity_matrix(code)
+        plan = P.Plan.encode(code)
+        for strip, off, length, nb in [(342, 0, 342, 1), (342, 2, 338, 3), (1026, 6, 1018, 2), (2050, 0, 2050, 4)]:
+            sym = spec.w * strip
+            pitch_in, pitch_out = k * sym + 2, r * sym + 6  # 2-byte aligned stripe pitches
+            buf_in = rng.integers(0, 256, nb * pitch_in + 16, dtype=np.uint8)
+            d = torch.from_numpy(buf_in).to(cuda)
+            o = torch.full((nb * pitch_out + 16,), 0x77, dtype=torch.uint8, device=cuda)
+            base_in, base_out = d.data_ptr() + 2, o.data_ptr() + 2
+            plan.apply_batch([base_in + j * sym for j in range(k)], [base_out + i * sym for i in range(r)], strip, nb,
+                             pitch_in, pitch_out, off, length, stream=torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            assert "_H0" in P.Plan.last_launch()["kernel"], P.Plan.last_launch()
+            got = o.cpu().numpy()
+            for b in range(nb):
+                ins = [buf_in[2 + b * pitch_in + j * sym: 2 + b * pitch_in + (j + 1) * sym].copy() for j in range(k)]
+                want = O.ring_replay(ofield(spec), m, ins, strip, off=off, length=length,
+                                     outs=[np.full(sym, 0x77, dtype=np.uint8) for _ in range(r)])
+                for i in range(r):
+                    at = 2 + b * pitch_out + i * sym
+                    np.testing.assert_array_equal(got[at: at + sym], want[i], err_msg=f"{spec.w} {strip} {b} {i}")
+            assert (got[:2] == 0x77).all()  # nothing written before the first output
 
 
 def test_empty_and_degenerate(cuda):
