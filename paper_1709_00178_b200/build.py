@@ -32,7 +32,7 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 HOST_SOURCES = ["algebra.cpp", "program.cpp", "runtime.cpp", "pipeline.cpp", "plans.cpp", "container.cpp", "hostpool.cpp", "capi.cpp"]
-CUDA_SOURCES = ["kernels.cu"]
+CUDA_SOURCES = ["kernels.cu", "ring_rt.cu"]
 HEADERS = ["algebra.hpp", "program.hpp", "runtime.hpp", "pipeline.hpp", "plans.hpp", "container.hpp", "kernels.hpp"]
 
 
@@ -59,12 +59,22 @@ def build_library(force=False) -> str:
             _run(["g++", "-std=c++20", "-O2", "-g", "-fPIC", "-fvisibility=hidden", "-Wall", "-Wextra",
                   f"-I{CUDA}/include", f'-DPYRIT_NVRTC_PATH="{CUDA}/lib64/libnvrtc.so.12"', "-c", s, "-o", o])
         objs.append(o)
+    # dispatch tables of the runtime-matrix ring kernel (generated, build/generated)
+    gen_dir = os.path.join(BUILD, "generated")
+    os.makedirs(gen_dir, exist_ok=True)
+    inc = os.path.join(gen_dir, "ring_rt_ops.inc")
+    gen = os.path.join(PKG, "gen_ring_rt.py")
+    if force or _stale(inc, [gen]):
+        sys.path.insert(0, ROOT)
+        from paper_1709_00178_b200 import gen_ring_rt
+
+        gen_ring_rt.main([inc])
     for src in CUDA_SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
-        if force or _stale(o, [s] + hdrs):
-            _run([NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
-                  "-Xptxas", "-v", "-c", s, "-o", o])
+        if force or _stale(o, [s, inc] + hdrs):
+            _run([NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", f"-I{gen_dir}", "-Xcompiler",
+                  "-fPIC,-fvisibility=hidden", "-c", s, "-o", o])
         objs.append(o)
     # the background-compile helper (tiered compilation runs NVRTC in its own process)
     helper_src = os.path.join(CSRC, "jit_helper.cpp")

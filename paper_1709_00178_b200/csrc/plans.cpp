@@ -83,7 +83,9 @@ DecodeProgram decode_program(const CodeParams& c, const std::vector<std::uint32_
         d.prog = p;
         return d;
     }
-    auto p = std::make_shared<const Program>(compile_program(c.field, c.kind, d.repair.m, CompileOptions{}));
+    Program prog = compile_program(c.field, c.kind, d.repair.m, CompileOptions{});
+    prog.adhoc = true; // one of many erasure patterns: the runtime-matrix kernel serves it
+    auto p = std::make_shared<const Program>(std::move(prog));
     cache().put(key.str(), p);
     d.prog = p;
     return d;

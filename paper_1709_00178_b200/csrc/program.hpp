@@ -69,6 +69,9 @@ struct Program {
     // plain-field bitmatrix of the program for the generic kernel: mask[(i*w + b)*cols + j] = strips of
     // input j feeding strip b of output i (empty for schedule programs that leave strips unwritten)
     std::vector<std::uint16_t> field_masks;
+    // one of many programs of a code (a decode erasure pattern): served by the
+    // runtime-matrix ring kernel, never compiled (runtime.cpp launch_batch)
+    bool adhoc = false;
     std::uint64_t ir_hash = 0; // hash of every instruction list a kernel is generated from (code, parts):
                                // part of the kernel name, so a cached cubin never outlives its program
 };

@@ -9,7 +9,9 @@
 
 #include <filesystem>
 
+#include <algorithm>
 #include <atomic>
+#include <bit>
 #include <cstdio>
 #include <cerrno>
 #include <thread>
@@ -516,16 +518,25 @@ int kernel_mode() {
     int m = g_mode.load();
     if (m < 0) {
         m = env_int("PYRIT_B200_MODE", 0);
-        if (m < 0 || m > 3) m = 0;
+        if (m < 0 || m > 4) m = 0;
         g_mode = m;
     }
     return m;
 }
 
 void set_kernel_mode(int mode) {
-    if (mode < 0 || mode > 3)
-        raise(Errc::InvalidArgument, "mode must be 0 (auto), 1 (direct), 2 (staged) or 3 (generic)");
+    if (mode < 0 || mode > 4)
+        raise(Errc::InvalidArgument,
+              "mode must be 0 (auto), 1 (direct), 2 (staged), 3 (generic) or 4 (runtime-matrix ring kernel)");
     g_mode = mode;
+}
+
+int rt_policy() {
+    static const int v = [] {
+        const int x = env_int("PYRIT_B200_RT", 1);
+        return x < 0 || x > 2 ? 1 : x;
+    }();
+    return v;
 }
 
 KernelShape choose_shape(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
@@ -636,7 +647,139 @@ LaunchInfo launch_generic_program(const Program& p, const std::uint8_t* const* i
     return info;
 }
 
+// ---- runtime-matrix ring kernel (ring_rt.cu) ------------------------------
+
+bool overlaps(const std::uint8_t* a, std::uint64_t alen, const std::uint8_t* b, std::uint64_t blen) {
+    const auto x = reinterpret_cast<std::uintptr_t>(a), y = reinterpret_cast<std::uintptr_t>(b);
+    return x < y + blen && y < x + alen;
+}
+
+// Does any output span overlap an input span where a column of one is not the
+// same column of the other?  Kernels that read every input of a tile before
+// storing its outputs (ring_rt, staged, unsplit direct) are exact when outputs
+// alias inputs column for column (decode() in place, slot aliasing of replay);
+// anything else must not run them concurrently with a read of the same bytes.
+bool unsafe_alias(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out, std::uint64_t strip,
+                  std::uint64_t nb, std::uint64_t in_pitch, std::uint64_t out_pitch) {
+    const std::uint64_t w = p.field.w;
+    const std::uint64_t ispan = (nb - 1) * in_pitch + w * strip, ospan = (nb - 1) * out_pitch + w * strip;
+    for (std::uint32_t i = 0; i < p.rows; ++i)
+        for (std::uint32_t j = 0; j < p.cols; ++j) {
+            if (!overlaps(out[i], ospan, in[j], ispan)) continue;
+            const std::int64_t d = reinterpret_cast<std::intptr_t>(out[i]) - reinterpret_cast<std::intptr_t>(in[j]);
+            if (nb > 1 && (in_pitch != out_pitch || d != 0)) return true;
+            if (d % static_cast<std::int64_t>(strip) != 0) return true;
+        }
+    return false;
+}
+
 } // namespace
+
+bool ring_rt_eligible(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out, std::uint64_t strip,
+                      std::uint64_t off, std::uint64_t len, std::uint64_t nb, std::uint64_t in_pitch,
+                      std::uint64_t out_pitch) {
+    if (p.crs || p.sched || p.reps.empty() || p.rows == 0 || p.cols > kRtMaxK) return false;
+    if (!rt_supported(p.field.w, p.field.n, p.field.modulus)) return false;
+    if (p.kind == TransformKind::Parity && p.field.n - p.field.w > 256 / p.field.w) return false;
+    bool ok = strip % 16 == 0 && off % 16 == 0 && len % 16 == 0 && (nb <= 1 || (in_pitch % 16 == 0 && out_pitch % 16 == 0));
+    for (std::uint32_t j = 0; ok && j < p.cols; ++j) ok = aligned(in[j], 16);
+    for (std::uint32_t i = 0; ok && i < p.rows; ++i) ok = aligned(out[i], 16);
+    if (!ok) return false;
+    if ((len + kRtTile - 1) / kRtTile * nb >= (std::uint64_t(1) << 31)) return false;
+    return !unsafe_alias(p, in, out, strip, nb, in_pitch, out_pitch);
+}
+
+LaunchInfo launch_ring_rt_program(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
+                                  std::uint64_t strip, std::uint64_t off, std::uint64_t len, std::uint64_t nb,
+                                  std::uint64_t in_pitch, std::uint64_t out_pitch, cudaStream_t stream) {
+    thread_local RtArgs a; // ~17 KB of kernel parameters
+    const std::uint32_t w = p.field.w, n = p.field.n, k = p.cols;
+    const std::uint32_t ep = static_cast<std::uint32_t>(rt_part_outputs(static_cast<int>(n)));
+    const std::uint32_t tile = kRtTile, elem = 8, slot = w * tile;
+    const std::uint64_t tpb = (len + tile - 1) / tile;
+    static const int promo_knob = env_int("PYRIT_B200_TMA_PROMO", 3);
+    const CUtensorMapL2promotion promo = static_cast<CUtensorMapL2promotion>(std::min(3, std::max(0, promo_knob)));
+    for (std::uint32_t j = 0; j < k; ++j) {
+        CUtensorMap m;
+        const cuuint64_t dims[3] = {strip / elem, w, nb};
+        const cuuint64_t strides[2] = {strip, nb > 1 ? in_pitch : strip * w};
+        const cuuint32_t box[3] = {kRtCpp, w, 1};
+        const cuuint32_t es[3] = {1, 1, 1};
+        check_cu(driver().tensorMapEncodeTiled(&m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<std::uint8_t*>(in[j]),
+                                               dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                               CU_TENSOR_MAP_SWIZZLE_NONE, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+                 "cuTensorMapEncodeTiled(ring_rt)");
+        std::memcpy(a.tm[j], &m, sizeof m);
+    }
+    a.S = strip;
+    a.off = off;
+    a.len = len;
+    a.nb = nb;
+    a.obp = nb > 1 ? out_pitch : 0;
+    a.k = k;
+    a.tpb = static_cast<std::uint32_t>(tpb);
+    a.ntiles = static_cast<std::uint32_t>(tpb * nb);
+    std::memset(a.fm, 0, sizeof a.fm);
+    const bool par = p.kind == TransformKind::Parity;
+    if (par) // strip w+q of the extended input = XOR of strips i = q (mod s) (phi_P, transform.hpp:50-60)
+        for (std::uint32_t q = 0; q + w < n; ++q)
+            for (std::uint32_t i = q; i < w; i += p.field.s) a.fm[q * w + i] = ~0u;
+    RtLaunch l;
+    l.w = w;
+    l.n = n;
+    l.modulus = p.field.modulus;
+    l.parity = par;
+    l.stream = stream;
+    static const bool pdl = env_int("PYRIT_B200_PDL", 1) != 0;
+    l.pdl = pdl;
+    // Outputs go to two parts of 256 threads (16 warps per SM); a single output
+    // runs one part per CTA and two CTAs per SM.  More outputs than 2 * ep go to
+    // further launches (each re-reads the inputs).
+    LaunchInfo info;
+    for (std::uint32_t i0 = 0; i0 < p.rows; i0 += 2 * ep) {
+        const std::uint32_t e = std::min(2 * ep, p.rows - i0);
+        l.R = e == 1 ? 1 : 2;
+        l.E = (e + 1) / 2;
+        a.epart[0] = std::min(l.E, e);
+        a.epart[1] = e - a.epart[0];
+        const std::uint32_t ctas_per_sm = l.R == 1 ? 2 : 1;
+        // shared-memory ring: mbarriers, then as many fragment slots as fit (<= 32)
+        std::uint32_t ns = 32, bar = 0;
+        const std::uint32_t budget = (ctas_per_sm == 2 ? 113 : 227) * 1024;
+        for (; ns >= 2; --ns) {
+            bar = (16 * ns + 127) / 128 * 128;
+            if (bar + ns * slot <= budget) break;
+        }
+        a.nslot = ns;
+        a.slot0 = bar;
+        l.smem = bar + ns * slot;
+        l.blocks = static_cast<unsigned>(
+            std::max<std::uint64_t>(1, std::min<std::uint64_t>(tpb * nb, std::uint64_t(ctas_per_sm) * sm_count())));
+        std::uint32_t nops = 0;
+        for (std::uint32_t part = 0; part < 2; ++part) {
+            const std::uint32_t b0 = i0 + part * l.E, ne = a.epart[part];
+            for (std::uint32_t j = 0; j < k; ++j) {
+                a.opoff[part][j] = static_cast<std::uint16_t>(nops);
+                for (std::uint32_t i = 0; i < ne; ++i)
+                    for (std::uint32_t m = p.reps[std::size_t(b0 + i) * k + j]; m; m &= m - 1) {
+                        if (nops >= kRtMaxOps) raise(Errc::InvalidArgument, "ring_rt: too many ring terms per launch");
+                        a.ops[nops++] = static_cast<std::uint8_t>(i * n + static_cast<std::uint32_t>(std::countr_zero(m)));
+                    }
+            }
+            a.opoff[part][k] = static_cast<std::uint16_t>(nops);
+            for (std::uint32_t i = 0; i < ne; ++i) a.out[part * kRtPartE + i] = out[b0 + i];
+        }
+        check_cuda(launch_ring_rt(a, l), "ring_rt launch");
+        ++g_launches;
+        info.blocks = l.blocks;
+        info.threads = l.R * kRtCpp;
+    }
+    info.kernel = "pyrit_ring_rt_w" + std::to_string(w) + "_n" + std::to_string(n) + (par ? "_par" : "");
+    info.lanes = 2;
+    info.staged = true;
+    g_last = info;
+    return info;
+}
 
 std::string prepare_program(const Program& p, std::uint32_t lanes) {
     int dev = 0;
@@ -664,13 +807,27 @@ LaunchInfo launch_batch(const Program& p, const std::uint8_t* const* in, std::ui
     if (nb == 1) in_pitch = out_pitch = 0;
     int dev = 0;
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    const int mode = kernel_mode();
+    const bool rt_ok = mode != 3 && rt_policy() != 0 &&
+                       ring_rt_eligible(p, in, out, strip, off, len, nb, in_pitch, out_pitch);
+    if (rt_ok && (mode == 4 || rt_policy() == 2))
+        return launch_ring_rt_program(p, in, out, strip, off, len, nb, in_pitch, out_pitch, stream);
     const KernelShape ks = choose_shape(p, in, out, strip, off, len, nb, in_pitch, out_pitch);
-    const bool gen_ok = generic_ok(p, in, out, strip, off, len, nb, in_pitch, out_pitch);
-    if (gen_ok && kernel_mode() == 3) return launch_generic_program(p, in, out, strip, off, len, nb, in_pitch, out_pitch, stream);
-    if (gen_ok && tiered()) {
+    const bool gen_ok = generic_ok(p, in, out, strip, off, len, nb, in_pitch, out_pitch) &&
+                        !unsafe_alias(p, in, out, strip, nb, in_pitch, out_pitch);
+    if (gen_ok && mode == 3) return launch_generic_program(p, in, out, strip, off, len, nb, in_pitch, out_pitch, stream);
+    if ((rt_ok || gen_ok) && (tiered() || (rt_ok && p.adhoc))) {
+        // a kernel that is not ready yet: the runtime-matrix ring kernel (else
+        // the generic bit-matrix kernel) serves the launch; programs of one of
+        // many erasure patterns (decode) never compile, others compile in the
+        // background for the next launches
         const std::string name = kernel_name(p, ks);
-        if (!kernel_ready(name, dev) && start_async_compile(p, ks, name))
-            return launch_generic_program(p, in, out, strip, off, len, nb, in_pitch, out_pitch, stream);
+        if (!kernel_ready(name, dev)) {
+            if (rt_ok && p.adhoc) return launch_ring_rt_program(p, in, out, strip, off, len, nb, in_pitch, out_pitch, stream);
+            if (start_async_compile(p, ks, name))
+                return rt_ok ? launch_ring_rt_program(p, in, out, strip, off, len, nb, in_pitch, out_pitch, stream)
+                             : launch_generic_program(p, in, out, strip, off, len, nb, in_pitch, out_pitch, stream);
+        }
     }
     const LoadedKernel k = load_kernel(p, ks, dev);
     // Args: in[cols], out[rows], S, off, len|nwords, nb, ibp, obp (, sq, sr)

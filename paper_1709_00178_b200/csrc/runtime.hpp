@@ -65,8 +65,21 @@ KernelShape shape_for(std::uint32_t lanes);
 // direct-kernel shape for p: rows split over thread groups when p has several output parts
 KernelShape direct_shape(const Program& p, std::uint32_t lanes);
 
-// 0 = auto (TMA-staged whenever alignment allows), 1 = direct LDG only, 2 = staged
+// 0 = auto (TMA-staged whenever alignment allows), 1 = direct LDG only, 2 = staged,
+// 3 = generic bit-matrix kernel, 4 = runtime-matrix ring kernel (ring_rt.cu)
 int kernel_mode();
+// PYRIT_B200_RT: 0 = never use the runtime-matrix ring kernel, 1 (default) =
+// for launches whose generated kernel is not ready and for ad-hoc programs
+// (decode patterns), 2 = for every eligible launch
+int rt_policy();
+// can the runtime-matrix ring kernel run this launch (prebuilt geometry,
+// 16-byte alignment, k <= 64, outputs aliasing inputs only column for column)
+bool ring_rt_eligible(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out, std::uint64_t strip,
+                      std::uint64_t off, std::uint64_t len, std::uint64_t nb, std::uint64_t in_pitch,
+                      std::uint64_t out_pitch);
+LaunchInfo launch_ring_rt_program(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
+                                  std::uint64_t strip, std::uint64_t off, std::uint64_t len, std::uint64_t nb,
+                                  std::uint64_t in_pitch, std::uint64_t out_pitch, cudaStream_t stream);
 void set_kernel_mode(int mode);
 // the kernel shape a launch with these arguments uses
 KernelShape choose_shape(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
