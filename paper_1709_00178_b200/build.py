@@ -113,6 +113,7 @@ def prebuild_kernels(lanes=(100, 1), force=False) -> list[str]:
     src_dir = os.path.join(BUILD, "generated")
     os.makedirs(src_dir, exist_ok=True)
     built = []
+    keys = []
     for tag, fld, k, r, erased in baseline_programs():
         code = L.pyrit_code(k, r, L.pyrit_field(*fld), 0)
         plan = C.c_void_p()
@@ -122,6 +123,9 @@ def prebuild_kernels(lanes=(100, 1), force=False) -> list[str]:
             er = (C.c_uint32 * len(erased))(*erased)
             L.check(lib.pyrit_plan_decode(C.byref(code), er, len(erased), C.byref(plan), None, None))
         try:
+            kb = C.create_string_buffer(128)
+            L.check(lib.pyrit_plan_key(plan, kb, 128))
+            keys.append(kb.value.decode())
             for ln in lanes:
                 size = C.c_size_t(0)
                 name = C.create_string_buffer(128)
@@ -142,6 +146,10 @@ def prebuild_kernels(lanes=(100, 1), force=False) -> list[str]:
                 built.append(cubin)
         finally:
             lib.pyrit_plan_destroy(plan)
+    # plan keys with prebuilt kernels: decode patterns listed here run their
+    # specialised kernel, every other pattern the runtime-matrix kernel
+    with open(os.path.join(KDIR, "prebuilt.tsv"), "w") as f:
+        f.write("\n".join(keys) + "\n")
     # cubins of older generator versions are never loaded again: drop them
     for f in os.listdir(KDIR):
         if f.endswith(".cubin") and os.path.join(KDIR, f) not in built:

@@ -2,6 +2,9 @@
 
 #include <algorithm>
 #include <bit>
+#include <map>
+#include <memory>
+#include <mutex>
 
 namespace pyrit_b200 {
 
@@ -41,12 +44,79 @@ void validate_field(const Field& f) {
         raise(Errc::InvalidArgument, "modulus does not divide x^n + 1");
 }
 
+namespace {
+
+// Log/antilog tables of GF(2^w) over a generator g of the multiplicative
+// group (x itself is not one for the all-one moduli: x^(w+1) = 1), so that a
+// product or inverse is two table reads instead of a carry-less multiply and
+// reduction (gf_mul) or a search over the field (gf_inv, field.hpp:82-89:
+// 2^w multiplies).  Same results: the tables are built with those functions.
+struct GfTables {
+    std::uint32_t q1 = 0;              // 2^w - 1
+    std::vector<std::uint16_t> log, exp; // exp has 2*q1 entries (no modulo on add)
+};
+
+std::uint32_t slow_mul(std::uint32_t a, std::uint32_t b, std::uint32_t modulus) {
+    return static_cast<std::uint32_t>(poly_mod(clmul(a, b), modulus));
+}
+
+std::shared_ptr<const GfTables> build_tables(std::uint32_t w, std::uint32_t modulus) {
+    auto t = std::make_shared<GfTables>();
+    const std::uint32_t q = 1u << w;
+    t->q1 = q - 1;
+    for (std::uint32_t g = q == 2 ? 1u : 2u; g < q; ++g) {
+        // order of g: the first power that returns to 1
+        std::uint32_t v = 1, ord = 0;
+        do {
+            v = slow_mul(v, g, modulus);
+            ++ord;
+        } while (v != 1 && ord <= t->q1);
+        if (ord == t->q1) {
+            t->log.assign(q, 0);
+            t->exp.assign(2 * std::size_t(t->q1), 0);
+            v = 1;
+            for (std::uint32_t i = 0; i < t->q1; ++i) {
+                t->exp[i] = t->exp[i + t->q1] = static_cast<std::uint16_t>(v);
+                t->log[v] = static_cast<std::uint16_t>(i);
+                v = slow_mul(v, g, modulus);
+            }
+            return t;
+        }
+    }
+    return nullptr; // p is not irreducible: no multiplicative group to tabulate
+}
+
+// tables of f, built once per (w, modulus) and kept (a thread's last field is
+// cached so a matrix loop pays one comparison per product)
+const GfTables* tables(const Field& f) {
+    const std::uint64_t key = (std::uint64_t(f.w) << 32) | f.modulus;
+    thread_local std::uint64_t last_key = ~0ull;
+    thread_local const GfTables* last = nullptr;
+    if (key == last_key) return last;
+    static std::mutex mu;
+    static std::map<std::uint64_t, std::shared_ptr<const GfTables>> all;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = all.find(key);
+    if (it == all.end()) it = all.emplace(key, build_tables(f.w, f.modulus)).first;
+    last_key = key;
+    last = it->second.get();
+    return last;
+}
+
+} // namespace
+
 std::uint32_t gf_mul(std::uint32_t a, std::uint32_t b, const Field& f) {
-    return static_cast<std::uint32_t>(poly_mod(clmul(a, b), f.modulus));
+    if (a < f.field_size() && b < f.field_size() && f.w <= 16) {
+        if (a == 0 || b == 0) return 0;
+        if (const GfTables* t = tables(f)) return t->exp[std::size_t(t->log[a]) + t->log[b]];
+    }
+    return slow_mul(a, b, f.modulus);
 }
 
 std::uint32_t gf_inv(std::uint32_t a, const Field& f) {
     if (a == 0) raise(Errc::ZeroInverse, "inverse of zero");
+    if (a < f.field_size() && f.w <= 16)
+        if (const GfTables* t = tables(f)) return t->exp[(t->q1 - t->log[a]) % t->q1];
     for (std::uint32_t b = 1; b < f.field_size(); ++b)
         if (gf_mul(a, b, f) == 1) return b;
     raise(Errc::ZeroInverse, "no inverse found");
@@ -66,7 +136,31 @@ std::uint32_t dense_transform(std::uint32_t u, const Field& f) {
     return ring_mul(u & f.field_mask(), (f.modulus ^ 1u) & f.ring_mask(), f);
 }
 
+namespace {
+std::uint32_t sparse_transform_uncached(std::uint32_t u, const Field& f);
+} // namespace
+
+// memoised per field (a code's matrices repeat entries, and every decode
+// pattern of a code draws from the same 2^w values)
 std::uint32_t sparse_transform(std::uint32_t u, const Field& f) {
+    if (f.w > 16 || u >= f.field_size()) return sparse_transform_uncached(u, f);
+    const std::uint64_t key = (std::uint64_t(f.w) << 48) ^ (std::uint64_t(f.n) << 40) ^ f.modulus;
+    static std::mutex mu;
+    static std::map<std::uint64_t, std::vector<std::uint64_t>> memo; // value + 1, 0 = not yet known
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto& v = memo[key];
+        if (v.empty()) v.assign(f.field_size(), 0);
+        if (v[u]) return static_cast<std::uint32_t>(v[u] - 1);
+    }
+    const std::uint32_t r = sparse_transform_uncached(u, f);
+    std::lock_guard<std::mutex> lk(mu);
+    memo[key][u] = std::uint64_t(r) + 1;
+    return r;
+}
+
+namespace {
+std::uint32_t sparse_transform_uncached(std::uint32_t u, const Field& f) {
     // Lightest element of the coset anchor + (p) of degree < n, ties toward
     // the smallest value (ring.hpp:77-90); candidates are anchor ^ m*p for
     // every m of degree < n - w (ring.hpp:65-72).
@@ -84,6 +178,7 @@ std::uint32_t sparse_transform(std::uint32_t u, const Field& f) {
     }
     return best;
 }
+} // namespace
 
 std::vector<std::uint32_t> fold_table(const Field& f) {
     std::vector<std::uint32_t> t;

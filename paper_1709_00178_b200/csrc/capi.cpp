@@ -293,19 +293,20 @@ int pyrit_plan_decode(const pyrit_code* code, const uint32_t* erased, uint32_t n
 int pyrit_plan_get_stats(const pyrit_plan* plan, pyrit_plan_stats* out) {
     return guarded([&] {
         if (!plan || !out) raise(Errc::InvalidArgument, "null argument");
-        const auto& s = plan->prog.stats;
-        out->rows = plan->prog.rows;
-        out->cols = plan->prog.cols;
+        const Program& fp = full_program(plan->prog);
+        const auto& s = fp.stats;
+        out->rows = fp.rows;
+        out->cols = fp.cols;
         out->matrix_ones = s.matrix_ones;
         out->ref_region_ops = s.ref_region_ops;
         out->naive_xors = s.naive_xors;
         out->xors = s.xors;
         out->loads = s.loads;
         out->stores = s.stores;
-        out->group = plan->prog.group;
-        out->parts = static_cast<uint32_t>(plan->prog.parts.size());
+        out->group = fp.group;
+        out->parts = static_cast<uint32_t>(fp.parts.size());
         out->part_xors = 0;
-        for (const Program& q : plan->prog.parts) out->part_xors += q.stats.xors;
+        for (const Program& q : fp.parts) out->part_xors += q.stats.xors;
     });
 }
 
@@ -333,9 +334,10 @@ int pyrit_plan_source(const pyrit_plan* plan, uint32_t lanes, char* buf, size_t 
         const bool staged = lanes == PYRIT_SOURCE_STAGED || lanes == PYRIT_SOURCE_STAGED + 1 ||
                             lanes == PYRIT_SOURCE_STAGED + 4 || lanes == PYRIT_SOURCE_STAGED + 8;
         if (lanes != 0 && lanes != 1 && lanes != 2 && lanes != 4 && !staged) raise(Errc::InvalidArgument, "bad lanes");
-        KernelShape ks = direct_shape(plan->prog, staged ? 1 : lanes);
+        const Program& fp = full_program(plan->prog);
+        KernelShape ks = direct_shape(fp, staged ? 1 : lanes);
         if (staged) {
-            ks = staged_shape(plan->prog, 227 * 1024);
+            ks = staged_shape(fp, 227 * 1024);
             if (!ks.staged) raise(Errc::BufferShape, "program tiles do not fit in shared memory");
             ks.chunk = lanes <= PYRIT_SOURCE_STAGED + 1 ? 16 : lanes - PYRIT_SOURCE_STAGED;
             if (ks.chunk != 16) ks.copy = 1; // TMA needs 16-byte alignment
@@ -346,8 +348,8 @@ int pyrit_plan_source(const pyrit_plan* plan, uint32_t lanes, char* buf, size_t 
                 ks.copy = c == 2 ? 2u : c ? 1u : 0u;
             }
         }
-        const std::string src = generate_cuda(plan->prog, ks);
-        const std::string nm = kernel_name(plan->prog, ks);
+        const std::string src = generate_cuda(fp, ks);
+        const std::string nm = kernel_name(fp, ks);
         if (len) *len = src.size();
         if (buf && cap) {
             const size_t n = std::min(cap - 1, src.size());
@@ -385,9 +387,10 @@ int pyrit_plan_interpret(const pyrit_plan* plan, const uint8_t* const* in, uint8
         }
         // PYRIT_B200_INTERPRET_GENERIC=1: evaluate the generic kernel's bitmatrix
         // (Program::field_masks) instead, so CPU tests pin what it computes
+        const Program& fp = full_program(plan->prog);
         const char* gen_env = std::getenv("PYRIT_B200_INTERPRET_GENERIC");
         if (gen_env && std::atoi(gen_env)) {
-            const Program& p = plan->prog;
+            const Program& p = fp;
             if (p.field_masks.empty()) raise(Errc::InvalidArgument, "no generic bitmatrix for this program");
             const std::uint32_t w = p.field.w;
             for (std::uint32_t i = 0; i < p.rows; ++i)
@@ -407,12 +410,12 @@ int pyrit_plan_interpret(const pyrit_plan* plan, const uint8_t* const* in, uint8
         // split kernels execute (rows part_row0[r] ..) instead of the whole
         // program, so CPU tests cover the part programs too
         const char* parts_env = std::getenv("PYRIT_B200_INTERPRET_PARTS");
-        if (parts_env && std::atoi(parts_env) && !plan->prog.parts.empty()) {
-            for (std::size_t r = 0; r < plan->prog.parts.size(); ++r)
-                interpret_program(plan->prog.parts[r], in, out + plan->prog.part_row0[r], strip_bytes, off, len);
+        if (parts_env && std::atoi(parts_env) && !fp.parts.empty()) {
+            for (std::size_t r = 0; r < fp.parts.size(); ++r)
+                interpret_program(fp.parts[r], in, out + fp.part_row0[r], strip_bytes, off, len);
             return;
         }
-        interpret_program(plan->prog, in, out, strip_bytes, off, len);
+        interpret_program(fp, in, out, strip_bytes, off, len);
     });
 }
 
@@ -437,7 +440,7 @@ int pyrit_cu_apply(const pyrit_plan* plan, const uint8_t* const* in, uint8_t* co
 int pyrit_cu_prepare(const pyrit_plan* plan) {
     return guarded([&] {
         if (!plan) raise(Errc::InvalidArgument, "null plan");
-        prepare_program(plan->prog, preferred_lanes());
+        prepare_program(full_program(plan->prog), preferred_lanes());
     });
 }
 

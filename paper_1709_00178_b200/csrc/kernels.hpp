@@ -36,11 +36,12 @@ struct alignas(64) RtArgs {
     std::uint8_t* out[2 * kRtPartE];     // output symbol bases of part p at [p*kRtPartE ..]
     std::uint64_t S, off, len, nb, obp;
     std::uint32_t k, tpb, ntiles, nslot, slot0; // slot0: byte offset of slot 0 in shared memory
+    std::uint32_t nops;                         // bytes of ops[] (op lists with their sentinels)
     std::uint32_t epart[2];              // outputs of each part
     std::uint32_t fm[256]; // Parity: fm[q*w + i] = ~0 when strip i feeds the parity strip w+q (i = q mod s)
-    // ops of input j for part p: ops[opoff[p][j] .. opoff[p][j+1]), each c = i*n + sh:
-    // output i of the part accumulates input j rotated by sh ring positions (a
-    // set bit of the representative of entry (i, j))
+    // op list of input j for part p: ops[opoff[p][j] ..], each c = i*n + sh
+    // (output i of the part accumulates input j rotated by sh ring positions, a
+    // set bit of the representative of entry (i, j)), terminated by E*n
     std::uint16_t opoff[2][kRtMaxK + 1];
     std::uint8_t ops[kRtMaxOps];
 };

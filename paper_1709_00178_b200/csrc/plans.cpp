@@ -10,21 +10,22 @@ namespace pyrit_b200 {
 
 namespace {
 
-class PlanCache {
+template <class T>
+class LruCache {
 public:
-    std::shared_ptr<const Program> get(const std::string& key) {
+    std::shared_ptr<const T> get(const std::string& key) {
         std::lock_guard<std::mutex> lk(mu_);
         auto it = map_.find(key);
         if (it == map_.end()) return nullptr;
         lru_.splice(lru_.begin(), lru_, it->second.second);
         return it->second.first;
     }
-    void put(const std::string& key, std::shared_ptr<const Program> p) {
+    void put(const std::string& key, std::shared_ptr<const T> p) {
         std::lock_guard<std::mutex> lk(mu_);
         if (map_.count(key)) return;
         lru_.push_front(key);
         map_[key] = {std::move(p), lru_.begin()};
-        while (map_.size() > 512) {
+        while (map_.size() > 4096) {
             map_.erase(lru_.back());
             lru_.pop_back();
         }
@@ -33,11 +34,16 @@ public:
 private:
     std::mutex mu_;
     std::list<std::string> lru_;
-    std::unordered_map<std::string, std::pair<std::shared_ptr<const Program>, std::list<std::string>::iterator>> map_;
+    std::unordered_map<std::string, std::pair<std::shared_ptr<const T>, std::list<std::string>::iterator>> map_;
 };
 
-PlanCache& cache() {
-    static PlanCache c;
+LruCache<Program>& cache() {
+    static LruCache<Program> c;
+    return c;
+}
+
+LruCache<DecodeProgram>& decode_cache() {
+    static LruCache<DecodeProgram> c;
     return c;
 }
 
@@ -62,6 +68,12 @@ std::shared_ptr<const Program> encode_program(const CodeParams& c) {
 }
 
 DecodeProgram decode_program(const CodeParams& c, const std::vector<std::uint32_t>& erased, bool data_only) {
+    // looked up by (code, erased list as given) before any algebra: a list that
+    // was valid once is valid again; an invalid one raises below and is never cached
+    std::string key(data_only ? "DD" : "D");
+    key += code_key(c);
+    key.append(reinterpret_cast<const char*>(erased.data()), erased.size() * sizeof(std::uint32_t));
+    if (auto d = decode_cache().get(key)) return *d;
     DecodeProgram d;
     d.repair = repair_matrix(c.k, c.r, c.field, erased);
     if (data_only) {
@@ -73,21 +85,11 @@ DecodeProgram decode_program(const CodeParams& c, const std::vector<std::uint32_
         d.repair.outputs.resize(nd);
         d.repair.m = std::move(m);
     }
-    if (d.repair.outputs.empty()) return d;
-    std::ostringstream key;
-    key << (data_only ? "DD" : "D") << code_key(c) << ':';
-    for (std::uint32_t o : d.repair.outputs) key << o << ',';
-    key << '/';
-    for (std::uint32_t s : d.repair.survivors) key << s << ',';
-    if (auto p = cache().get(key.str())) {
-        d.prog = p;
-        return d;
-    }
-    Program prog = compile_program(c.field, c.kind, d.repair.m, CompileOptions{});
-    prog.adhoc = true; // one of many erasure patterns: the runtime-matrix kernel serves it
-    auto p = std::make_shared<const Program>(std::move(prog));
-    cache().put(key.str(), p);
-    d.prog = p;
+    // one of many erasure patterns: a light program (representatives only)
+    // that the runtime-matrix ring kernel serves without compiling
+    if (!d.repair.outputs.empty())
+        d.prog = std::make_shared<const Program>(light_program(c.field, c.kind, d.repair.m));
+    decode_cache().put(key, std::make_shared<const DecodeProgram>(d));
     return d;
 }
 

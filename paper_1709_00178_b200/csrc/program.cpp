@@ -549,7 +549,48 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
         }
     }
     p.ir_hash = ir_hash_of(p);
+    p.key = plan_key(p);
     return p;
+}
+
+struct LazyCompile {
+    std::once_flag once;
+    std::shared_ptr<const Program> prog;
+};
+
+Program light_program(const Field& f, TransformKind kind, const Matrix& m) {
+    validate_field(f);
+    if (m.cols == 0) raise(Errc::InvalidArgument, "matrix has no columns");
+    Program p;
+    p.field = f;
+    p.kind = kind;
+    p.rows = m.rows;
+    p.cols = m.cols;
+    p.matrix = m.e;
+    p.fold = fold_table(f);
+    p.reps.resize(std::size_t(m.rows) * m.cols);
+    for (std::size_t i = 0; i < p.reps.size(); ++i) {
+        if (m.e[i] >= f.field_size()) raise(Errc::InvalidArgument, "matrix entry outside the field");
+        p.reps[i] = sparse_transform(m.e[i], f);
+        p.stats.matrix_ones += std::uint64_t(std::popcount(p.reps[i])) * f.w;
+    }
+    p.adhoc = true;
+    p.light = true;
+    p.key = plan_key(p);
+    p.lazy = std::make_shared<LazyCompile>();
+    return p;
+}
+
+const Program& full_program(const Program& p) {
+    if (!p.light) return p;
+    std::call_once(p.lazy->once, [&] {
+        Matrix m(p.rows, p.cols);
+        m.e = p.matrix;
+        Program q = compile_program(p.field, p.kind, m, CompileOptions{});
+        q.adhoc = true;
+        p.lazy->prog = std::make_shared<const Program>(std::move(q));
+    });
+    return *p.lazy->prog;
 }
 
 ScheduleProgram compile_schedule_program(const Field& f, std::uint32_t k, std::uint32_t outputs,

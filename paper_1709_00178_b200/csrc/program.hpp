@@ -19,6 +19,8 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -72,6 +74,12 @@ struct Program {
     // one of many programs of a code (a decode erasure pattern): served by the
     // runtime-matrix ring kernel, never compiled (runtime.cpp launch_batch)
     bool adhoc = false;
+    // light: only field, kind, shape, matrix, reps and fold are set (what the
+    // runtime-matrix kernel needs); full_program() compiles the rest on first
+    // use.  key = plan_key, computed once.
+    bool light = false;
+    std::string key;
+    std::shared_ptr<struct LazyCompile> lazy;
     std::uint64_t ir_hash = 0; // hash of every instruction list a kernel is generated from (code, parts):
                                // part of the kernel name, so a cached cubin never outlives its program
 };
@@ -107,6 +115,13 @@ const TunedEntry* find_tuned(const std::string& key);
 
 // compile_schedule analogue: matrix (rows x cols, GF(2^w) entries) -> program
 Program compile_program(const Field& f, TransformKind kind, const Matrix& m, const CompileOptions& opt);
+
+// A light ad-hoc program (decode patterns): representatives and fold only,
+// microseconds to build; full_program() compiles it (once, shared by copies)
+// when something needs the instruction lists -- a generated kernel, the
+// interpreter or the statistics.
+Program light_program(const Field& f, TransformKind kind, const Matrix& m);
+const Program& full_program(const Program& p);
 
 // One region op of a reference XorSchedule (schedule.hpp:40-48); mode is
 // OpMode: 0 Copy, 1 Xor, 2 Zero.

@@ -122,6 +122,10 @@ __global__ void __launch_bounds__(R * kRtCpp, R == 1 ? 2 : 1) ring_rt_kernel(con
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    // the op lists go to shared memory (after the barriers), where the
+    // threaded dispatch reads them one byte per op
+    const u32 ops_s = sbase + 16u * ns;
+    for (u32 i = threadIdx.x; i < a.nops; i += blockDim.x) sm[16u * ns + i] = a.ops[i];
     __syncthreads();
     // programmatic dependent launch: the setup above overlaps the previous
     // grid's tail; global memory is touched only after it has completed
@@ -182,19 +186,8 @@ __global__ void __launch_bounds__(R * kRtCpp, R == 1 ? 2 : 1) ring_rt_kernel(con
                         x[q][v] = p;
                     }
             }
-            // this part's op list of input j, the next op's byte loaded ahead of the jump
-            u32 q = opoff[j];
-            const u32 q1 = opoff[j + 1];
-            if (q < q1) {
-                u32 c = a.ops[q];
-#pragma unroll 1
-                for (++q; q < q1; ++q) {
-                    const u32 cn = a.ops[q];
-                    RtOps<W, N, E, V, PAR>::apply(c, acc, x);
-                    c = cn;
-                }
-                RtOps<W, N, E, V, PAR>::apply(c, acc, x);
-            }
+            // this part's op list of input j (shared memory, sentinel-terminated)
+            RtOps<W, N, E, V, PAR>::run(ops_s + opoff[j], acc, x);
         }
         const u64 rel = u64(tt) * TILE + col * (4u * V);
         const bool live = rel < a.len;

@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <fstream>
 #include <iterator>
+#include <memory>
 #include <mutex>
 #include <unordered_map>
 #include <type_traits>
@@ -447,6 +448,19 @@ std::string kernel_dir() {
     return g_kernel_dir;
 }
 
+bool prebuilt_plan(const std::string& key) {
+    static std::once_flag once;
+    static std::unordered_map<std::string, int>& keys = *new std::unordered_map<std::string, int>;
+    std::call_once(once, [] {
+        // kernels/prebuilt.tsv (build.py): plan keys of the programs whose
+        // specialised kernels ship prebuilt
+        std::ifstream f(kernel_dir() + "/prebuilt.tsv");
+        std::string k;
+        while (f >> k) keys[k] = 1;
+    });
+    return keys.count(key) != 0;
+}
+
 void jit_wait() {
     std::vector<std::shared_future<std::vector<char>>> pending;
     {
@@ -689,10 +703,29 @@ bool ring_rt_eligible(const Program& p, const std::uint8_t* const* in, std::uint
     return !unsafe_alias(p, in, out, strip, nb, in_pitch, out_pitch);
 }
 
-LaunchInfo launch_ring_rt_program(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
-                                  std::uint64_t strip, std::uint64_t off, std::uint64_t len, std::uint64_t nb,
-                                  std::uint64_t in_pitch, std::uint64_t out_pitch, cudaStream_t stream) {
-    thread_local RtArgs a; // ~17 KB of kernel parameters
+namespace {
+
+// The launches of one runtime-matrix call, kept per thread: a call with the same
+// program (plan key), buffers and window as the previous one reuses its kernel
+// parameters (tensor maps, op lists) and only launches.
+struct RtCall {
+    std::string key;
+    int dev = -1;
+    std::vector<const std::uint8_t*> in;
+    std::vector<std::uint8_t*> out;
+    std::uint64_t strip = 0, off = 0, len = 0, nb = 0, ip = 0, op = 0;
+    std::vector<std::unique_ptr<RtArgs>> args; // ~17 KB of kernel parameters each
+    std::vector<RtLaunch> launches;
+    LaunchInfo info;
+};
+
+void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
+                   std::uint64_t strip, std::uint64_t off, std::uint64_t len, std::uint64_t nb, std::uint64_t in_pitch,
+                   std::uint64_t out_pitch) {
+    call.args.clear();
+    call.launches.clear();
+    RtArgs tmpl;
+    RtArgs& a = tmpl;
     const std::uint32_t w = p.field.w, n = p.field.n, k = p.cols;
     const std::uint32_t ep = static_cast<std::uint32_t>(rt_part_outputs(static_cast<int>(n)));
     const std::uint32_t tile = kRtTile, elem = 8, slot = w * tile;
@@ -729,7 +762,6 @@ LaunchInfo launch_ring_rt_program(const Program& p, const std::uint8_t* const* i
     l.n = n;
     l.modulus = p.field.modulus;
     l.parity = par;
-    l.stream = stream;
     static const bool pdl = env_int("PYRIT_B200_PDL", 1) != 0;
     l.pdl = pdl;
     // Outputs go to two parts of 256 threads (16 warps per SM); a single output
@@ -743,18 +775,7 @@ LaunchInfo launch_ring_rt_program(const Program& p, const std::uint8_t* const* i
         a.epart[0] = std::min(l.E, e);
         a.epart[1] = e - a.epart[0];
         const std::uint32_t ctas_per_sm = l.R == 1 ? 2 : 1;
-        // shared-memory ring: mbarriers, then as many fragment slots as fit (<= 32)
-        std::uint32_t ns = 32, bar = 0;
-        const std::uint32_t budget = (ctas_per_sm == 2 ? 113 : 227) * 1024;
-        for (; ns >= 2; --ns) {
-            bar = (16 * ns + 127) / 128 * 128;
-            if (bar + ns * slot <= budget) break;
-        }
-        a.nslot = ns;
-        a.slot0 = bar;
-        l.smem = bar + ns * slot;
-        l.blocks = static_cast<unsigned>(
-            std::max<std::uint64_t>(1, std::min<std::uint64_t>(tpb * nb, std::uint64_t(ctas_per_sm) * sm_count())));
+        // op lists, one per (part, input), each ended by the sentinel E*n
         std::uint32_t nops = 0;
         for (std::uint32_t part = 0; part < 2; ++part) {
             const std::uint32_t b0 = i0 + part * l.E, ne = a.epart[part];
@@ -762,23 +783,74 @@ LaunchInfo launch_ring_rt_program(const Program& p, const std::uint8_t* const* i
                 a.opoff[part][j] = static_cast<std::uint16_t>(nops);
                 for (std::uint32_t i = 0; i < ne; ++i)
                     for (std::uint32_t m = p.reps[std::size_t(b0 + i) * k + j]; m; m &= m - 1) {
-                        if (nops >= kRtMaxOps) raise(Errc::InvalidArgument, "ring_rt: too many ring terms per launch");
+                        if (nops + 2 >= kRtMaxOps) raise(Errc::InvalidArgument, "ring_rt: too many ring terms per launch");
                         a.ops[nops++] = static_cast<std::uint8_t>(i * n + static_cast<std::uint32_t>(std::countr_zero(m)));
                     }
+                a.ops[nops++] = static_cast<std::uint8_t>(l.E * n);
             }
             a.opoff[part][k] = static_cast<std::uint16_t>(nops);
             for (std::uint32_t i = 0; i < ne; ++i) a.out[part * kRtPartE + i] = out[b0 + i];
         }
-        check_cuda(launch_ring_rt(a, l), "ring_rt launch");
-        ++g_launches;
+        a.ops[nops] = 0; // the byte the last list's look-ahead reads
+        a.nops = nops + 1;
+        // shared memory: mbarriers, op lists, then as many fragment slots as fit (<= 32)
+        std::uint32_t ns = 32, bar = 0;
+        const std::uint32_t budget = (ctas_per_sm == 2 ? 113 : 227) * 1024;
+        for (; ns >= 2; --ns) {
+            bar = (16 * ns + a.nops + 127) / 128 * 128;
+            if (bar + ns * slot <= budget) break;
+        }
+        a.nslot = ns;
+        a.slot0 = bar;
+        l.smem = bar + ns * slot;
+        l.blocks = static_cast<unsigned>(
+            std::max<std::uint64_t>(1, std::min<std::uint64_t>(tpb * nb, std::uint64_t(ctas_per_sm) * sm_count())));
+        call.args.push_back(std::make_unique<RtArgs>(a));
+        call.launches.push_back(l);
         info.blocks = l.blocks;
         info.threads = l.R * kRtCpp;
     }
     info.kernel = "pyrit_ring_rt_w" + std::to_string(w) + "_n" + std::to_string(n) + (par ? "_par" : "");
     info.lanes = 2;
     info.staged = true;
-    g_last = info;
-    return info;
+    call.info = info;
+}
+
+} // namespace
+
+LaunchInfo launch_ring_rt_program(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
+                                  std::uint64_t strip, std::uint64_t off, std::uint64_t len, std::uint64_t nb,
+                                  std::uint64_t in_pitch, std::uint64_t out_pitch, cudaStream_t stream) {
+    thread_local RtCall last;
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    bool same = !p.key.empty() && last.key == p.key && last.dev == dev && last.strip == strip && last.off == off &&
+                last.len == len && last.nb == nb && last.ip == in_pitch && last.op == out_pitch &&
+                last.in.size() == p.cols && last.out.size() == p.rows;
+    for (std::uint32_t j = 0; same && j < p.cols; ++j) same = last.in[j] == in[j];
+    for (std::uint32_t i = 0; same && i < p.rows; ++i) same = last.out[i] == out[i];
+    if (!same) {
+        last.key.clear(); // invalid until fully built
+        build_ring_rt(last, p, in, out, strip, off, len, nb, in_pitch, out_pitch);
+        last.key = p.key;
+        last.dev = dev;
+        last.strip = strip;
+        last.off = off;
+        last.len = len;
+        last.nb = nb;
+        last.ip = in_pitch;
+        last.op = out_pitch;
+        last.in.assign(in, in + p.cols);
+        last.out.assign(out, out + p.rows);
+    }
+    for (std::size_t c = 0; c < last.launches.size(); ++c) {
+        RtLaunch l = last.launches[c];
+        l.stream = stream;
+        check_cuda(launch_ring_rt(*last.args[c], l), "ring_rt launch");
+        ++g_launches;
+    }
+    g_last = last.info;
+    return last.info;
 }
 
 std::string prepare_program(const Program& p, std::uint32_t lanes) {
@@ -798,7 +870,7 @@ LaunchInfo launch_program(const Program& p, const std::uint8_t* const* in, std::
     return launch_batch(p, in, out, strip, off, len, 1, 0, 0, stream);
 }
 
-LaunchInfo launch_batch(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
+LaunchInfo launch_batch(const Program& p0, const std::uint8_t* const* in, std::uint8_t* const* out,
                         std::uint64_t strip, std::uint64_t off, std::uint64_t len, std::uint64_t nb,
                         std::uint64_t in_pitch, std::uint64_t out_pitch, cudaStream_t stream) {
     LaunchInfo info;
@@ -809,9 +881,15 @@ LaunchInfo launch_batch(const Program& p, const std::uint8_t* const* in, std::ui
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
     const int mode = kernel_mode();
     const bool rt_ok = mode != 3 && rt_policy() != 0 &&
-                       ring_rt_eligible(p, in, out, strip, off, len, nb, in_pitch, out_pitch);
+                       ring_rt_eligible(p0, in, out, strip, off, len, nb, in_pitch, out_pitch);
     if (rt_ok && (mode == 4 || rt_policy() == 2))
-        return launch_ring_rt_program(p, in, out, strip, off, len, nb, in_pitch, out_pitch, stream);
+        return launch_ring_rt_program(p0, in, out, strip, off, len, nb, in_pitch, out_pitch, stream);
+    // a light (decode-pattern) program stays on the runtime-matrix kernel unless
+    // a specialised kernel was prebuilt for it (the benchmarked patterns) or a
+    // kernel mode asks for the generated kernels
+    if (p0.light && rt_ok && mode == 0 && !prebuilt_plan(p0.key))
+        return launch_ring_rt_program(p0, in, out, strip, off, len, nb, in_pitch, out_pitch, stream);
+    const Program& p = full_program(p0);
     const KernelShape ks = choose_shape(p, in, out, strip, off, len, nb, in_pitch, out_pitch);
     const bool gen_ok = generic_ok(p, in, out, strip, off, len, nb, in_pitch, out_pitch) &&
                         !unsafe_alias(p, in, out, strip, nb, in_pitch, out_pitch);

@@ -51,6 +51,10 @@ std::string prepare_program(const Program& p, std::uint32_t lanes);
 std::uint32_t preferred_lanes();
 void set_preferred_lanes(std::uint32_t lanes);
 
+// Is plan_key `key` one of the programs with a prebuilt specialised kernel
+// (kernels/prebuilt.tsv, written by build.py)?
+bool prebuilt_plan(const std::string& key);
+
 // Directory searched for prebuilt <kernel>.cubin files.
 void set_kernel_dir(const std::string& dir);
 std::string kernel_dir();

@@ -130,10 +130,12 @@ def test_generic_baseline_shapes_and_batches(cuda, generic):
                 assert np.array_equal(got[b, i], want[i]), (cfg, b, i)
 
 
-def test_tiered_compilation(cuda, tmp_path):
-    """A code with no prebuilt or cached kernel: the first launch runs the generic kernel while the
-    specialised one compiles in the background; after pyrit_jit_wait() the next launch runs the
-    specialised kernel. Both give the oracle's bytes."""
+@pytest.mark.parametrize("rt", ["1", "0"])
+def test_tiered_compilation(cuda, tmp_path, rt):
+    """A code with no prebuilt or cached kernel: the first launch runs the runtime-matrix ring kernel
+    (PYRIT_B200_RT=0: the generic bit-matrix kernel) while the specialised one compiles in the
+    background; after pyrit_jit_wait() the next launch runs the specialised kernel. Both give the
+    oracle's bytes."""
     script = textwrap.dedent("""
         import time, numpy as np, torch
         import oracle as O
@@ -156,18 +158,19 @@ def test_tiered_compilation(cuda, tmp_path):
             torch.cuda.synchronize()
             kernels.append(P.Plan.last_launch()["kernel"])
             ok.append(bool(np.array_equal(p.cpu().numpy(), want)))
-            if kernels[-1] != "pyrit_generic_bitmatrix":
+            if kernels[-1] != "pyrit_generic_bitmatrix" and not kernels[-1].startswith("pyrit_ring_rt_"):
                 break
             time.sleep(0.5)
         print(kernels[0], kernels[1], all(ok), L.load().pyrit_jit_compiles())
     """)
-    env = dict(os.environ, PYRIT_B200_TIERED="1", PYRIT_B200_JIT_CACHE=str(tmp_path))
+    env = dict(os.environ, PYRIT_B200_TIERED="1", PYRIT_B200_JIT_CACHE=str(tmp_path), PYRIT_B200_RT=rt)
     r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, cwd=ROOT,
                        timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     first, second, ok, jit = r.stdout.split()[-4:]
     # the launch right after pyrit_jit_wait() already runs the specialised kernel
-    assert first == "pyrit_generic_bitmatrix" and second.startswith("pyrit_ring_"), r.stdout
+    stand_in = "pyrit_ring_rt_w10_n11" if rt == "1" else "pyrit_generic_bitmatrix"
+    assert first == stand_in and second.startswith("pyrit_ring_k"), r.stdout
     assert ok == "True" and int(jit) == 1
 
 
@@ -187,4 +190,4 @@ def test_exit_while_compiling(cuda, tmp_path):
     r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, cwd=ROOT,
                        timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
-    assert r.stdout.split()[-1] == "pyrit_generic_bitmatrix"
+    assert r.stdout.split()[-1] == "pyrit_ring_rt_w12_n13"
