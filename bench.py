@@ -124,9 +124,14 @@ def cpu_baseline(wl, steps=None, warmup=1, budget_s=12.0, sample_frag=None):
         plan = None
     if plan is None:
         return None
-    rng = np.random.default_rng(wl.seed)
+    # seeded bytes: a 16 MiB block of uniform bytes tiled over every symbol (the
+    # CPU kernel's speed does not depend on the values; filling 10 GiB of full
+    # config-5 buffers byte by byte from the generator would dominate the run)
+    blk = np.frombuffer(np.random.default_rng(wl.seed).bytes(min(frag, 16 << 20)), dtype=np.uint8)
     for s in range(wl.k + wl.m):
-        plan.symbol(s)[:] = rng.integers(0, 256, frag, dtype=np.uint8)
+        v = plan.symbol(s)
+        for o in range(0, frag, blk.size):
+            v[o:o + blk.size] = blk[: min(blk.size, frag - o)]
     for _ in range(warmup):
         plan.run(threads)
     times = []
@@ -158,7 +163,7 @@ def cpu_baseline(wl, steps=None, warmup=1, budget_s=12.0, sample_frag=None):
     extra = {"value_1_thread": src / min(t1) / 1e9} if t1 else {}
     # the reference bench's own convention counts (k + r) * F bytes (bench.hpp:205-207)
     extra["value_kr_convention"] = (wl.k + wl.m) * frag / t / 1e9
-    return {"value": src / t / 1e9, "unit": "GB/s", "cores": threads, "kind": kind, **extra,
+    return {"value": src / t / 1e9, "unit": "GB/s", "cores": threads, "kind": kind, **extra, "fragment_bytes": frag,
             "sample": f"{wl.k}x{frag}-byte fragments ({src / 2**20:.0f} MiB source) of the {wl.name} shape, "
                       f"{names[mode]}, {threads} threads, median of {len(times)} runs",
             "times_s": [round(x, 5) for x in times]}
@@ -169,7 +174,9 @@ def run_reference(args, rank, world):
     if rank != 0:
         return 0
     wl = WORKLOADS[args.config]
-    res = cpu_baseline(wl, steps=args.steps, warmup=args.warmup)
+    # the full BASELINE workload every step (same_config): config 5 is 8 GiB of
+    # source per parallel_replay pass, ~2 s on the box's 16 host threads
+    res = cpu_baseline(wl, steps=args.steps, warmup=min(args.warmup, 1), sample_frag=wl.frag)
     if res is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpyrit_ref.so not built"}))
         return 0
@@ -178,11 +185,49 @@ def run_reference(args, rank, world):
     line = {"metric": METRIC, "value": res["value"], "unit": "GB/s", "n_gpus": world, "steps": len(times),
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded uniform bytes)",
-            "config": {"workload": wl.name, "sample_of_full_workload": True}, "impl": "reference",
+            "config": {"workload": wl.name, "fragment_bytes": res.get("fragment_bytes"),
+                       "same_config": res.get("fragment_bytes") == wl.frag}, "impl": "reference",
             "cpu_baseline": res,
             "e2e": {"value": res["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def dry_run(args, rank, world) -> int:
+    """PYRIT_B200_BENCH_DRYRUN=1: the rank plumbing only (no GPU work), on gloo --
+    what tests/test_bench_cli.py checks on CPU: every rank joins one group."""
+    import torch
+    import torch.distributed as dist
+    n = 1
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.ones(1)
+        dist.all_reduce(t)
+        n = int(t.item())
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"dryrun": True, "world_size": world, "comm_nranks": n, "requested_gpus": args.gpus,
+                          "spawned_by_bench": os.environ.get("PYRIT_B200_SPAWNED") == "1"}), flush=True)
+    return 0
+
+
+def spawn_ranks(n: int, argv) -> int:
+    """`bench.py --gpus N` without torchrun: launch N ranks of this script with
+    torch.distributed.run on 127.0.0.1 (one process per GPU, NCCL); rank 0's
+    JSON line is this process's output.  NCCL's init log goes to stderr."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    if env.get("PYRIT_B200_DIST_BACKEND", "nccl") == "nccl" and env.get("PYRIT_B200_BENCH_DRYRUN") != "1":
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    env["PYRIT_B200_SPAWNED"] = "1"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *argv]
+    print("bench.py: spawning", n, "ranks:", " ".join(cmd), file=sys.stderr, flush=True)
+    return subprocess.run(cmd, env=env).returncode
 
 
 def main(argv=None):
@@ -199,11 +244,17 @@ def main(argv=None):
     ap.add_argument("--no-graph", action="store_true", help="launch the timed steps from Python")
     args = ap.parse_args(argv)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "b200":
+        # one process per GPU: re-run this command under torchrun (the driver may
+        # launch `bench.py --gpus N` directly or under torchrun itself)
+        return spawn_ranks(args.gpus, sys.argv[1:] if argv is None else list(argv))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        return run_reference(args, rank, world)
+        return run_reference(args, rank, max(world, args.gpus))
+    if os.environ.get("PYRIT_B200_BENCH_DRYRUN") == "1":
+        return dry_run(args, rank, world)
     if args.warmup < 3:
         args.warmup = 3  # contract: at least 3 warm-up steps
 
@@ -230,6 +281,17 @@ def main(argv=None):
         else:
             dist.init_process_group(backend)
     cdev = dev if backend == "nccl" else torch.device("cpu")  # where collective tensors live
+    ranks = {"world_size": world, "requested_gpus": args.gpus, "backend": backend if world > 1 else None,
+             "spawned_by_bench": os.environ.get("PYRIT_B200_SPAWNED") == "1"}
+    if world > 1:
+        one = torch.ones(1, dtype=torch.float64, device=cdev)
+        dist.all_reduce(one)  # every rank joined the communicator
+        ranks["comm_nranks"] = int(one.item())
+        dl = [None] * world
+        dist.all_gather_object(dl, {"rank": rank, "device": torch.cuda.current_device(),
+                                    "name": torch.cuda.get_device_name(dev)})
+        ranks["devices"] = dl
+    ranks["ok"] = world == args.gpus and ranks.get("comm_nranks", 1) == world
     lib = L.load()
     if args.lanes:
         L.check(lib.pyrit_set_lanes(args.lanes))
@@ -326,11 +388,15 @@ def main(argv=None):
     # digests of repaired vs original bytes must match on every rank (K3 digests
     # gathered over NCCL -- the only collective, verification only).
     verified = verify(P, wl, plan, sets[0], sym, Ls, dev, stream, world)
+    refcheck = verify_reference(wl, plan, sets[0], sym, Ls, dev, world)
 
     # ---- end to end through the public host-buffer API
     e2e = None
+    e2e_dev = None
     if not args.no_e2e:
         e2e = run_e2e(P, wl, sets[0], sym, Ls, dev, world, args.e2e_steps or min(args.steps, 10))
+        if world > 1:
+            e2e_dev = run_e2e_devices(P, wl, world, rank, args.e2e_steps or min(args.steps, 10))
 
     peak, peak_src = measured_peaks()
     alg_bytes = (n_in + n_out) * sym
@@ -366,8 +432,12 @@ def main(argv=None):
                          "algorithmic_bytes_per_launch": alg_bytes, "launch_ms": ms,
                          "frac_of_8TBps_nominal": achieved / 8000.0},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": int(launches),
-            "verified": verified,
+            "verified": bool(refcheck["identical"]) if refcheck.get("identical") is not None else verified,
+            "verification": {"reference": refcheck, "repair_round_trip": verified},
+            "ranks": ranks,
         }
+        if e2e_dev is not None:
+            line["e2e_devices"] = e2e_dev
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -407,6 +477,106 @@ def verify(P, wl, plan, s0, sym, Ls, dev, stream, world):
         dg = torch.stack(allg)
     dg = dg.view(-1, 2, len(ref))
     return bool(ok and torch.equal(dg[:, 0], dg[:, 1]))
+
+
+def verify_reference(wl, plan, s0, sym, Ls, dev, world):
+    """Every output byte of this rank's shard against the reference's own CPU
+    output on the same input bytes: oracle/_ref (the unmodified reference
+    headers), parallel_replay of the reference's schedule over all host threads
+    -- the ring schedule for AOP fields, the CRS schedule for R_{2,17} where the
+    reference's ring path is wrong; for decode, decode() restated
+    over the survivors the GPU decoded from.  Outside the timed region."""
+    import numpy as np
+    import torch
+    try:
+        import oracle as O
+        f = O.Field(wl.fld.w, wl.fld.n, wl.fld.kind, wl.fld.s, wl.fld.r_esp or wl.fld.w, wl.fld.modulus)
+        aop_esp = wl.fld.n <= 16
+        mode = (0 if aop_esp else 1) if wl.op == "encode" else (3 if aop_esp else 2)
+        ref = O.RefPlan(f, wl.k, wl.m, mode, sym, wl.erased)
+    except Exception as e:  # no reference build on this box
+        return {"identical": None, "why": f"reference unavailable: {e}"}
+    t0 = time.perf_counter()
+    try:
+        full = s0[2]
+        if wl.op == "encode":
+            for j in range(wl.k):
+                torch.from_numpy(ref.symbol(j)).copy_(full[j])
+            outs = list(range(wl.k, wl.k + wl.m))
+            gpu = {wl.k + i: s0[3][i] for i in range(wl.m)}
+        else:
+            # the GPU repaired full[outputs] in place from full[survivors]
+            for s in plan.survivors:
+                torch.from_numpy(ref.symbol(s)).copy_(full[s])
+            outs = list(plan.outputs)
+            gpu = {o: full[o] for o in outs}
+        torch.cuda.synchronize(dev)
+        ref.run(os.cpu_count() or 1)
+        same = True
+        host = torch.empty(sym, dtype=torch.uint8, pin_memory=True)
+        for o in outs:
+            host.copy_(gpu[o])
+            same &= bool(np.array_equal(host.numpy(), ref.symbol(o)))
+        return {"identical": same, "bytes_compared": len(outs) * sym,
+                "reference": ("ring schedule" if mode in (0, 3) else "CRS schedule") + " parallel_replay"
+                             + (" + decode()" if wl.op == "decode" else ""),
+                "threads": os.cpu_count(), "seconds": round(time.perf_counter() - t0, 2),
+                "scope": f"rank shard: {len(outs)} outputs x {sym} bytes"}
+    finally:
+        ref.close()
+
+
+def run_e2e_devices(P, wl, world, rank, steps):
+    """The library's own multi-device path: rank 0 calls pyrit_encode_host_devices /
+    pyrit_decode_host_devices over devices 0..N-1 on the WHOLE workload (byte-offset
+    shards, one host thread + staging ring per device) while the other ranks wait."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    res = None
+    if rank == 0:
+        try:
+            sym = wl.frag
+            devs = [i % torch.cuda.device_count() for i in range(world)]  # gloo harness: ranks share GPUs
+            blk = np.frombuffer(np.random.default_rng(wl.seed).bytes(16 << 20), dtype=np.uint8)
+            if wl.op == "encode":
+                host_in = torch.empty((wl.k, sym), dtype=torch.uint8, pin_memory=True)
+                host_out = torch.empty((wl.m, sym), dtype=torch.uint8, pin_memory=True)
+                a_in, a_out = host_in.numpy(), host_out.numpy()
+                flat = a_in.reshape(-1)
+                for o in range(0, flat.size, blk.size):
+                    flat[o:o + blk.size] = blk[: min(blk.size, flat.size - o)]
+
+                def call():
+                    P.encode_host(a_in, wl.code, parity=a_out, devices=devs)
+                h2d, d2h = wl.k * sym, wl.m * sym
+            else:
+                host = torch.empty((wl.k + wl.m, sym), dtype=torch.uint8, pin_memory=True)
+                a = host.numpy()
+                flat = a.reshape(-1)
+                for o in range(0, flat.size, blk.size):
+                    flat[o:o + blk.size] = blk[: min(blk.size, flat.size - o)]
+
+                def call():
+                    P.decode_host(a, wl.erased, wl.code, devices=devs)
+                h2d, d2h = wl.k * sym, len(wl.erased) * sym
+            call()
+            times = []
+            for _ in range(max(2, steps // 2)):
+                t0 = time.perf_counter()
+                call()
+                times.append(time.perf_counter() - t0)
+            t = statistics.median(times)
+            res = {"value": wl.source_bytes() / t / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": d2h, "ms_per_step": t * 1e3, "steps": len(times),
+                   "api": ("pyrit_encode_host_devices" if wl.op == "encode" else "pyrit_decode_host_devices")
+                          + f" over devices {devs} from rank 0 (one process)",
+                   "data": "16 MiB seeded block tiled (pinned host buffers)"}
+            del flat
+        except Exception as e:
+            res = {"error": str(e)[:300]}
+    dist.barrier()
+    return res
 
 
 def run_e2e(P, wl, s0, sym, Ls, dev, world, steps):
