@@ -242,6 +242,8 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--no-graph", action="store_true", help="launch the timed steps from Python")
+    ap.add_argument("--erased", default="", help="decode configs: erased symbols, e.g. 0,1,2,3 (config 4's "
+                                                 "all-data worst case; default: the BASELINE pattern)")
     args = ap.parse_args(argv)
 
     if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "b200":
@@ -296,6 +298,10 @@ def main(argv=None):
     if args.lanes:
         L.check(lib.pyrit_set_lanes(args.lanes))
     wl = WORKLOADS[args.config]
+    if args.erased and wl.op == "decode":
+        import dataclasses
+        er = tuple(int(x) for x in args.erased.split(","))
+        wl = dataclasses.replace(wl, erased=er, name=wl.name.rsplit("-e", 1)[0] + "-e" + ",".join(map(str, er)))
     w = wl.fld.w
     lo, hi = shard(wl.strip, rank, world)
     Ls = hi - lo

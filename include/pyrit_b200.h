@@ -119,6 +119,12 @@ int pyrit_plan_encode(const pyrit_code* code, pyrit_plan** out);
 int pyrit_plan_decode(const pyrit_code* code, const uint32_t* erased, uint32_t n_erased, pyrit_plan** out,
                       uint32_t* survivors, uint32_t* outputs);
 int pyrit_plan_get_stats(const pyrit_plan* plan, pyrit_plan_stats* out);
+/* Negative control (the reference's hidden `pyrit verify --inject-theta-fault`,
+ * tools/pyrit.cpp:281-282, selfcheck.hpp:28-34, flips one bit of the embedding
+ * idempotent): flip bit `bit` of the ring representative of matrix entry
+ * `entry` (row-major) and recompile the plan, so that tests can show the GPU
+ * parity checks detect a wrong program.  Test hook; never used by the codec. */
+int pyrit_plan_inject_fault(pyrit_plan* plan, uint32_t entry, uint32_t bit);
 int pyrit_plan_reps(const pyrit_plan* plan, uint32_t* reps /* rows x cols */);
 /* key of the plan in the staged-kernel tuning table (tuned.tsv next to the library) */
 int pyrit_plan_key(const pyrit_plan* plan, char* buf, size_t cap);

@@ -309,6 +309,11 @@ class Plan:
         L.check(_clib().pyrit_cu_apply_batch(self._h, _ptr_array(list(in_ptrs)), _ptr_array(list(out_ptrs)), strip,
                                             off, length, stripes, in_pitch, out_pitch, stream))
 
+    def inject_fault(self, entry: int, bit: int) -> None:
+        """Negative control (tools/pyrit.cpp:281-282 --inject-theta-fault): flip bit `bit` of the ring
+        representative of matrix entry `entry` and recompile; the plan is then WRONG on purpose."""
+        L.check(_clib().pyrit_plan_inject_fault(self._h, entry, bit))
+
     def prepare(self) -> None:
         L.check(_clib().pyrit_cu_prepare(self._h))
 

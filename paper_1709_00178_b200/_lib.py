@@ -49,7 +49,7 @@ EXPORTS = (
     "pyrit_version", "pyrit_strerror", "pyrit_field_named", "pyrit_field_validate", "pyrit_gf_mul", "pyrit_gf_inv",
     "pyrit_sparse_transform", "pyrit_fold_table", "pyrit_cauchy_parity_matrix", "pyrit_decode_matrix",
     "pyrit_repair_matrix", "pyrit_plan_create", "pyrit_plan_encode", "pyrit_plan_decode", "pyrit_plan_get_stats",
-    "pyrit_plan_reps", "pyrit_plan_key", "pyrit_plan_source", "pyrit_plan_interpret", "pyrit_plan_destroy", "pyrit_cu_apply",
+    "pyrit_plan_reps", "pyrit_plan_inject_fault", "pyrit_plan_key", "pyrit_plan_source", "pyrit_plan_interpret", "pyrit_plan_destroy", "pyrit_cu_apply",
     "pyrit_cu_prepare", "pyrit_cu_encode", "pyrit_cu_decode", "pyrit_encode_host", "pyrit_decode_host",
     "pyrit_set_host_chunk", "pyrit_cu_fill", "pyrit_cu_digest", "pyrit_set_lanes", "pyrit_set_kernel_mode", "pyrit_set_kernel_dir",
     "pyrit_cu_last_launch", "pyrit_jit_compiles", "pyrit_kernel_launches", "pyrit_cu_apply_batch",
@@ -89,6 +89,7 @@ def load():
     lib.pyrit_plan_get_stats.argtypes = [vp, P(pyrit_plan_stats)]
     lib.pyrit_plan_reps.argtypes = [vp, vp]
     lib.pyrit_plan_key.argtypes = [vp, vp, C.c_size_t]
+    lib.pyrit_plan_inject_fault.argtypes = [vp, u32, u32]
     lib.pyrit_plan_source.argtypes = [vp, u32, vp, C.c_size_t, P(C.c_size_t), vp, C.c_size_t]
     lib.pyrit_plan_interpret.argtypes = [vp, vp, vp, u64, u64, u64]
     lib.pyrit_plan_destroy.argtypes = [vp]

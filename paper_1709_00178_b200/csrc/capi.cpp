@@ -320,6 +320,22 @@ int pyrit_plan_key(const pyrit_plan* plan, char* buf, size_t cap) {
     });
 }
 
+int pyrit_plan_inject_fault(pyrit_plan* plan, uint32_t entry, uint32_t bit) {
+    return guarded([&] {
+        if (!plan) raise(Errc::InvalidArgument, "null plan");
+        const Program& fp = full_program(plan->prog);
+        if (plan->sched || fp.crs) raise(Errc::InvalidArgument, "fault injection applies to ring programs");
+        if (entry >= fp.reps.size() || bit >= fp.field.n) raise(Errc::InvalidArgument, "no such representative bit");
+        std::vector<uint32_t> reps = fp.reps;
+        reps[entry] ^= 1u << bit;
+        Matrix m(fp.rows, fp.cols);
+        m.e = fp.matrix;
+        CompileOptions opt;
+        opt.reps = &reps;
+        plan->prog = compile_program(fp.field, fp.kind, m, opt);
+    });
+}
+
 int pyrit_plan_reps(const pyrit_plan* plan, uint32_t* reps) {
     return guarded([&] {
         if (!plan || !reps) raise(Errc::InvalidArgument, "null argument");

@@ -7,6 +7,7 @@
 
 #include <immintrin.h>
 
+#include <cstdio>
 #include <cstring>
 
 #include "hostpool.hpp"
@@ -293,28 +294,76 @@ void run_host_window(const Program& p, const std::vector<const std::uint8_t*>& h
     }
     std::vector<const std::uint8_t*> din(p.cols);
     std::vector<std::uint8_t*> dout(p.rows);
+    // PYRIT_B200_PIPE_TRACE=<file>: CUDA events around every chunk's H2D, kernel
+    // and D2H, written as a timeline (ms from the first event) -- the copy-engine
+    // overlap evidence nsys would give (nsys is not on these boxes)
+    static const char* trace_path = std::getenv("PYRIT_B200_PIPE_TRACE");
+    struct Ev {
+        cudaEvent_t e[4];
+        int slot;
+        std::uint64_t bytes_in, bytes_out;
+    };
+    std::vector<Ev> trace;
     std::uint64_t c0 = off;
-    for (int c = 0; c0 < off + win; ++c) {
-        const std::uint64_t len = std::min(chunk, off + win - c0);
-        Slot& s = ctx.slots[c % kSlots];
-        for (std::uint32_t j = 0; j < p.cols; ++j) din[j] = s.buf + std::uint64_t(j) * w * chunk;
-        for (std::uint32_t i = 0; i < p.rows; ++i) dout[i] = s.buf + std::uint64_t(p.cols + i) * w * chunk;
-        for (const auto& [j0, j1] : in_runs)
-            check_cuda(cudaMemcpy2DAsync(const_cast<std::uint8_t*>(din[j0]), chunk, host_in[j0] + c0, strip, len,
-                                         std::size_t(j1 - j0) * w, cudaMemcpyHostToDevice, s.stream),
-                       "H2D");
-        launch_program(p, din.data(), dout.data(), chunk, 0, len, s.stream);
-        for (const auto& [i0, i1] : out_runs)
-            check_cuda(cudaMemcpy2DAsync(host_out[i0] + c0, strip, dout[i0], chunk, len, std::size_t(i1 - i0) * w,
-                                         cudaMemcpyDeviceToHost, s.stream),
-                       "D2H");
-        for (const auto& [i, b] : partial)
-            check_cuda(cudaMemcpyAsync(host_out[i] + std::uint64_t(b) * strip + c0, dout[i] + std::uint64_t(b) * chunk,
-                                       len, cudaMemcpyDeviceToHost, s.stream),
-                       "D2H");
-        c0 += len;
+    try {
+        for (int c = 0; c0 < off + win; ++c) {
+            const std::uint64_t len = std::min(chunk, off + win - c0);
+            Slot& s = ctx.slots[c % kSlots];
+            for (std::uint32_t j = 0; j < p.cols; ++j) din[j] = s.buf + std::uint64_t(j) * w * chunk;
+            for (std::uint32_t i = 0; i < p.rows; ++i) dout[i] = s.buf + std::uint64_t(p.cols + i) * w * chunk;
+            Ev ev{};
+            if (trace_path) {
+                for (auto& e : ev.e) check_cuda(cudaEventCreate(&e), "trace event");
+                ev.slot = c % kSlots;
+                ev.bytes_in = std::uint64_t(p.cols) * w * len;
+                ev.bytes_out = std::uint64_t(p.rows) * w * len;
+                check_cuda(cudaEventRecord(ev.e[0], s.stream), "trace");
+            }
+            for (const auto& [j0, j1] : in_runs)
+                check_cuda(cudaMemcpy2DAsync(const_cast<std::uint8_t*>(din[j0]), chunk, host_in[j0] + c0, strip, len,
+                                             std::size_t(j1 - j0) * w, cudaMemcpyHostToDevice, s.stream),
+                           "H2D");
+            if (trace_path) check_cuda(cudaEventRecord(ev.e[1], s.stream), "trace");
+            launch_program(p, din.data(), dout.data(), chunk, 0, len, s.stream);
+            if (trace_path) check_cuda(cudaEventRecord(ev.e[2], s.stream), "trace");
+            for (const auto& [i0, i1] : out_runs)
+                check_cuda(cudaMemcpy2DAsync(host_out[i0] + c0, strip, dout[i0], chunk, len, std::size_t(i1 - i0) * w,
+                                             cudaMemcpyDeviceToHost, s.stream),
+                           "D2H");
+            for (const auto& [i, b] : partial)
+                check_cuda(cudaMemcpyAsync(host_out[i] + std::uint64_t(b) * strip + c0,
+                                           dout[i] + std::uint64_t(b) * chunk, len, cudaMemcpyDeviceToHost, s.stream),
+                           "D2H");
+            if (trace_path) {
+                check_cuda(cudaEventRecord(ev.e[3], s.stream), "trace");
+                trace.push_back(ev);
+            }
+            c0 += len;
+        }
+        for (Slot& s : ctx.slots) check_cuda(cudaStreamSynchronize(s.stream), "cudaStreamSynchronize");
+    } catch (...) {
+        // no copy may outlive the caller's buffers (a later chunk's launch or copy failed)
+        for (Slot& s : ctx.slots) (void)cudaStreamSynchronize(s.stream);
+        throw;
     }
-    for (Slot& s : ctx.slots) check_cuda(cudaStreamSynchronize(s.stream), "cudaStreamSynchronize");
+    if (trace_path && !trace.empty()) {
+        if (FILE* f = std::fopen(trace_path, "a")) {
+            std::fprintf(f, "{\"chunks\": [");
+            for (std::size_t c = 0; c < trace.size(); ++c) {
+                float t[4];
+                for (int q = 0; q < 4; ++q) cudaEventElapsedTime(&t[q], trace[0].e[0], trace[c].e[q]);
+                std::fprintf(f, "%s{\"slot\": %d, \"h2d\": [%.4f, %.4f], \"kernel\": [%.4f, %.4f], \"d2h\": [%.4f, %.4f], "
+                                "\"h2d_bytes\": %llu, \"d2h_bytes\": %llu}",
+                             c ? ", " : "", trace[c].slot, t[0], t[1], t[1], t[2], t[2], t[3],
+                             static_cast<unsigned long long>(trace[c].bytes_in),
+                             static_cast<unsigned long long>(trace[c].bytes_out));
+            }
+            std::fprintf(f, "]}\n");
+            std::fclose(f);
+        }
+        for (Ev& ev : trace)
+            for (auto& e : ev.e) cudaEventDestroy(e);
+    }
 }
 
 } // namespace pyrit_b200

@@ -234,7 +234,8 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
     p.reps.resize(std::size_t(e) * k);
     for (std::size_t i = 0; i < p.reps.size(); ++i) {
         if (m.e[i] >= f.field_size()) raise(Errc::InvalidArgument, "matrix entry outside the field");
-        p.reps[i] = opt.dense ? dense_transform(m.e[i], f) : sparse_transform(m.e[i], f);
+        p.reps[i] = opt.reps ? (*opt.reps)[i] & f.ring_mask()
+                    : opt.dense ? dense_transform(m.e[i], f) : sparse_transform(m.e[i], f);
         p.stats.matrix_ones += std::uint64_t(std::popcount(p.reps[i])) * w;
     }
     // CRS: the w x w bitmatrix of every entry (field_to_bitmatrix, field.hpp:198-207):
@@ -845,6 +846,11 @@ KernelShape staged_shape(const Program& p, std::uint32_t smem_limit) {
         const bool big_box = std::uint64_t(w) * tile >= 6144;
         std::uint32_t prod = p.staged_producer;
         if (!prod) prod = big_box ? (heavy ? 2u : 3u) : 1u;
+        // a TMA producer carries one 128-byte tensor map per input in the
+        // kernel parameters (runtime.cpp launch_batch): past ~240 inputs they
+        // overflow the 32764-byte parameter space, so copy with cp.async
+        const std::uint64_t param_bytes = (8ull * (k + p.rows + 6) + 63) / 64 * 64 + 128ull * k;
+        if (prod != 1 && param_bytes > 32764) prod = 1;
         ks.copy = prod == 1 ? 1u : 2u;
         ks.ws = prod == 3 ? 1u : 0u;
         return ks;

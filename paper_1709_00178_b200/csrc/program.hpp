@@ -98,6 +98,9 @@ struct CompileOptions {
     // matrix passed alongside only gives the shape
     const std::vector<std::uint32_t>* bits = nullptr;
     const std::vector<std::uint8_t>* written = nullptr;
+    // representatives to use instead of sparse_transform of the matrix (the
+    // negative-control fault injection, pyrit_plan_inject_fault)
+    const std::vector<std::uint32_t>* reps = nullptr;
 };
 
 // Measured staged-kernel choices for specific programs (tuned.tsv):

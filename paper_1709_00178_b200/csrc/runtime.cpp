@@ -341,9 +341,14 @@ bool start_async_compile(const Program& p, const KernelShape& ks, const std::str
     if (!cache.empty()) {
         std::error_code ec;
         std::filesystem::create_directories(cache, ec);
+        if (ec || ::access(cache.c_str(), W_OK) != 0) cache.clear(); // unwritable cache: compile into /tmp
+    }
+    if (!cache.empty()) {
         out = cache + "/" + cache_name(name) + ".cubin";
     } else {
-        out = (std::filesystem::temp_directory_path() / (name + "." + std::to_string(::getpid()) + ".cubin")).string();
+        std::error_code ec;
+        const auto tmp = std::filesystem::temp_directory_path(ec);
+        out = ((ec ? std::filesystem::path("/tmp") : tmp) / (name + "." + std::to_string(::getpid()) + ".cubin")).string();
     }
     g_async[name] = std::async(std::launch::async, [src = std::move(src), name, out, keep = !cache.empty(),
                                                     lib = nvrtc_path()] {
@@ -375,9 +380,19 @@ LoadedKernel load_kernel(const Program& p, const KernelShape& ks, int device) {
             auto it = g_async.find(name);
             if (it != g_async.end()) pending = it->second;
         }
+        bool compiled = false;
         if (pending.valid()) {
-            cubin = pending.get();
-        } else {
+            try {
+                cubin = pending.get();
+                compiled = true;
+            } catch (const std::exception&) {
+                // the background compile failed (e.g. an unwritable cache): forget
+                // it and compile here, in process, with a best-effort cache write
+                std::lock_guard<std::mutex> lk(g_async_mu);
+                g_async.erase(name);
+            }
+        }
+        if (!compiled) {
             cubin = nvrtc_compile(generate_cuda(p, ks), name);
             if (!cache.empty()) write_cache(cache, cname, cubin);
         }
@@ -441,6 +456,8 @@ void set_kernel_dir(const std::string& dir) {
 }
 
 std::string kernel_dir() {
+    // first use may come from several host threads at once (run_host_devices)
+    std::lock_guard<std::mutex> lk(g_mu);
     if (g_kernel_dir.empty()) {
         const char* env = std::getenv("PYRIT_B200_KERNEL_DIR");
         g_kernel_dir = env ? env : default_kernel_dir();
@@ -668,6 +685,17 @@ bool overlaps(const std::uint8_t* a, std::uint64_t alen, const std::uint8_t* b, 
     return x < y + blen && y < x + alen;
 }
 
+// Does any output span overlap any input span at all?
+bool any_alias(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out, std::uint64_t strip,
+               std::uint64_t nb, std::uint64_t in_pitch, std::uint64_t out_pitch) {
+    const std::uint64_t w = p.field.w;
+    const std::uint64_t ispan = (nb - 1) * in_pitch + w * strip, ospan = (nb - 1) * out_pitch + w * strip;
+    for (std::uint32_t i = 0; i < p.rows; ++i)
+        for (std::uint32_t j = 0; j < p.cols; ++j)
+            if (overlaps(out[i], ospan, in[j], ispan)) return true;
+    return false;
+}
+
 // Does any output span overlap an input span where a column of one is not the
 // same column of the other?  Kernels that read every input of a tile before
 // storing its outputs (ring_rt, staged, unsplit direct) are exact when outputs
@@ -890,7 +918,13 @@ LaunchInfo launch_batch(const Program& p0, const std::uint8_t* const* in, std::u
     if (p0.light && rt_ok && mode == 0 && !prebuilt_plan(p0.key))
         return launch_ring_rt_program(p0, in, out, strip, off, len, nb, in_pitch, out_pitch, stream);
     const Program& p = full_program(p0);
-    const KernelShape ks = choose_shape(p, in, out, strip, off, len, nb, in_pitch, out_pitch);
+    KernelShape ks = choose_shape(p, in, out, strip, off, len, nb, in_pitch, out_pitch);
+    if (ks.split > 1 && any_alias(p, in, out, strip, nb, in_pitch, out_pitch)) {
+        // split kernels walk a column with several thread groups: one group may
+        // store an output column before another loads the input it aliases
+        ks.split = 0;
+        ks.min_blocks = 1;
+    }
     const bool gen_ok = generic_ok(p, in, out, strip, off, len, nb, in_pitch, out_pitch) &&
                         !unsafe_alias(p, in, out, strip, nb, in_pitch, out_pitch);
     if (gen_ok && mode == 3) return launch_generic_program(p, in, out, strip, off, len, nb, in_pitch, out_pitch, stream);
