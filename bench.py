@@ -414,10 +414,13 @@ def main(argv=None):
             cpu.pop("times_s", None)
     st = plan.stats()
     if rank == 0:
+        # ncu DRAM bytes of THIS kernel at this shard size (profiles/traffic.json is keyed by
+        # kernel name; a kernel the table has not seen reports null, never a stale number)
         traffic = None
         try:
             with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-                traffic = json.load(f).get(wl.name, {}).get(str(world))
+                ent = json.load(f).get("kernels", {}).get(f"{launch['kernel']}|{Ls}")
+            traffic = ent["traffic_bytes"] if ent else None
         except Exception:
             pass
         line = {

@@ -554,11 +554,6 @@ Program compile_program(const Field& f, TransformKind kind, const Matrix& m, con
     return p;
 }
 
-struct LazyCompile {
-    std::once_flag once;
-    std::shared_ptr<const Program> prog;
-};
-
 Program light_program(const Field& f, TransformKind kind, const Matrix& m) {
     validate_field(f);
     if (m.cols == 0) raise(Errc::InvalidArgument, "matrix has no columns");

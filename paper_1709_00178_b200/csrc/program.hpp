@@ -18,6 +18,7 @@
 // bytes are identical to the reference's op-by-op replay.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <memory>
 #include <mutex>
@@ -118,6 +119,15 @@ const TunedEntry* find_tuned(const std::string& key);
 
 // compile_schedule analogue: matrix (rows x cols, GF(2^w) entries) -> program
 Program compile_program(const Field& f, TransformKind kind, const Matrix& m, const CompileOptions& opt);
+
+// Shared state of a light program and its copies: the full program, compiled
+// once on demand, and how many launches the pattern has had (hot patterns get
+// a specialised kernel compiled in the background, runtime.cpp)
+struct LazyCompile {
+    std::once_flag once;
+    std::shared_ptr<const Program> prog;
+    std::atomic<std::uint32_t> uses{0};
+};
 
 // A light ad-hoc program (decode patterns): representatives and fold only,
 // microseconds to build; full_program() compiles it (once, shared by copies)

@@ -800,24 +800,45 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
         const std::uint32_t e = std::min(2 * ep, p.rows - i0);
         l.R = e == 1 ? 1 : 2;
         l.E = (e + 1) / 2;
-        a.epart[0] = std::min(l.E, e);
-        a.epart[1] = e - a.epart[0];
+        // the two parts run in lockstep on the shared slots, so give them equal
+        // ring terms: the subset of outputs (<= E of them) for part 0 whose
+        // weight is closest to half (config 5's rows weigh 16/62/72/80)
+        std::vector<std::uint32_t> wt(e, 0);
+        for (std::uint32_t i = 0; i < e; ++i)
+            for (std::uint32_t j = 0; j < k; ++j) wt[i] += std::popcount(p.reps[std::size_t(i0 + i) * k + j]);
+        std::uint32_t total = 0;
+        for (std::uint32_t x : wt) total += x;
+        std::uint32_t best = (1u << std::min(l.E, e)) - 1, best_cost = ~0u;
+        if (l.R == 2 && e <= 16)
+            for (std::uint32_t m = 1; m < (1u << e); ++m) {
+                const std::uint32_t c = static_cast<std::uint32_t>(std::popcount(m));
+                if (c > l.E || e - c > l.E) continue;
+                std::uint32_t s0 = 0;
+                for (std::uint32_t i = 0; i < e; ++i)
+                    if ((m >> i) & 1u) s0 += wt[i];
+                const std::uint32_t cost = std::max(s0, total - s0);
+                if (cost < best_cost) best_cost = cost, best = m;
+            }
+        std::vector<std::uint32_t> part_rows[2];
+        for (std::uint32_t i = 0; i < e; ++i) part_rows[(best >> i) & 1u ? 0 : 1].push_back(i0 + i);
+        a.epart[0] = static_cast<std::uint32_t>(part_rows[0].size());
+        a.epart[1] = static_cast<std::uint32_t>(part_rows[1].size());
         const std::uint32_t ctas_per_sm = l.R == 1 ? 2 : 1;
         // op lists, one per (part, input), each ended by the sentinel E*n
         std::uint32_t nops = 0;
         for (std::uint32_t part = 0; part < 2; ++part) {
-            const std::uint32_t b0 = i0 + part * l.E, ne = a.epart[part];
+            const std::uint32_t ne = a.epart[part];
             for (std::uint32_t j = 0; j < k; ++j) {
                 a.opoff[part][j] = static_cast<std::uint16_t>(nops);
                 for (std::uint32_t i = 0; i < ne; ++i)
-                    for (std::uint32_t m = p.reps[std::size_t(b0 + i) * k + j]; m; m &= m - 1) {
+                    for (std::uint32_t m = p.reps[std::size_t(part_rows[part][i]) * k + j]; m; m &= m - 1) {
                         if (nops + 2 >= kRtMaxOps) raise(Errc::InvalidArgument, "ring_rt: too many ring terms per launch");
                         a.ops[nops++] = static_cast<std::uint8_t>(i * n + static_cast<std::uint32_t>(std::countr_zero(m)));
                     }
                 a.ops[nops++] = static_cast<std::uint8_t>(l.E * n);
             }
             a.opoff[part][k] = static_cast<std::uint16_t>(nops);
-            for (std::uint32_t i = 0; i < ne; ++i) a.out[part * kRtPartE + i] = out[b0 + i];
+            for (std::uint32_t i = 0; i < ne; ++i) a.out[part * kRtPartE + i] = out[part_rows[part][i]];
         }
         a.ops[nops] = 0; // the byte the last list's look-ahead reads
         a.nops = nops + 1;
@@ -915,8 +936,25 @@ LaunchInfo launch_batch(const Program& p0, const std::uint8_t* const* in, std::u
     // a light (decode-pattern) program stays on the runtime-matrix kernel unless
     // a specialised kernel was prebuilt for it (the benchmarked patterns) or a
     // kernel mode asks for the generated kernels
-    if (p0.light && rt_ok && mode == 0 && !prebuilt_plan(p0.key))
-        return launch_ring_rt_program(p0, in, out, strip, off, len, nb, in_pitch, out_pitch, stream);
+    if (p0.light && rt_ok && mode == 0 && !prebuilt_plan(p0.key)) {
+        // a hot pattern (PYRIT_B200_HOT_PATTERN launches, default 8, with tiered
+        // compilation on) gets its specialised kernel compiled in the background;
+        // once that is ready its launches take it, until then the runtime kernel
+        static const int hot = env_int("PYRIT_B200_HOT_PATTERN", 8);
+        bool specialised = false;
+        if (hot > 0 && tiered() && p0.lazy) {
+            const std::uint32_t uses = ++p0.lazy->uses;
+            if (uses >= static_cast<std::uint32_t>(hot)) {
+                const Program& fp = full_program(p0);
+                const KernelShape ks = choose_shape(fp, in, out, strip, off, len, nb, in_pitch, out_pitch);
+                const std::string name = kernel_name(fp, ks);
+                specialised = kernel_ready(name, dev);
+                if (!specialised && uses == static_cast<std::uint32_t>(hot)) start_async_compile(fp, ks, name);
+            }
+        }
+        if (!specialised)
+            return launch_ring_rt_program(p0, in, out, strip, off, len, nb, in_pitch, out_pitch, stream);
+    }
     const Program& p = full_program(p0);
     KernelShape ks = choose_shape(p, in, out, strip, off, len, nb, in_pitch, out_pitch);
     if (ks.split > 1 && any_alias(p, in, out, strip, nb, in_pitch, out_pitch)) {

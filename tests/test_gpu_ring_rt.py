@@ -211,3 +211,46 @@ def test_full_size_config4_random_patterns(cuda):
             rt_launched()
         torch.cuda.synchronize()
         assert torch.equal(buf, ref), er
+
+
+def test_hot_pattern_gets_specialised_kernel(cuda, tmp_path):
+    """With tiered compilation on, a decode pattern launched PYRIT_B200_HOT_PATTERN times gets its
+    specialised kernel compiled in the background (the runtime kernel serves until then); a
+    pattern used fewer times never compiles."""
+    import subprocess
+    import sys
+    import textwrap
+    script = textwrap.dedent("""
+        import numpy as np, torch
+        import paper_1709_00178_b200 as P
+        from paper_1709_00178_b200 import _lib as L
+        code = P.CodeSpec(10, 4, P.FieldSpec.gf256_r17())
+        d = torch.from_numpy(np.random.default_rng(5).integers(0, 256, (14, 8 * 16 * 512), dtype=np.uint8)).cuda()
+        d[10:] = P.encode(d[:10], code)
+        ref = d.clone()
+        kernels = []
+        for er in [(2, 3, 4, 5)] * 3 + [(0, 2, 7, 11)] * 4:
+            d[list(er)] = 0
+            P.decode(d, er, code)
+            torch.cuda.synchronize()
+            assert torch.equal(d, ref)
+            kernels.append(P.Plan.last_launch()["kernel"])
+        cold = L.load().pyrit_jit_compiles()
+        L.check(L.load().pyrit_jit_wait())
+        d[[0, 2, 7, 11]] = 0
+        P.decode(d, (0, 2, 7, 11), code)
+        torch.cuda.synchronize()
+        assert torch.equal(d, ref)
+        kernels.append(P.Plan.last_launch()["kernel"])
+        print(cold, L.load().pyrit_jit_compiles(), " ".join(kernels))
+    """)
+    env = dict(os.environ, PYRIT_B200_TIERED="1", PYRIT_B200_JIT_CACHE=str(tmp_path), PYRIT_B200_HOT_PATTERN="4")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, cwd=root,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = r.stdout.split()
+    kernels = out[2:]
+    assert all(k.startswith("pyrit_ring_rt_") for k in kernels[:7]), kernels
+    assert kernels[-1].startswith("pyrit_ring_k10_e4_w8_n17"), kernels  # the hot pattern, specialised
+    assert int(out[1]) == 1  # one compile: the pattern used 4 times, not the one used 3 times
