@@ -27,34 +27,44 @@ cudaError_t launch_generic(const GenericArgs& args, unsigned blocks, cudaStream_
 // geometry (w, n) applies any e x k matrix of ring representatives passed in
 // kernel parameters -- no per-code or per-erasure-pattern compilation.
 constexpr std::uint32_t kRtMaxK = 64;    // inputs per launch (one TMA tensor map each)
+constexpr std::uint32_t kRtParts = 4;    // output parts per CTA (all read the same shared-memory tiles)
 constexpr std::uint32_t kRtPartE = 8;    // output slots per part
-constexpr std::uint32_t kRtCpp = 256;    // threads per part (thread 0 of the CTA also issues the TMA copies)
 constexpr std::uint32_t kRtMaxOps = 8192; // (output, shift) ops per launch
-constexpr std::uint32_t kRtTile = 2048;  // bytes per strip per tile (8 per thread)
+constexpr std::uint32_t kRtTile = 2048;  // bytes per strip per tile (4*V per thread)
+constexpr std::uint32_t kRtBox = kRtTile / 8; // TMA box width in 8-byte elements
+// threads per part: one 4*V-byte word group of every strip of the tile each
+// (thread 0 of the CTA also issues the TMA copies)
+constexpr std::uint32_t rt_part_threads(std::uint32_t v) { return kRtTile / (4 * v); }
 struct alignas(64) RtArgs {
     std::uint64_t tm[kRtMaxK][16];       // CUtensorMap per input: (8-byte column element, strip, stripe)
-    std::uint8_t* out[2 * kRtPartE];     // output symbol bases of part p at [p*kRtPartE ..]
+    std::uint8_t* out[kRtParts * kRtPartE]; // output symbol bases of part p at [p*kRtPartE ..]
     std::uint64_t S, off, len, nb, obp;
     std::uint32_t k, tpb, ntiles, nslot, slot0; // slot0: byte offset of slot 0 in shared memory
     std::uint32_t nops;                         // bytes of ops[] (op lists with their sentinels)
-    std::uint32_t epart[2];              // outputs of each part
+    std::uint32_t prod;                         // thread that issues the TMA copies (first of the lightest part)
+    std::uint32_t epart[kRtParts];       // outputs of each part
     std::uint32_t fm[256]; // Parity: fm[q*w + i] = ~0 when strip i feeds the parity strip w+q (i = q mod s)
     // op list of input j for part p: ops[opoff[p][j] ..], each c = i*n + sh
     // (output i of the part accumulates input j rotated by sh ring positions, a
     // set bit of the representative of entry (i, j)), terminated by E*n
-    std::uint16_t opoff[2][kRtMaxK + 1];
+    std::uint16_t opoff[kRtParts][kRtMaxK + 1];
     std::uint8_t ops[kRtMaxOps];
 };
 struct RtLaunch {
-    std::uint32_t w = 0, n = 0, modulus = 0, E = 0, R = 2;
+    std::uint32_t w = 0, n = 0, modulus = 0, E = 0, R = 2, V = 2; // E outputs in each of R parts, V words
     bool parity = false, pdl = true;
     unsigned blocks = 1;
     std::uint32_t smem = 0;
     cudaStream_t stream = nullptr;
 };
-// accumulated outputs per part for ring length n: e*n*2 accumulator registers
-// within ~72 of the 128 a thread of a 512-thread CTA may hold
-constexpr int rt_part_outputs(int n) { return 36 / n < 1 ? 1 : (36 / n > 8 ? 8 : 36 / n); }
+// accumulated outputs per part for ring length n and V words per thread:
+//   V = 2: e*n*2 accumulator registers within ~72 of the 128 a thread of a
+//          512-thread CTA may hold;
+//   V = 4: e*n*4 accumulators next to the w*4 input words, within ~104.
+constexpr int rt_clamp_e(int e) { return e < 1 ? 1 : (e > 8 ? 8 : e); }
+constexpr int rt_part_outputs(int n, int w, int v) {
+    return v == 4 ? rt_clamp_e((104 - 4 * w) / (4 * n)) : rt_clamp_e(36 / n);
+}
 bool rt_supported(std::uint32_t w, std::uint32_t n, std::uint32_t modulus);
 cudaError_t launch_ring_rt(const RtArgs& a, const RtLaunch& l);
 

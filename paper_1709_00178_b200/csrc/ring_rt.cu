@@ -18,8 +18,8 @@
 //     2 KiB) into a ring of shared-memory slots with one TMA tensor box
 //     (cp.async.bulk.tensor.3d) per (tile, fragment), NSLOT-1 ahead of the
 //     consumers, tracked by FULL/EMPTY mbarriers;
-//   * R parts of 256 threads split the outputs (E accumulated outputs each);
-//     a thread owns 8 bytes of every strip of the tile: it reads the w strip
+//   * R parts of 2048/(4V) threads split the outputs (E accumulated outputs
+//     each); a thread owns 4V bytes of every strip of the tile: it reads the w strip
 //     words of a fragment from shared memory into registers and runs the
 //     fragment's op list -- each op (i, sh) a warp-uniform jump (brx.idx)
 //     into a compile-time XOR block "acc_i ^= x rotated by sh", so every
@@ -51,8 +51,12 @@ __device__ __forceinline__ void mbar_expect_tx(u32 bar, u32 bytes) {
     asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                  : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(u32 bar) {
-    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+// lane 0 arrives, predicated rather than branched (no divergent region)
+__device__ __forceinline__ void mbar_arrive_lane0(u32 bar, u32 lane) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.eq.u32 p, %1, 0;\n @p mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n}" ::"r"(bar),
+        "r"(lane)
+        : "memory");
 }
 __device__ __forceinline__ void mbar_wait(u32 bar, u32 parity) {
     asm volatile(
@@ -91,8 +95,7 @@ template <int W, int N, int E, int V, bool PAR>
 struct RtOps;
 #include "ring_rt_ops.inc"
 
-constexpr u32 kV = 2;                  // 32-bit words per thread per strip
-constexpr u32 kTile = 4u * kV * kRtCpp; // bytes per strip per tile (2 KiB)
+constexpr u32 kTile = kRtTile; // bytes per strip per tile (2 KiB)
 
 // x^t mod p (the Embedding fold row of ring position t >= w)
 __host__ __device__ constexpr u32 xpow_mod(int t, u32 p, int w) {
@@ -102,9 +105,12 @@ __host__ __device__ constexpr u32 xpow_mod(int t, u32 p, int w) {
     return static_cast<u32>(a);
 }
 
-template <int W, int N, u32 P, int E, int R, bool PAR>
-__global__ void __launch_bounds__(R * kRtCpp, R == 1 ? 2 : 1) ring_rt_kernel(const __grid_constant__ RtArgs a) {
-    constexpr u32 V = kV, TILE = kTile;
+// R parts of CPP threads, V 32-bit words of every strip per thread; a CTA is
+// 256 or 512 threads and an SM holds 512 (16 warps, <= 128 registers each)
+template <int W, int N, u32 P, int E, int R, int V, bool PAR>
+__global__ void __launch_bounds__(R * (kRtTile / (4 * V)), 512 / (R * (kRtTile / (4 * V))))
+    ring_rt_kernel(const __grid_constant__ RtArgs a) {
+    constexpr u32 TILE = kTile, CPP = kRtTile / (4u * V);
     constexpr u32 SLOT = W * TILE;  // one fragment tile
     constexpr int AR = PAR ? W : N; // accumulator rows
     constexpr int XR = PAR ? N : W; // input rows held in registers
@@ -118,7 +124,7 @@ __global__ void __launch_bounds__(R * kRtCpp, R == 1 ? 2 : 1) ring_rt_kernel(con
     if (threadIdx.x == 0) {
         for (u32 s = 0; s < ns; ++s) {
             mbar_init(FULL(s), 1);
-            mbar_init(EMPTY(s), R * kRtCpp / 32);
+            mbar_init(EMPTY(s), R * CPP / 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -131,14 +137,16 @@ __global__ void __launch_bounds__(R * kRtCpp, R == 1 ? 2 : 1) ring_rt_kernel(con
     // grid's tail; global memory is touched only after it has completed
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const u32 lane = threadIdx.x & 31u;
-    // producer (thread 0): the next unit to load, (tile pt of this CTA,
-    // fragment pj) into slot psl of phase pph; NSLOT-1 units run ahead
+    // producer (the first thread of the part whose outputs weigh least, so the
+    // copies are not issued from the critical path):
+    // the next unit to load, (tile pt of this CTA, fragment pj) into slot psl
+    // of phase pph; NSLOT-1 units run ahead
     u32 pj = 0, pt = blockIdx.x, psl = 0, pph = 0, pb = 0, px = 0;
     auto produce = [&]() {
         if (pt >= ntiles) return;
         if (pj == 0) {
             pb = pt / tpb;
-            px = static_cast<u32>((a.off + u64(pt - pb * tpb) * TILE) / (4u * V));
+            px = static_cast<u32>((a.off + u64(pt - pb * tpb) * TILE) / 8u); // 8-byte TMA elements
         }
         mbar_wait(EMPTY(psl), pph ^ 1u);
         mbar_expect_tx(FULL(psl), SLOT);
@@ -146,13 +154,14 @@ __global__ void __launch_bounds__(R * kRtCpp, R == 1 ? 2 : 1) ring_rt_kernel(con
         if (++psl == ns) psl = 0, pph ^= 1u;
         if (++pj == k) pj = 0, pt += gridDim.x;
     };
-    if (threadIdx.x == 0)
+    const u32 PROD = a.prod;
+    if (threadIdx.x == PROD)
         for (u32 u2 = 0; u2 + 1 < ns; ++u2) produce();
-    const u32 part = R == 1 ? 0u : threadIdx.x / kRtCpp;
-    const u32 col = R == 1 ? threadIdx.x : threadIdx.x % kRtCpp;
+    const u32 part = R == 1 ? 0u : threadIdx.x / CPP;
+    const u32 col = R == 1 ? threadIdx.x : threadIdx.x % CPP;
     const u64 S = a.S;
     const u32 ep = a.epart[part];
-    const std::uint16_t* opoff = a.opoff[part];
+    const u32 list0 = ops_s + a.opoff[part][0]; // this part's op lists, input 0 first
     u32 sl = 0, ph = 0;
     for (u32 t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const u32 b = t / tpb, tt = t - b * tpb;
@@ -163,15 +172,19 @@ __global__ void __launch_bounds__(R * kRtCpp, R == 1 ? 2 : 1) ring_rt_kernel(con
             for (int r = 0; r < AR; ++r)
 #pragma unroll
                 for (int v = 0; v < V; ++v) acc[i][r][v] = 0;
+        // op cursor: q the next byte, d the op already loaded; the lists of
+        // inputs 0..k-1 follow each other, each ended by its sentinel
+        u32 q = list0 + 1, d;
+        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(d) : "r"(list0));
         for (u32 j = 0; j < k; ++j) {
-            if (threadIdx.x == 0) produce();
+            if (threadIdx.x == PROD) produce();
             mbar_wait(FULL(sl), ph);
             u32 x[XR][V];
             const u32 src = a.slot0 + sbase + sl * SLOT + col * (4u * V);
 #pragma unroll
             for (int s = 0; s < W; ++s) lds<V>(x[s], src + s * TILE);
             __syncwarp();
-            if (lane == 0) mbar_arrive(EMPTY(sl));
+            mbar_arrive_lane0(EMPTY(sl), lane);
             if (++sl == ns) sl = 0, ph ^= 1u;
             if constexpr (PAR) {
                 // column parities: strip W+q = XOR of strips i = q (mod s)
@@ -187,7 +200,7 @@ __global__ void __launch_bounds__(R * kRtCpp, R == 1 ? 2 : 1) ring_rt_kernel(con
                     }
             }
             // this part's op list of input j (shared memory, sentinel-terminated)
-            RtOps<W, N, E, V, PAR>::run(ops_s + opoff[j], acc, x);
+            RtOps<W, N, E, V, PAR>::run(q, d, acc, x);
         }
         const u64 rel = u64(tt) * TILE + col * (4u * V);
         const bool live = rel < a.len;
@@ -217,9 +230,9 @@ __global__ void __launch_bounds__(R * kRtCpp, R == 1 ? 2 : 1) ring_rt_kernel(con
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-template <int W, int N, u32 P, int E, int R, bool PAR>
+template <int W, int N, u32 P, int E, int R, int V, bool PAR>
 cudaError_t launch_one(const RtArgs& a, const RtLaunch& l) {
-    auto fn = ring_rt_kernel<W, N, P, E, R, PAR>;
+    auto fn = ring_rt_kernel<W, N, P, E, R, V, PAR>;
     static bool attr_set[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -230,7 +243,7 @@ cudaError_t launch_one(const RtArgs& a, const RtLaunch& l) {
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(l.blocks);
-    cfg.blockDim = dim3(R * kRtCpp);
+    cfg.blockDim = dim3(R * rt_part_threads(V));
     cfg.dynamicSmemBytes = l.smem;
     cfg.stream = l.stream;
     cudaLaunchAttribute attr[1];
@@ -241,21 +254,32 @@ cudaError_t launch_one(const RtArgs& a, const RtLaunch& l) {
     return cudaLaunchKernelEx(&cfg, fn, a);
 }
 
-template <int W, int N, u32 P, bool PAR, int E>
+template <int W, int N, u32 P, int R, int V, bool PAR, int E>
 cudaError_t launch_e(const RtArgs& a, const RtLaunch& l) {
     if constexpr (E >= 1) {
-        if (l.E == E) return launch_one<W, N, P, E, 2, PAR>(a, l);
-        return launch_e<W, N, P, PAR, E - 1>(a, l);
+        if (l.E == E) return launch_one<W, N, P, E, R, V, PAR>(a, l);
+        return launch_e<W, N, P, R, V, PAR, E - 1>(a, l);
     }
     return cudaErrorInvalidValue;
 }
 
+template <int W, int N, u32 P, int R, int V>
+cudaError_t launch_rv(const RtArgs& a, const RtLaunch& l) {
+    constexpr int EP = rt_part_outputs(N, W, V);
+    return l.parity ? launch_e<W, N, P, R, V, true, EP>(a, l) : launch_e<W, N, P, R, V, false, EP>(a, l);
+}
+
+// (R, V) shapes: a single output runs one 256-thread part per CTA (two CTAs
+// per SM); V = 2 pairs two 256-thread parts, V = 4 two (two CTAs per SM) or
+// four 128-thread parts
 template <int W, int N, u32 P>
 cudaError_t launch_wn(const RtArgs& a, const RtLaunch& l) {
-    if (l.R == 1) // a single output: 8 warps per CTA, two CTAs per SM
-        return l.parity ? launch_one<W, N, P, 1, 1, true>(a, l) : launch_one<W, N, P, 1, 1, false>(a, l);
-    constexpr int EP = rt_part_outputs(N);
-    return l.parity ? launch_e<W, N, P, true, EP>(a, l) : launch_e<W, N, P, false, EP>(a, l);
+    if (l.R == 1 && l.V == 2)
+        return l.parity ? launch_one<W, N, P, 1, 1, 2, true>(a, l) : launch_one<W, N, P, 1, 1, 2, false>(a, l);
+    if (l.R == 2 && l.V == 2) return launch_rv<W, N, P, 2, 2>(a, l);
+    if (l.R == 2 && l.V == 4) return launch_rv<W, N, P, 2, 4>(a, l);
+    if (l.R == 4 && l.V == 4) return launch_rv<W, N, P, 4, 4>(a, l);
+    return cudaErrorInvalidValue;
 }
 
 // the ring geometries with an ahead-of-time instance: the reference's field

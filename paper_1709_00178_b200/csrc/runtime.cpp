@@ -755,7 +755,6 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
     RtArgs tmpl;
     RtArgs& a = tmpl;
     const std::uint32_t w = p.field.w, n = p.field.n, k = p.cols;
-    const std::uint32_t ep = static_cast<std::uint32_t>(rt_part_outputs(static_cast<int>(n)));
     const std::uint32_t tile = kRtTile, elem = 8, slot = w * tile;
     const std::uint64_t tpb = (len + tile - 1) / tile;
     static const int promo_knob = env_int("PYRIT_B200_TMA_PROMO", 3);
@@ -764,7 +763,7 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
         CUtensorMap m;
         const cuuint64_t dims[3] = {strip / elem, w, nb};
         const cuuint64_t strides[2] = {strip, nb > 1 ? in_pitch : strip * w};
-        const cuuint32_t box[3] = {kRtCpp, w, 1};
+        const cuuint32_t box[3] = {kRtBox, w, 1};
         const cuuint32_t es[3] = {1, 1, 1};
         check_cu(driver().tensorMapEncodeTiled(&m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<std::uint8_t*>(in[j]),
                                                dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -792,41 +791,62 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
     l.parity = par;
     static const bool pdl = env_int("PYRIT_B200_PDL", 1) != 0;
     l.pdl = pdl;
-    // Outputs go to two parts of 256 threads (16 warps per SM); a single output
-    // runs one part per CTA and two CTAs per SM.  More outputs than 2 * ep go to
-    // further launches (each re-reads the inputs).
+    // Outputs go to R parts of 2048/(4V) threads that all read the same tiles
+    // (16 warps per SM): V = 4 (16 bytes of each strip per thread) halves the
+    // dispatch per XOR and doubles the XORs between jumps; V = 2 holds more
+    // outputs per part.  A single output runs one 256-thread part per CTA, two
+    // CTAs per SM.  More outputs than one launch holds go to further launches
+    // (each re-reads the inputs).
+    static const int vknob = env_int("PYRIT_B200_RT_V", 4);
+    const std::uint32_t V = vknob == 2 ? 2u : 4u;
+    const std::uint32_t ep = static_cast<std::uint32_t>(rt_part_outputs(static_cast<int>(n), static_cast<int>(w),
+                                                                        static_cast<int>(V)));
+    const std::uint32_t per_launch = (V == 4 ? 4u : 2u) * ep;
     LaunchInfo info;
-    for (std::uint32_t i0 = 0; i0 < p.rows; i0 += 2 * ep) {
-        const std::uint32_t e = std::min(2 * ep, p.rows - i0);
-        l.R = e == 1 ? 1 : 2;
-        l.E = (e + 1) / 2;
-        // the two parts run in lockstep on the shared slots, so give them equal
-        // ring terms: the subset of outputs (<= E of them) for part 0 whose
-        // weight is closest to half (config 5's rows weigh 16/62/72/80)
-        std::vector<std::uint32_t> wt(e, 0);
-        for (std::uint32_t i = 0; i < e; ++i)
+    for (std::uint32_t i0 = 0; i0 < p.rows; i0 += per_launch) {
+        const std::uint32_t e = std::min(per_launch, p.rows - i0);
+        if (e == 1) {
+            l.V = 2;
+            l.R = 1;
+        } else if (V == 2) {
+            l.V = 2;
+            l.R = 2;
+        } else {
+            l.V = 4;
+            l.R = e <= 2 * ep ? 2u : 4u;
+        }
+        l.E = (e + l.R - 1) / l.R;
+        // the parts run in lockstep on the shared slots, so give them equal
+        // ring terms: heaviest output first onto the lightest part with room
+        // (config 5's rows weigh 16/62/72/80)
+        std::vector<std::uint32_t> wt(e, 0), order(e);
+        for (std::uint32_t i = 0; i < e; ++i) {
+            order[i] = i;
             for (std::uint32_t j = 0; j < k; ++j) wt[i] += std::popcount(p.reps[std::size_t(i0 + i) * k + j]);
-        std::uint32_t total = 0;
-        for (std::uint32_t x : wt) total += x;
-        std::uint32_t best = (1u << std::min(l.E, e)) - 1, best_cost = ~0u;
-        if (l.R == 2 && e <= 16)
-            for (std::uint32_t m = 1; m < (1u << e); ++m) {
-                const std::uint32_t c = static_cast<std::uint32_t>(std::popcount(m));
-                if (c > l.E || e - c > l.E) continue;
-                std::uint32_t s0 = 0;
-                for (std::uint32_t i = 0; i < e; ++i)
-                    if ((m >> i) & 1u) s0 += wt[i];
-                const std::uint32_t cost = std::max(s0, total - s0);
-                if (cost < best_cost) best_cost = cost, best = m;
-            }
-        std::vector<std::uint32_t> part_rows[2];
-        for (std::uint32_t i = 0; i < e; ++i) part_rows[(best >> i) & 1u ? 0 : 1].push_back(i0 + i);
-        a.epart[0] = static_cast<std::uint32_t>(part_rows[0].size());
-        a.epart[1] = static_cast<std::uint32_t>(part_rows[1].size());
-        const std::uint32_t ctas_per_sm = l.R == 1 ? 2 : 1;
+        }
+        std::stable_sort(order.begin(), order.end(), [&](std::uint32_t x, std::uint32_t y) { return wt[x] > wt[y]; });
+        std::vector<std::uint32_t> part_rows[kRtParts];
+        std::uint32_t load[kRtParts] = {};
+        for (std::uint32_t i : order) {
+            std::uint32_t best = kRtParts;
+            for (std::uint32_t q = 0; q < l.R; ++q)
+                if (part_rows[q].size() < l.E && (best == kRtParts || load[q] < load[best])) best = q;
+            part_rows[best].push_back(i0 + i);
+            load[best] += wt[i];
+        }
+        for (std::uint32_t q = 0; q < kRtParts; ++q) {
+            std::sort(part_rows[q].begin(), part_rows[q].end());
+            a.epart[q] = static_cast<std::uint32_t>(part_rows[q].size());
+        }
+        std::uint32_t light = 0;
+        for (std::uint32_t q = 1; q < l.R; ++q)
+            if (load[q] <= load[light]) light = q;
+        a.prod = light * rt_part_threads(l.V);
+        const std::uint32_t cta_threads = l.R * rt_part_threads(l.V);
+        const std::uint32_t ctas_per_sm = 512 / cta_threads;
         // op lists, one per (part, input), each ended by the sentinel E*n
         std::uint32_t nops = 0;
-        for (std::uint32_t part = 0; part < 2; ++part) {
+        for (std::uint32_t part = 0; part < l.R; ++part) {
             const std::uint32_t ne = a.epart[part];
             for (std::uint32_t j = 0; j < k; ++j) {
                 a.opoff[part][j] = static_cast<std::uint16_t>(nops);
@@ -857,7 +877,7 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
         call.args.push_back(std::make_unique<RtArgs>(a));
         call.launches.push_back(l);
         info.blocks = l.blocks;
-        info.threads = l.R * kRtCpp;
+        info.threads = l.R * rt_part_threads(l.V);
     }
     info.kernel = "pyrit_ring_rt_w" + std::to_string(w) + "_n" + std::to_string(n) + (par ? "_par" : "");
     info.lanes = 2;
