@@ -1,0 +1,13 @@
+"""Summarise tools/bench_rt.py output files: runtime-kernel fraction of HBM peak per config / pattern."""
+import json
+import sys
+
+for fn in sys.argv[1:]:
+    cells = []
+    for line in open(fn):
+        d = json.loads(line)
+        if d.get("kernel") == "ring_rt":
+            cells.append(f"c{d['cfg']}={d['frac']:.3f}")
+        elif "pattern" in d:
+            cells.append(f"{''.join(map(str, d['pattern']))}={d['frac']:.3f}")
+    print(fn.split("/")[-1], " ".join(cells))
