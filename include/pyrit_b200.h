@@ -268,8 +268,11 @@ int pyrit_set_lanes(uint32_t lanes); /* 32-bit words per thread per strip: 1, 2 
 /* 0 = auto (TMA-staged kernel whenever pointers/pitch/window are 16-byte
  * aligned and the tiles fit in shared memory), 1 = direct kernel only,
  * 2 = staged whenever possible, 3 = the generic bit-matrix kernel (no
- * per-code compilation; 4-byte aligned launches) -- it also serves launches
- * whose specialised kernel is still compiling (PYRIT_B200_TIERED, default on) */
+ * per-code compilation; 4-byte aligned launches), 4 = the runtime-matrix ring
+ * kernel (no per-code compilation; 16-byte aligned launches of the AOT ring
+ * geometries).  In mode 0 the runtime-matrix kernel (else the generic one)
+ * serves decode patterns and launches whose specialised kernel is still
+ * compiling (PYRIT_B200_TIERED, default on) */
 int pyrit_set_kernel_mode(int mode);
 int pyrit_set_kernel_dir(const char* dir);
 /* name and geometry of this thread's most recent generated-kernel launch */
