@@ -40,7 +40,8 @@ struct Case {
     unsigned transform;
     unsigned long long strip; // bytes per strip (symbol = w strips)
     unsigned long long stripes;
-    int mode; // 0 auto, 1 direct, 2 staged
+    int mode; // 0 auto, 1 direct, 2 staged, 3 generic bit-matrix, 4 runtime-matrix ring kernel
+    const char* expect = nullptr; // prefix the launched kernel's name must have
 };
 
 void run(const Case& c) {
@@ -113,9 +114,10 @@ void run(const Case& c) {
         CK(cudaMemcpy(back.data(), din[j], bytes, cudaMemcpyDeviceToHost));
         guards = back == hin[j];
     }
-    std::printf("%-34s mode %d %-52s %s%s\n", c.name, c.mode, kname, ok ? "OK" : "MISMATCH",
-                guards ? "" : " (STRAY WRITE)");
-    failures += !ok + !guards;
+    const bool kind = !c.expect || std::strncmp(kname, c.expect, std::strlen(c.expect)) == 0;
+    std::printf("%-34s mode %d %-52s %s%s%s\n", c.name, c.mode, kname, ok ? "OK" : "MISMATCH",
+                guards ? "" : " (STRAY WRITE)", kind ? "" : " (UNEXPECTED KERNEL)");
+    failures += !ok + !guards + !kind;
     for (auto* p : base) CK(cudaFree(p));
     pyrit_plan_destroy(plan);
     pyrit_set_kernel_mode(0);
@@ -137,6 +139,16 @@ int main() {
         {"gf64 k20 r40 parity (staged)", "gf64", 20, 40, 1, 1024, 2, 2},
         {"gf16 k8 r4 (byte mode)", "gf16", 8, 4, 0, 129, 3, 1},
         {"gf16 k8 r4 (many tiny stripes)", "gf16", 8, 4, 0, 32, 257, 0},
+        // runtime-matrix ring kernel (ring_rt.cu): one part (R=1), 2 parts in
+        // 2 CTAs/SM, 4 parts with one idle, several launches, Parity transform
+        {"cfg5 gf4096 k16 r4 (runtime 4 parts)", "gf4096", 16, 4, 0, 2048 + 16, 2, 4, "pyrit_ring_rt_"},
+        {"cfg4 gf256/R17 k10 r4 (runtime)", "gf256_r17", 10, 4, 0, 4096 + 32, 2, 4, "pyrit_ring_rt_"},
+        {"gf1024 k12 r3 (runtime, idle part)", "gf1024", 12, 3, 0, 2048 + 48, 2, 4, "pyrit_ring_rt_"},
+        {"gf16 k4 r1 (runtime, one output)", "gf16", 4, 1, 0, 4096 + 16, 3, 4, "pyrit_ring_rt_"},
+        {"gf16 k8 r2 (runtime, 2 parts)", "gf16", 8, 2, 0, 2048, 2, 4, "pyrit_ring_rt_"},
+        {"gf64 k6 r9 (runtime, 2 launches)", "gf64", 6, 9, 0, 1024 + 16, 2, 4, "pyrit_ring_rt_"},
+        {"gf64 k20 r4 parity (runtime)", "gf64", 20, 4, 1, 2048 + 32, 2, 4, "pyrit_ring_rt_"},
+        {"gf4096 k16 r4 (generic bitmatrix)", "gf4096", 16, 4, 0, 1024 + 4, 2, 3, "pyrit_generic"},
     };
     for (const Case& c : cases) run(c);
     std::printf(failures ? "SANITIZE CHECK FAILED\n" : "SANITIZE CHECK PASSED\n");
