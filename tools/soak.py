@@ -29,6 +29,9 @@ def main():
     ap.add_argument("--knobs", action="store_true",
                     help="also random matrices, more (w, n, p) fields and random compile knobs (parts, fragment "
                          "groups, pair sharing windows, CTA size)")
+    ap.add_argument("--rt", action="store_true",
+                    help="runtime-matrix ring kernel only (kernel mode 4): random matrices over the AOT ring "
+                         "geometries, 16-byte aligned strips, e up to 24 outputs, k up to 64")
     a = ap.parse_args()
 
     import numpy as np
@@ -46,15 +49,15 @@ def main():
     exotic = [P.FieldSpec(2, 3, 0, 1, 2, 0b111), P.FieldSpec(3, 7, 0, 1, 3, 0b1011),
               P.FieldSpec(4, 15, 0, 1, 4, 0b10011)]
     knob_names = ("PARTS", "PART_GROUP", "PART_CSE", "CSE_WINDOW", "THREADS")
-    fails, t0, kernels = [], time.time(), set()
+    fails, t0, kernels, rt_cases = [], time.time(), set(), 0
     for case in range(a.cases):
         f = rng.choice(fields + (exotic if a.knobs else []))
-        k = rng.randint(1, min(32, f.field_size() - 1))
-        r = rng.randint(1, min(16, f.field_size() - k))
+        k = rng.randint(1, min(64 if a.rt else 32, f.field_size() - 1))
+        r = rng.randint(1, min(24 if a.rt else 16, f.field_size() - k))
         kind = rng.choice([0, 0, 0, 1]) if f not in exotic else 0
-        strip = 16 * rng.randint(1, 2048) + rng.choice([0, 0, 0, 4, 8])
+        strip = 16 * rng.randint(1, 2048) + (0 if a.rt else rng.choice([0, 0, 0, 4, 8]))
         nb = rng.choice([1, 1, 2, 5])
-        mode = rng.choice([0, 2, 2])
+        mode = 4 if a.rt else rng.choice([0, 2, 2])
         prod = rng.choice(["1", "2", "2", "3"])
         os.environ["PYRIT_B200_COPY"] = "1" if prod == "1" else "2"
         os.environ["PYRIT_B200_WS"] = "1" if prod == "3" else "0"
@@ -68,7 +71,7 @@ def main():
             os.environ.pop("PYRIT_B200_" + n, None)
         for n, v in knobs.items():
             os.environ["PYRIT_B200_" + n] = str(v)
-        if a.knobs and rng.random() < 0.5:
+        if (a.knobs or a.rt) and rng.random() < 0.5:
             m = np.array([[rng.randrange(f.field_size()) for _ in range(k)] for _ in range(r)], dtype=np.uint16)
         else:
             m = P.cauchy_parity_matrix(code)
@@ -82,6 +85,7 @@ def main():
                              nb, k * sym, r * sym, stream=torch.cuda.current_stream().cuda_stream)
             torch.cuda.synchronize()
             kernels.add(P.Plan.last_launch()["kernel"])
+            rt_cases += P.Plan.last_launch()["kernel"].startswith("pyrit_ring_rt_")
             got = out.cpu().numpy()
             of = O.Field(f.w, f.n, f.kind, f.s, f.r_esp, f.modulus)
             for b in sorted({0, nb - 1}):
@@ -97,7 +101,7 @@ def main():
     L.check(lib.pyrit_set_kernel_mode(0))
     for n in knob_names:
         os.environ.pop("PYRIT_B200_" + n, None)
-    print(json.dumps({"cases": a.cases, "knobs": a.knobs, "failures": len(fails), "distinct_kernels": len(kernels),
+    print(json.dumps({"cases": a.cases, "knobs": a.knobs, "rt": a.rt, "failures": len(fails), "distinct_kernels": len(kernels), "runtime_matrix_cases": rt_cases,
                       "seconds": round(time.time() - t0, 1), "first_failures": fails[:5]}))
     return 1 if fails else 0
 
