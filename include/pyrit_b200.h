@@ -278,6 +278,10 @@ int pyrit_set_kernel_dir(const char* dir);
 /* name and geometry of this thread's most recent generated-kernel launch */
 int pyrit_cu_last_launch(char* kernel, size_t cap, uint32_t* blocks, uint32_t* threads);
 uint64_t pyrit_jit_compiles(void);
+/* wall time of the most recent kernel compile and of all compiles so far, in
+ * milliseconds (NVRTC in process, or the background helper process) -- what a
+ * new code or a hot erasure pattern costs before its specialised kernel runs */
+int pyrit_jit_time(double* last_ms, double* total_ms);
 /* which NVRTC compiles kernels that are not prebuilt: "nvrtc 12.9 (<file>)" */
 int pyrit_jit_info(char* buf, size_t cap);
 /* wait until every background compile started so far has finished (their

@@ -803,6 +803,10 @@ int pyrit_jit_info(char* buf, size_t cap) {
 }
 
 uint64_t pyrit_jit_compiles(void) { return jit_compiles(); }
+int pyrit_jit_time(double* last_ms, double* total_ms) {
+    jit_time(last_ms, total_ms);
+    return 0;
+}
 uint64_t pyrit_kernel_launches(void) { return kernel_launches(); }
 
 } // extern "C"

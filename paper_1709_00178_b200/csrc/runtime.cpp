@@ -99,6 +99,14 @@ std::mutex g_mu;
 std::unordered_map<std::string, LoadedKernel> g_kernels; // name@device
 std::unordered_map<std::string, CUmodule> g_modules;
 std::atomic<std::uint64_t> g_jit{0}, g_launches{0};
+// wall time of compiles (NVRTC in process, or the helper process), nanoseconds
+std::atomic<std::uint64_t> g_jit_ns_last{0}, g_jit_ns_total{0};
+void note_compile(std::chrono::steady_clock::time_point t0) {
+    const auto ns = static_cast<std::uint64_t>(
+        std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count());
+    g_jit_ns_last = ns;
+    g_jit_ns_total += ns;
+}
 std::atomic<std::uint32_t> g_lanes{0};
 std::string g_kernel_dir;
 
@@ -227,6 +235,7 @@ std::string nvrtc_tag() {
 }
 
 std::vector<char> nvrtc_compile(const std::string& src, const std::string& name) {
+    const auto t0 = std::chrono::steady_clock::now();
     const Nvrtc& rt = nvrtc();
     nvrtcProgram prog;
     auto chk = [&](nvrtcResult r, const char* what) {
@@ -250,6 +259,7 @@ std::vector<char> nvrtc_compile(const std::string& src, const std::string& name)
     chk(rt.cubin(prog, cubin.data()), "nvrtcGetCUBIN");
     rt.destroy(&prog);
     ++g_jit;
+    note_compile(t0);
     return cubin;
 }
 
@@ -303,6 +313,7 @@ std::string helper_path() {
 // compile `src` in a helper process into `out` (blocking; runs on a background thread)
 std::vector<char> helper_compile(const std::string& src, const std::string& name, const std::string& out,
                                  const std::string& lib) {
+    const auto t0 = std::chrono::steady_clock::now();
     const std::string base = out + ".src" + std::to_string(::getpid()) + "_" +
                              std::to_string(std::hash<std::thread::id>{}(std::this_thread::get_id()));
     {
@@ -326,6 +337,7 @@ std::vector<char> helper_compile(const std::string& src, const std::string& name
     std::vector<char> cubin = read_file(out);
     if (cubin.empty()) throw CudaFailure(-1000, "background compile of " + name + " produced nothing");
     ++g_jit;
+    note_compile(t0);
     return cubin;
 }
 
@@ -495,6 +507,10 @@ std::string jit_info() {
 }
 
 std::uint64_t jit_compiles() { return g_jit.load(); }
+void jit_time(double* last_ms, double* total_ms) {
+    if (last_ms) *last_ms = static_cast<double>(g_jit_ns_last.load()) * 1e-6;
+    if (total_ms) *total_ms = static_cast<double>(g_jit_ns_total.load()) * 1e-6;
+}
 std::uint64_t kernel_launches() { return g_launches.load(); }
 
 KernelShape direct_shape(const Program& p, std::uint32_t lanes) {

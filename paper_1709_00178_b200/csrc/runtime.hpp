@@ -61,6 +61,7 @@ std::string kernel_dir();
 
 LaunchInfo last_launch(); // this thread's most recent launch_program
 std::uint64_t jit_compiles(); // number of NVRTC compilations performed so far
+void jit_time(double* last_ms, double* total_ms); // wall time of the last / all compiles
 std::string jit_info();
 void jit_wait(); // wait for every background (tiered) compile started so far       // "nvrtc <major>.<minor> (<library file>)"; throws if NVRTC cannot be loaded
 std::uint64_t kernel_launches(); // number of generated-kernel launches so far
