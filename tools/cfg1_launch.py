@@ -92,6 +92,23 @@ def main():
     res["floor_fill_wide"] = {"us_per_launch": round(graph_ms(lambda i: P.fill(buf[:wide], 1, i % 7, stream=st()),
                                                               a.steps) * 1e3, 3),
                               "grid": [148, 256], "bytes": wide}
+    # the same bytes through library kernels, same rotating sets and graph: torch's
+    # XOR of two 2 MiB halves of each set's data (4 MiB read, 2 MiB written, like
+    # config 1's 4 MiB in / 2 MiB out) and a 6 MiB device-to-device copy (3 + 3)
+    half = wl.k * wl.frag // 2
+    flat = [s[2].view(-1) for s in sets]
+    outs = [s[3].view(-1) for s in sets]
+
+    def xor_step(i):
+        f = flat[i % nsets]
+        torch.bitwise_xor(f[:half], f[half:2 * half], out=outs[i % nsets][:half])
+
+    res["torch_xor_4MiB_in_2MiB_out"] = {"us_per_launch": round(graph_ms(xor_step, a.steps) * 1e3, 3),
+                                         "bytes": 3 * half}
+    cp_src = [torch.empty(moved // 2, dtype=torch.uint8, device=dev) for _ in range(nsets)]
+    cp_dst = [torch.empty(moved // 2, dtype=torch.uint8, device=dev) for _ in range(nsets)]
+    res["torch_copy_3MiB"] = {"us_per_launch": round(graph_ms(lambda i: cp_dst[i % nsets].copy_(cp_src[i % nsets]),
+                                                              a.steps) * 1e3, 3), "bytes": moved}
     print(json.dumps(res))
     if a.out:
         with open(a.out, "w") as f:
