@@ -29,6 +29,11 @@ cudaError_t launch_generic(const GenericArgs& args, unsigned blocks, cudaStream_
 constexpr std::uint32_t kRtMaxK = 64;    // inputs per launch (one TMA tensor map each)
 constexpr std::uint32_t kRtParts = 4;    // output parts per CTA (all read the same shared-memory tiles)
 constexpr std::uint32_t kRtPartE = 8;    // output slots per part
+// output groups per launch: a tile is a unit per group, so a code with more
+// outputs than one CTA holds is still one launch; the groups of a tile run on
+// neighbouring CTAs at about the same time, so only the first reads HBM and
+// the others hit L2
+constexpr std::uint32_t kRtMaxGroups = 8;
 constexpr std::uint32_t kRtMaxOps = 8192; // (output, shift) ops per launch
 constexpr std::uint32_t kRtTile = 2048;  // bytes per strip per tile (4*V per thread)
 constexpr std::uint32_t kRtBox = kRtTile / 8; // TMA box width in 8-byte elements
@@ -37,17 +42,18 @@ constexpr std::uint32_t kRtBox = kRtTile / 8; // TMA box width in 8-byte element
 constexpr std::uint32_t rt_part_threads(std::uint32_t v) { return kRtTile / (4 * v); }
 struct alignas(64) RtArgs {
     std::uint64_t tm[kRtMaxK][16];       // CUtensorMap per input: (8-byte column element, strip, stripe)
-    std::uint8_t* out[kRtParts * kRtPartE]; // output symbol bases of part p at [p*kRtPartE ..]
+    std::uint8_t* out[kRtMaxGroups][kRtParts * kRtPartE]; // output bases of group g, part p at [g][p*kRtPartE ..]
     std::uint64_t S, off, len, nb, obp;
     std::uint32_t k, tpb, ntiles, nslot, slot0; // slot0: byte offset of slot 0 in shared memory
     std::uint32_t nops;                         // bytes of ops[] (op lists with their sentinels)
     std::uint32_t prod;                         // thread that issues the TMA copies (first of the lightest part)
-    std::uint32_t epart[kRtParts];       // outputs of each part
+    std::uint32_t ngrp;                  // output groups (units per tile)
+    std::uint32_t epart[kRtMaxGroups][kRtParts]; // outputs of each part of each group
     std::uint32_t fm[256]; // Parity: fm[q*w + i] = ~0 when strip i feeds the parity strip w+q (i = q mod s)
-    // op list of input j for part p: ops[opoff[p][j] ..], each c = i*n + sh
+    // op list of input j for part p of group g: ops[opoff[g][p][j] ..], each c = i*n + sh
     // (output i of the part accumulates input j rotated by sh ring positions, a
     // set bit of the representative of entry (i, j)), terminated by E*n
-    std::uint16_t opoff[kRtParts][kRtMaxK + 1];
+    std::uint16_t opoff[kRtMaxGroups][kRtParts][kRtMaxK + 1];
     std::uint8_t ops[kRtMaxOps];
 };
 struct RtLaunch {

@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(R * (kRtTile / (4 * V)), 512 / (R * (kRtTile /
     const u32 ns = a.nslot;
     const u32 k = a.k;
     const u32 ntiles = a.ntiles, tpb = a.tpb;
+    const u32 G = a.ngrp, nunits = ntiles * G; // unit u = (tile u / G, output group u % G)
 #define FULL(s) (sbase + 8u * (s))
 #define EMPTY(s) (sbase + 8u * (ns + (s)))
     if (threadIdx.x == 0) {
@@ -141,10 +142,11 @@ __global__ void __launch_bounds__(R * (kRtTile / (4 * V)), 512 / (R * (kRtTile /
     // copies are not issued from the critical path):
     // the next unit to load, (tile pt of this CTA, fragment pj) into slot psl
     // of phase pph; NSLOT-1 units run ahead
-    u32 pj = 0, pt = blockIdx.x, psl = 0, pph = 0, pb = 0, px = 0;
+    u32 pj = 0, pu = blockIdx.x, psl = 0, pph = 0, pb = 0, px = 0;
     auto produce = [&]() {
-        if (pt >= ntiles) return;
+        if (pu >= nunits) return;
         if (pj == 0) {
+            const u32 pt = pu / G;
             pb = pt / tpb;
             px = static_cast<u32>((a.off + u64(pt - pb * tpb) * TILE) / 8u); // 8-byte TMA elements
         }
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(R * (kRtTile / (4 * V)), 512 / (R * (kRtTile /
         mbar_expect_tx(FULL(psl), SLOT);
         tma3d(a.slot0 + sbase + psl * SLOT, &a.tm[pj], px, 0u, pb, FULL(psl));
         if (++psl == ns) psl = 0, pph ^= 1u;
-        if (++pj == k) pj = 0, pt += gridDim.x;
+        if (++pj == k) pj = 0, pu += gridDim.x;
     };
     const u32 PROD = a.prod;
     if (threadIdx.x == PROD)
@@ -160,11 +162,12 @@ __global__ void __launch_bounds__(R * (kRtTile / (4 * V)), 512 / (R * (kRtTile /
     const u32 part = R == 1 ? 0u : threadIdx.x / CPP;
     const u32 col = R == 1 ? threadIdx.x : threadIdx.x % CPP;
     const u64 S = a.S;
-    const u32 ep = a.epart[part];
-    const u32 list0 = ops_s + a.opoff[part][0]; // this part's op lists, input 0 first
     u32 sl = 0, ph = 0;
-    for (u32 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (u32 u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const u32 t = u / G, g = u - t * G;
         const u32 b = t / tpb, tt = t - b * tpb;
+        const u32 ep = a.epart[g][part];
+        const u32 list0 = ops_s + a.opoff[g][part][0]; // this part's op lists, input 0 first
         u32 acc[E][AR][V];
 #pragma unroll
         for (int i = 0; i < E; ++i)
@@ -219,7 +222,7 @@ __global__ void __launch_bounds__(R * (kRtTile / (4 * V)), 512 / (R * (kRtTile /
                             for (int v = 0; v < V; ++v) acc[i][r][v] ^= acc[i][t2][v];
             }
             if (live) {
-                std::uint8_t* dst = a.out[part * kRtPartE + i] + o;
+                std::uint8_t* dst = a.out[g][part * kRtPartE + i] + o;
 #pragma unroll
                 for (int r = 0; r < W; ++r) st_cs<V>(dst + r * S, acc[i][r]);
             }

@@ -743,7 +743,7 @@ bool ring_rt_eligible(const Program& p, const std::uint8_t* const* in, std::uint
     for (std::uint32_t j = 0; ok && j < p.cols; ++j) ok = aligned(in[j], 16);
     for (std::uint32_t i = 0; ok && i < p.rows; ++i) ok = aligned(out[i], 16);
     if (!ok) return false;
-    if ((len + kRtTile - 1) / kRtTile * nb >= (std::uint64_t(1) << 31)) return false;
+    if ((len + kRtTile - 1) / kRtTile * nb * kRtMaxGroups >= (std::uint64_t(1) << 31)) return false;
     return !unsafe_alias(p, in, out, strip, nb, in_pitch, out_pitch);
 }
 
@@ -811,16 +811,28 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
     // (16 warps per SM): V = 4 (16 bytes of each strip per thread) halves the
     // dispatch per XOR and doubles the XORs between jumps; V = 2 holds more
     // outputs per part.  A single output runs one 256-thread part per CTA, two
-    // CTAs per SM.  More outputs than one launch holds go to further launches
-    // (each re-reads the inputs).
+    // CTAs per SM.  More outputs than one CTA holds form output groups: each
+    // (tile, group) is a unit of the same launch, and the groups of a tile run on
+    // neighbouring CTAs, so the tile's re-reads come from L2, not HBM.  Past
+    // kRtMaxGroups groups, further launches.
     static const int vknob = env_int("PYRIT_B200_RT_V", 4);
     const std::uint32_t V = vknob == 2 ? 2u : 4u;
     const std::uint32_t ep = static_cast<std::uint32_t>(rt_part_outputs(static_cast<int>(n), static_cast<int>(w),
                                                                         static_cast<int>(V)));
-    const std::uint32_t per_launch = (V == 4 ? 4u : 2u) * ep;
+    const std::uint32_t per_group = (V == 4 ? 4u : 2u) * ep;
     LaunchInfo info;
-    for (std::uint32_t i0 = 0; i0 < p.rows; i0 += per_launch) {
-        const std::uint32_t e = std::min(per_launch, p.rows - i0);
+    auto r_for = [&](std::uint32_t e) { return e == 1 ? 1u : V == 2 ? 2u : e <= 2 * ep ? 2u : 4u; };
+    for (std::uint32_t i0 = 0, e = 0; i0 < p.rows; i0 += e) {
+        // as many groups as fit the op budget (ring terms + one sentinel per list)
+        e = std::min(per_group * kRtMaxGroups, p.rows - i0);
+        for (;;) {
+            std::uint64_t terms = 0;
+            for (std::uint32_t i = 0; i < e; ++i)
+                for (std::uint32_t j = 0; j < k; ++j) terms += std::popcount(p.reps[std::size_t(i0 + i) * k + j]);
+            const std::uint64_t lists = std::uint64_t((e + per_group - 1) / per_group) * r_for(e) * k;
+            if (terms + lists + 2 < kRtMaxOps || e == 1) break;
+            e = e > per_group ? (e - 1) / per_group * per_group : e - 1;
+        }
         if (e == 1) {
             l.V = 2;
             l.R = 1;
@@ -831,51 +843,63 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
             l.V = 4;
             l.R = e <= 2 * ep ? 2u : 4u;
         }
-        l.E = (e + l.R - 1) / l.R;
-        // the parts run in lockstep on the shared slots, so give them equal
-        // ring terms: heaviest output first onto the lightest part with room
-        // (config 5's rows weigh 16/62/72/80)
+        const std::uint32_t G = (e + per_group - 1) / per_group;
+        l.E = (e + l.R * G - 1) / (l.R * G);
+        a.ngrp = G;
+        // the parts of a group run in lockstep on the shared slots, so give
+        // them equal ring terms: heaviest output first onto the lightest
+        // (group, part) bin with room (config 5's rows weigh 16/62/72/80)
         std::vector<std::uint32_t> wt(e, 0), order(e);
         for (std::uint32_t i = 0; i < e; ++i) {
             order[i] = i;
             for (std::uint32_t j = 0; j < k; ++j) wt[i] += std::popcount(p.reps[std::size_t(i0 + i) * k + j]);
         }
         std::stable_sort(order.begin(), order.end(), [&](std::uint32_t x, std::uint32_t y) { return wt[x] > wt[y]; });
-        std::vector<std::uint32_t> part_rows[kRtParts];
-        std::uint32_t load[kRtParts] = {};
+        const std::uint32_t bins = G * l.R;
+        std::vector<std::vector<std::uint32_t>> rows_of(bins);
+        std::vector<std::uint32_t> load(bins, 0);
         for (std::uint32_t i : order) {
-            std::uint32_t best = kRtParts;
-            for (std::uint32_t q = 0; q < l.R; ++q)
-                if (part_rows[q].size() < l.E && (best == kRtParts || load[q] < load[best])) best = q;
-            part_rows[best].push_back(i0 + i);
+            std::uint32_t best = bins;
+            for (std::uint32_t q = 0; q < bins; ++q)
+                if (rows_of[q].size() < l.E && (best == bins || load[q] < load[best])) best = q;
+            rows_of[best].push_back(i0 + i);
             load[best] += wt[i];
         }
-        for (std::uint32_t q = 0; q < kRtParts; ++q) {
-            std::sort(part_rows[q].begin(), part_rows[q].end());
-            a.epart[q] = static_cast<std::uint32_t>(part_rows[q].size());
+        std::memset(a.epart, 0, sizeof a.epart);
+        for (std::uint32_t q = 0; q < bins; ++q) {
+            std::sort(rows_of[q].begin(), rows_of[q].end());
+            a.epart[q / l.R][q % l.R] = static_cast<std::uint32_t>(rows_of[q].size());
         }
-        std::uint32_t light = 0;
-        for (std::uint32_t q = 1; q < l.R; ++q)
-            if (load[q] <= load[light]) light = q;
+        // the TMA producer: the first thread of the part that carries least over all groups
+        std::uint32_t light = 0, light_load = ~0u;
+        for (std::uint32_t part = 0; part < l.R; ++part) {
+            std::uint32_t sum = 0;
+            for (std::uint32_t g = 0; g < G; ++g) sum += load[g * l.R + part];
+            if (sum <= light_load) light = part, light_load = sum;
+        }
         a.prod = light * rt_part_threads(l.V);
         const std::uint32_t cta_threads = l.R * rt_part_threads(l.V);
         const std::uint32_t ctas_per_sm = 512 / cta_threads;
-        // op lists, one per (part, input), each ended by the sentinel E*n
+        // op lists, one per (group, part, input), each ended by the sentinel E*n
         std::uint32_t nops = 0;
-        for (std::uint32_t part = 0; part < l.R; ++part) {
-            const std::uint32_t ne = a.epart[part];
-            for (std::uint32_t j = 0; j < k; ++j) {
-                a.opoff[part][j] = static_cast<std::uint16_t>(nops);
-                for (std::uint32_t i = 0; i < ne; ++i)
-                    for (std::uint32_t m = p.reps[std::size_t(part_rows[part][i]) * k + j]; m; m &= m - 1) {
-                        if (nops + 2 >= kRtMaxOps) raise(Errc::InvalidArgument, "ring_rt: too many ring terms per launch");
-                        a.ops[nops++] = static_cast<std::uint8_t>(i * n + static_cast<std::uint32_t>(std::countr_zero(m)));
-                    }
-                a.ops[nops++] = static_cast<std::uint8_t>(l.E * n);
+        for (std::uint32_t g = 0; g < G; ++g)
+            for (std::uint32_t part = 0; part < l.R; ++part) {
+                const std::vector<std::uint32_t>& pr = rows_of[g * l.R + part];
+                const std::uint32_t ne = static_cast<std::uint32_t>(pr.size());
+                for (std::uint32_t j = 0; j < k; ++j) {
+                    a.opoff[g][part][j] = static_cast<std::uint16_t>(nops);
+                    for (std::uint32_t i = 0; i < ne; ++i)
+                        for (std::uint32_t m = p.reps[std::size_t(pr[i]) * k + j]; m; m &= m - 1) {
+                            if (nops + 2 >= kRtMaxOps)
+                                raise(Errc::InvalidArgument, "ring_rt: too many ring terms per launch");
+                            a.ops[nops++] =
+                                static_cast<std::uint8_t>(i * n + static_cast<std::uint32_t>(std::countr_zero(m)));
+                        }
+                    a.ops[nops++] = static_cast<std::uint8_t>(l.E * n);
+                }
+                a.opoff[g][part][k] = static_cast<std::uint16_t>(nops);
+                for (std::uint32_t i = 0; i < ne; ++i) a.out[g][part * kRtPartE + i] = out[pr[i]];
             }
-            a.opoff[part][k] = static_cast<std::uint16_t>(nops);
-            for (std::uint32_t i = 0; i < ne; ++i) a.out[part * kRtPartE + i] = out[part_rows[part][i]];
-        }
         a.ops[nops] = 0; // the byte the last list's look-ahead reads
         a.nops = nops + 1;
         // shared memory: mbarriers, op lists, then as many fragment slots as fit (<= 32)
@@ -888,8 +912,8 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
         a.nslot = ns;
         a.slot0 = bar;
         l.smem = bar + ns * slot;
-        l.blocks = static_cast<unsigned>(
-            std::max<std::uint64_t>(1, std::min<std::uint64_t>(tpb * nb, std::uint64_t(ctas_per_sm) * sm_count())));
+        l.blocks = static_cast<unsigned>(std::max<std::uint64_t>(
+            1, std::min<std::uint64_t>(tpb * nb * G, std::uint64_t(ctas_per_sm) * sm_count())));
         call.args.push_back(std::make_unique<RtArgs>(a));
         call.launches.push_back(l);
         info.blocks = l.blocks;

@@ -58,9 +58,11 @@ def rt_launched() -> str:
 @pytest.mark.parametrize("f", FIELDS, ids=lambda f: f"w{f.w}n{f.n}")
 @pytest.mark.parametrize("kind", [0, 1])
 def test_random_matrices_match_oracle(cuda, f, kind):
-    """Random GF(2^w) matrices, e = 1 .. past one launch's outputs, k up to 64."""
+    """Random GF(2^w) matrices, e = 1 .. past one launch's outputs (output groups of one launch,
+    then further launches), k up to 64."""
     rng = np.random.default_rng(1000 * f.w + kind)
-    for e, k in [(1, 1), (2, 3), (3, 7), (4, 10), (5, 16), (8, 12), (9, 5), (17, 3), (4, 64), (2, 33)]:
+    for e, k in [(1, 1), (2, 3), (3, 7), (4, 10), (5, 16), (8, 12), (9, 5), (17, 3), (4, 64), (2, 33), (20, 40),
+                 (40, 3)]:
         m = rng.integers(0, 1 << f.w, (e, k), dtype=np.uint16)
         m[rng.random((e, k)) < 0.1] = 0  # zero entries: no ops
         plan = P.Plan.create(f, m, P.TransformKind(kind))
