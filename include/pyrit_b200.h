@@ -141,6 +141,13 @@ int pyrit_plan_source(const pyrit_plan* plan, uint32_t lanes, char* buf, size_t 
  * device involved); used to test the compiler where no GPU exists */
 int pyrit_plan_interpret(const pyrit_plan* plan, const uint8_t* const* in, uint8_t* const* out,
                          uint64_t strip_bytes, uint64_t off, uint64_t len);
+/* verification aid: runs, on HOST buffers, the launch plan the runtime-matrix
+ * ring kernel would get for this stripe batch (output groups and parts, op
+ * lists read back from its kernel parameters) -- the CPU check of that planner.
+ * Same arguments as pyrit_cu_apply_batch minus the stream; buffers 16-byte
+ * aligned, strip/off/len multiples of 16, a ring geometry with an AOT kernel. */
+int pyrit_rt_interpret(const pyrit_plan* plan, const uint8_t* const* in, uint8_t* const* out, uint64_t strip_bytes,
+                       uint64_t off, uint64_t len, uint64_t stripes, uint64_t in_pitch, uint64_t out_pitch);
 void pyrit_plan_destroy(pyrit_plan* plan);
 
 /* ---- plans from a reference schedule (the replay operator) ------------ */

@@ -266,6 +266,15 @@ class Plan:
                                             _ptr_array([a.ctypes.data for a in outs]), strip, off, length))
         return list(outs)
 
+    def interpret_rt(self, in_ptrs: Sequence[int], out_ptrs: Sequence[int], strip: int, off: int = 0,
+                     length: int | None = None, stripes: int = 1, in_pitch: int = 0, out_pitch: int = 0) -> None:
+        """The runtime-matrix kernel's launch plan run on HOST memory (pointers to 16-byte
+        aligned host buffers; verification of the planner only)."""
+        self._counts(in_ptrs, out_ptrs)
+        length = strip - off if length is None else length
+        L.check(_clib().pyrit_rt_interpret(self._h, _ptr_array(in_ptrs), _ptr_array(out_ptrs), strip, off, length,
+                                           stripes, in_pitch, out_pitch))
+
     def _counts(self, ins, outs) -> None:
         """The C ABI reads in[]/out[] by slot count: refuse short pointer lists here."""
         if self.slots is None:

@@ -57,7 +57,7 @@ EXPORTS = (
     "pyrit_field_id", "pyrit_field_from_id", "pyrit_shard_path", "pyrit_encode_file", "pyrit_decode_file",
     "pyrit_set_file_chunk", "pyrit_cu_encode_crs", "pyrit_encode_crs_host", "pyrit_encode_host_devices",
     "pyrit_decode_host_devices", "pyrit_plan_from_schedule", "pyrit_apply_host", "pyrit_jit_info",
-    "pyrit_jit_wait", "pyrit_jit_time",
+    "pyrit_jit_wait", "pyrit_jit_time", "pyrit_rt_interpret",
 )
 
 HEADER_SIZE = 29
@@ -113,6 +113,7 @@ def load():
     lib.pyrit_cu_last_launch.argtypes = [vp, C.c_size_t, vp, vp]
     lib.pyrit_jit_compiles.restype = u64
     lib.pyrit_jit_time.argtypes = [P(C.c_double), P(C.c_double)]
+    lib.pyrit_rt_interpret.argtypes = [vp, vp, vp, u64, u64, u64, u64, u64, u64]
     lib.pyrit_kernel_launches.restype = u64
     lib.pyrit_field_named.argtypes = [C.c_char_p, P(pyrit_field)]
     lib.pyrit_field_validate.argtypes = [P(pyrit_field)]

@@ -503,6 +503,17 @@ int pyrit_cu_decode(const pyrit_code* code, uint8_t* const* symbols, const uint3
     });
 }
 
+int pyrit_rt_interpret(const pyrit_plan* plan, const uint8_t* const* in, uint8_t* const* out, uint64_t strip_bytes,
+                       uint64_t off, uint64_t len, uint64_t stripes, uint64_t in_pitch, uint64_t out_pitch) {
+    return guarded([&] {
+        if (!plan || !in || !out) raise(Errc::InvalidArgument, "null argument");
+        if (plan->sched) raise(Errc::InvalidArgument, "replayed schedules do not run on the runtime-matrix kernel");
+        if (off + len > strip_bytes) raise(Errc::BufferShape, "column window out of range");
+        if (len == 0 || stripes == 0 || plan->prog.rows == 0) return;
+        interpret_ring_rt(plan->prog, in, out, strip_bytes, off, len, stripes, in_pitch, out_pitch);
+    });
+}
+
 int pyrit_cu_apply_batch(const pyrit_plan* plan, const uint8_t* const* in, uint8_t* const* out,
                          uint64_t strip_bytes, uint64_t off, uint64_t len, uint64_t stripes, uint64_t in_pitch,
                          uint64_t out_pitch, void* stream) {

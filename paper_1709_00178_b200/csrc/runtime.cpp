@@ -763,9 +763,11 @@ struct RtCall {
     LaunchInfo info;
 };
 
+// device = false: the same launch plan without tensor maps or a device query
+// (interpret_ring_rt, the host check of the planner)
 void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
                    std::uint64_t strip, std::uint64_t off, std::uint64_t len, std::uint64_t nb, std::uint64_t in_pitch,
-                   std::uint64_t out_pitch) {
+                   std::uint64_t out_pitch, bool device = true) {
     call.args.clear();
     call.launches.clear();
     RtArgs tmpl;
@@ -775,7 +777,7 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
     const std::uint64_t tpb = (len + tile - 1) / tile;
     static const int promo_knob = env_int("PYRIT_B200_TMA_PROMO", 3);
     const CUtensorMapL2promotion promo = static_cast<CUtensorMapL2promotion>(std::min(3, std::max(0, promo_knob)));
-    for (std::uint32_t j = 0; j < k; ++j) {
+    for (std::uint32_t j = 0; device && j < k; ++j) {
         CUtensorMap m;
         const cuuint64_t dims[3] = {strip / elem, w, nb};
         const cuuint64_t strides[2] = {strip, nb > 1 ? in_pitch : strip * w};
@@ -912,7 +914,7 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
         a.nslot = ns;
         a.slot0 = bar;
         l.smem = bar + ns * slot;
-        l.blocks = static_cast<unsigned>(std::max<std::uint64_t>(
+        l.blocks = !device ? 1u : static_cast<unsigned>(std::max<std::uint64_t>(
             1, std::min<std::uint64_t>(tpb * nb * G, std::uint64_t(ctas_per_sm) * sm_count())));
         call.args.push_back(std::make_unique<RtArgs>(a));
         call.launches.push_back(l);
@@ -925,7 +927,81 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
     call.info = info;
 }
 
+// x^t mod p (ring_rt.cu xpow_mod)
+std::uint32_t rt_xpow_mod(std::uint32_t t, std::uint32_t p, std::uint32_t w) {
+    std::uint64_t a = std::uint64_t(1) << t;
+    for (std::uint32_t d = t; d >= w; --d)
+        if ((a >> d) & 1u) a ^= std::uint64_t(p) << (d - w);
+    return static_cast<std::uint32_t>(a);
+}
+
 } // namespace
+
+// Host restatement of what the runtime-matrix kernel computes from the launch
+// plan it would be given: same units (tile, group), parts, op lists (read back
+// from the kernel parameters), parity extension, fold and column window, one
+// 8-byte column word at a time.  Lets CPU tests check the planner (balancing,
+// groups, op encoding, op budget) against the oracle without a GPU.
+void interpret_ring_rt(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out, std::uint64_t strip,
+                       std::uint64_t off, std::uint64_t len, std::uint64_t nb, std::uint64_t in_pitch,
+                       std::uint64_t out_pitch) {
+    if (nb == 1) in_pitch = out_pitch = 0;
+    if (!ring_rt_eligible(p, in, out, strip, off, len, nb, in_pitch, out_pitch))
+        raise(Errc::InvalidArgument, "not a runtime-matrix kernel launch (geometry, alignment or aliasing)");
+    RtCall call;
+    build_ring_rt(call, p, in, out, strip, off, len, nb, in_pitch, out_pitch, false);
+    const std::uint32_t w = p.field.w, n = p.field.n, k = p.cols;
+    const bool par = p.kind == TransformKind::Parity;
+    const std::uint32_t xr = par ? n : w, ar = par ? w : n;
+    const std::uint64_t ibp = nb > 1 ? in_pitch : strip * w;
+    for (std::size_t c = 0; c < call.launches.size(); ++c) {
+        const RtArgs& a = *call.args[c];
+        const RtLaunch& l = call.launches[c];
+        const std::uint32_t E = l.E, G = a.ngrp;
+        std::vector<std::uint64_t> acc(std::size_t(E) * ar), x(n);
+        for (std::uint64_t u = 0; u < std::uint64_t(a.ntiles) * G; ++u) {
+            const std::uint64_t t = u / G, g = u % G, b = t / a.tpb, tt = t - b * a.tpb;
+            for (std::uint32_t part = 0; part < l.R; ++part) {
+                const std::uint32_t ep = a.epart[g][part];
+                for (std::uint64_t col = 0; col < kRtTile; col += 8) {
+                    const std::uint64_t rel = tt * kRtTile + col;
+                    if (rel >= a.len) break; // the kernel loads these columns but never stores them
+                    std::fill(acc.begin(), acc.end(), 0);
+                    std::uint32_t q = a.opoff[g][part][0];
+                    for (std::uint32_t j = 0; j < k; ++j) {
+                        for (std::uint32_t s2 = 0; s2 < w; ++s2)
+                            std::memcpy(&x[s2], in[j] + b * ibp + s2 * strip + a.off + rel, 8);
+                        if (par)
+                            for (std::uint32_t q2 = w; q2 < n; ++q2) {
+                                x[q2] = 0;
+                                for (std::uint32_t i = 0; i < w; ++i)
+                                    if (a.fm[(q2 - w) * w + i]) x[q2] ^= x[i];
+                            }
+                        for (;;) {
+                            const std::uint32_t op = a.ops[q++];
+                            if (op == E * n) break;
+                            const std::uint32_t i = op / n, sh = op % n;
+                            for (std::uint32_t s2 = 0; s2 < xr; ++s2) {
+                                const std::uint32_t r = (s2 + sh) % n;
+                                if (par && r >= w) continue;
+                                acc[std::size_t(i) * ar + r] ^= x[s2];
+                            }
+                        }
+                    }
+                    for (std::uint32_t i = 0; i < ep; ++i) {
+                        std::uint64_t* A = &acc[std::size_t(i) * ar];
+                        if (!par)
+                            for (std::uint32_t t2 = w; t2 < n; ++t2)
+                                for (std::uint32_t r = 0; r < w; ++r)
+                                    if ((rt_xpow_mod(t2, p.field.modulus, w) >> r) & 1u) A[r] ^= A[t2];
+                        std::uint8_t* dst = a.out[g][part * kRtPartE + i] + a.off + rel + b * a.obp;
+                        for (std::uint32_t r = 0; r < w; ++r) std::memcpy(dst + r * strip, &A[r], 8);
+                    }
+                }
+            }
+        }
+    }
+}
 
 LaunchInfo launch_ring_rt_program(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
                                   std::uint64_t strip, std::uint64_t off, std::uint64_t len, std::uint64_t nb,
