@@ -107,7 +107,9 @@ __host__ __device__ constexpr u32 xpow_mod(int t, u32 p, int w) {
 
 // R parts of CPP threads, V 32-bit words of every strip per thread; a CTA is
 // 256 or 512 threads and an SM holds 512 (16 warps, <= 128 registers each)
-template <int W, int N, u32 P, int E, int R, int V, bool PAR>
+// GRP: more than one output group (units = tiles x groups); without it the
+// group is the constant 0 and its parameters are loop invariant
+template <int W, int N, u32 P, int E, int R, int V, bool PAR, bool GRP>
 __global__ void __launch_bounds__(R * (kRtTile / (4 * V)), 512 / (R * (kRtTile / (4 * V))))
     ring_rt_kernel(const __grid_constant__ RtArgs a) {
     constexpr u32 TILE = kTile, CPP = kRtTile / (4u * V);
@@ -119,7 +121,7 @@ __global__ void __launch_bounds__(R * (kRtTile / (4 * V)), 512 / (R * (kRtTile /
     const u32 ns = a.nslot;
     const u32 k = a.k;
     const u32 ntiles = a.ntiles, tpb = a.tpb;
-    const u32 G = a.ngrp, nunits = ntiles * G; // unit u = (tile u / G, output group u % G)
+    const u32 G = GRP ? a.ngrp : 1u, nunits = ntiles * G; // unit u = (tile u / G, output group u % G)
 #define FULL(s) (sbase + 8u * (s))
 #define EMPTY(s) (sbase + 8u * (ns + (s)))
     if (threadIdx.x == 0) {
@@ -146,7 +148,7 @@ __global__ void __launch_bounds__(R * (kRtTile / (4 * V)), 512 / (R * (kRtTile /
     auto produce = [&]() {
         if (pu >= nunits) return;
         if (pj == 0) {
-            const u32 pt = pu / G;
+            const u32 pt = GRP ? pu / G : pu;
             pb = pt / tpb;
             px = static_cast<u32>((a.off + u64(pt - pb * tpb) * TILE) / 8u); // 8-byte TMA elements
         }
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(R * (kRtTile / (4 * V)), 512 / (R * (kRtTile /
     const u64 S = a.S;
     u32 sl = 0, ph = 0;
     for (u32 u = blockIdx.x; u < nunits; u += gridDim.x) {
-        const u32 t = u / G, g = u - t * G;
+        const u32 t = GRP ? u / G : u, g = GRP ? u - t * G : 0u;
         const u32 b = t / tpb, tt = t - b * tpb;
         const u32 ep = a.epart[g][part];
         const u32 list0 = ops_s + a.opoff[g][part][0]; // this part's op lists, input 0 first
@@ -233,9 +235,9 @@ __global__ void __launch_bounds__(R * (kRtTile / (4 * V)), 512 / (R * (kRtTile /
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-template <int W, int N, u32 P, int E, int R, int V, bool PAR>
-cudaError_t launch_one(const RtArgs& a, const RtLaunch& l) {
-    auto fn = ring_rt_kernel<W, N, P, E, R, V, PAR>;
+template <int W, int N, u32 P, int E, int R, int V, bool PAR, bool GRP>
+cudaError_t launch_grp(const RtArgs& a, const RtLaunch& l) {
+    auto fn = ring_rt_kernel<W, N, P, E, R, V, PAR, GRP>;
     static bool attr_set[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -255,6 +257,14 @@ cudaError_t launch_one(const RtArgs& a, const RtLaunch& l) {
     cfg.attrs = attr;
     cfg.numAttrs = l.pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, fn, a);
+}
+
+template <int W, int N, u32 P, int E, int R, int V, bool PAR>
+cudaError_t launch_one(const RtArgs& a, const RtLaunch& l) {
+    // a single output (R = 1) never has groups
+    if constexpr (R > 1)
+        if (a.ngrp > 1) return launch_grp<W, N, P, E, R, V, PAR, true>(a, l);
+    return launch_grp<W, N, P, E, R, V, PAR, false>(a, l);
 }
 
 template <int W, int N, u32 P, int R, int V, bool PAR, int E>

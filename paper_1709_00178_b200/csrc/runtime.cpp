@@ -821,9 +821,12 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
     const std::uint32_t V = vknob == 2 ? 2u : 4u;
     const std::uint32_t ep = static_cast<std::uint32_t>(rt_part_outputs(static_cast<int>(n), static_cast<int>(w),
                                                                         static_cast<int>(V)));
-    const std::uint32_t per_group = (V == 4 ? 4u : 2u) * ep;
+    // PYRIT_B200_RT_PARTS=2: at most two parts per CTA (two CTAs per SM, more groups)
+    static const int parts_knob = env_int("PYRIT_B200_RT_PARTS", 4);
+    const std::uint32_t max_parts = V == 4 && parts_knob != 2 ? 4u : 2u;
+    const std::uint32_t per_group = max_parts * ep;
     LaunchInfo info;
-    auto r_for = [&](std::uint32_t e) { return e == 1 ? 1u : V == 2 ? 2u : e <= 2 * ep ? 2u : 4u; };
+    auto r_for = [&](std::uint32_t e) { return e == 1 ? 1u : V == 2 || max_parts == 2 ? 2u : e <= 2 * ep ? 2u : 4u; };
     for (std::uint32_t i0 = 0, e = 0; i0 < p.rows; i0 += e) {
         // as many groups as fit the op budget (ring terms + one sentinel per list)
         e = std::min(per_group * kRtMaxGroups, p.rows - i0);
@@ -843,7 +846,7 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
             l.R = 2;
         } else {
             l.V = 4;
-            l.R = e <= 2 * ep ? 2u : 4u;
+            l.R = r_for(e);
         }
         const std::uint32_t G = (e + per_group - 1) / per_group;
         l.E = (e + l.R * G - 1) / (l.R * G);
