@@ -156,3 +156,46 @@ def test_planner_negative_control(f):
     assert not np.array_equal(bad[2], want[2])
     for i in (0, 1, 3):
         np.testing.assert_array_equal(bad[i], want[i])
+
+
+from hypothesis import given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+
+@st.composite
+def rt_cases(draw):
+    f = draw(st.sampled_from(FIELDS))
+    kind = draw(st.sampled_from([0, 0, 1]))
+    e = draw(st.integers(1, 40))
+    k = draw(st.integers(1, 64))
+    strip = 16 * draw(st.integers(1, 400))
+    off = 16 * draw(st.integers(0, strip // 16 - 1))
+    length = 16 * draw(st.integers(1, (strip - off) // 16))
+    nb = draw(st.sampled_from([1, 1, 2, 3]))
+    seed = draw(st.integers(0, 2**31 - 1))
+    return f, kind, e, k, strip, off, length, nb, seed
+
+
+@settings(max_examples=120, deadline=None)
+@given(rt_cases())
+def test_planner_property(case):
+    """Random geometry, transform, output count (parts, groups, launches), input count,
+    strip, column window and stripe batch: the runtime-matrix launch plan reproduces the
+    oracle inside the window and leaves every byte outside it untouched."""
+    f, kind, e, k, strip, off, length, nb, seed = case
+    rng = np.random.default_rng(seed)
+    m = rng.integers(0, 1 << f.w, (e, k), dtype=np.uint16)
+    plan = P.Plan.create(f, m, P.TransformKind(kind))
+    sym = f.w * strip
+    data = aligned((nb * k, sym))
+    data[...] = rng.integers(0, 256, (nb * k, sym), dtype=np.uint8)
+    got = run_rt(plan, data, e, strip, off, length, stripes=nb)
+    for b in range(nb):
+        want = oracle_ring(f, m, data[b * k:(b + 1) * k], kind=kind)
+        for i in range(e):
+            for s in range(f.w):
+                lo, hi = s * strip + off, s * strip + off + length
+                row = got[b * e + i]
+                np.testing.assert_array_equal(row[lo:hi], want[i, lo:hi])
+                assert (row[s * strip:lo] == 0x5A).all() and (row[hi:(s + 1) * strip] == 0x5A).all()
+    plan.close()
