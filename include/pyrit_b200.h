@@ -150,6 +150,28 @@ int pyrit_rt_interpret(const pyrit_plan* plan, const uint8_t* const* in, uint8_t
                        uint64_t off, uint64_t len, uint64_t stripes, uint64_t in_pitch, uint64_t out_pitch);
 void pyrit_plan_destroy(pyrit_plan* plan);
 
+/* ---- a raw ring-representative matrix (SURVEY 8(b) pyrit_cu_ringmat) --- */
+/* rows x cols ring elements, row-major n-bit shift masks: the reference's
+ * RingElem / to_shift_set form (ring.hpp:94-102, schedule.hpp:78), any
+ * element of each coset under the Embedding transform -- it stands for the
+ * field element u mod p (phi_E^{-1}); the Parity transform takes the
+ * canonical (sparse_transform) representative only.  Applied by the runtime-matrix ring kernel with the masks in
+ * its kernel parameters: no code generation and no compile (16-byte aligned
+ * buffers, strip, window; the AOT ring geometries -- anything else runs the
+ * generated kernel of the field matrix, the same symbols). */
+typedef struct pyrit_ringmat {
+    pyrit_field field;
+    uint32_t transform; /* 0 Embedding, 1 Parity */
+    uint32_t rows, cols;
+    const uint32_t* reps;
+} pyrit_ringmat;
+/* a plan of it (all the pyrit_cu_apply* / interpret entry points take it) */
+int pyrit_plan_from_ringmat(const pyrit_ringmat* m, pyrit_plan** out);
+/* one call: out[i] = sum_j reps[i][j] * in[j] over the window, the program
+ * cached by matrix (replay, codec.hpp:118-157, with the masks as the operand) */
+int pyrit_cu_apply_ringmat(const pyrit_ringmat* m, const uint8_t* const* in, uint8_t* const* out,
+                           uint64_t strip_bytes, uint64_t off, uint64_t len, void* stream);
+
 /* ---- plans from a reference schedule (the replay operator) ------------ */
 /* One region op of an XorSchedule, laid out like the reference's XorOp
  * (schedule.hpp:42-48; mode = OpMode: 0 Copy, 1 Xor, 2 Zero), so a

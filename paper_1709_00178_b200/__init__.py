@@ -197,6 +197,16 @@ class Plan:
         return cls(h)
 
     @classmethod
+    def from_ringmat(cls, f: FieldSpec, reps: np.ndarray, transform=TransformKind.Embedding) -> "Plan":
+        """A plan of raw ring representatives (n-bit shift masks, any element of each coset;
+        SURVEY 8(b) pyrit_cu_ringmat): runs on the runtime-matrix kernel, never compiled."""
+        r = np.ascontiguousarray(reps, dtype=np.uint32)
+        m = L.pyrit_ringmat(f.c(), int(transform), r.shape[0], r.shape[1], r.ctypes.data)
+        h = C.c_void_p()
+        L.check(_clib().pyrit_plan_from_ringmat(C.byref(m), C.byref(h)))
+        return cls(h)
+
+    @classmethod
     def from_schedule(cls, sched: XorSchedule, labels: Sequence[int] | None = None) -> "Plan":
         """Any XorSchedule as one fused kernel with replay()'s semantics (codec.hpp:118-157); labels:
         k + outputs storage labels, equal labels = slots sharing storage (None = all distinct)."""
@@ -398,6 +408,20 @@ def parallel_replay(sched: XorSchedule, inp, in_map: Sequence[int], out, out_map
     """parallel_replay (codec.hpp:176-193): replay over the whole packet (the column windows of the
     reference's threads are one grid here)."""
     replay(sched, inp, in_map, out, out_map, 0, None, device)
+
+
+def apply_ringmat(f: FieldSpec, reps: np.ndarray, in_ptrs: Sequence[int], out_ptrs: Sequence[int], strip: int,
+                  off: int = 0, length: int | None = None, transform=TransformKind.Embedding,
+                  stream: int | None = None) -> None:
+    """out[i] = sum_j reps[i][j] * in[j] on device pointers (pyrit_cu_apply_ringmat): the
+    runtime-matrix kernel with the masks in its parameters, asynchronously on `stream`."""
+    r = np.ascontiguousarray(reps, dtype=np.uint32)
+    if len(in_ptrs) < r.shape[1] or len(out_ptrs) < r.shape[0]:
+        raise PyritError(4, f"{r.shape[1]} input and {r.shape[0]} output symbols expected")
+    length = strip - off if length is None else length
+    m = L.pyrit_ringmat(f.c(), int(transform), r.shape[0], r.shape[1], r.ctypes.data)
+    L.check(_clib().pyrit_cu_apply_ringmat(C.byref(m), _ptr_array(in_ptrs), _ptr_array(out_ptrs), strip, off, length,
+                                           stream))
 
 
 def encode(data, code: CodeSpec):

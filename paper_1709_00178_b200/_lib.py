@@ -24,6 +24,11 @@ class pyrit_code(C.Structure):
     _fields_ = [("k", C.c_uint32), ("r", C.c_uint32), ("field", pyrit_field), ("transform", C.c_uint32)]
 
 
+class pyrit_ringmat(C.Structure):
+    _fields_ = [("field", pyrit_field), ("transform", C.c_uint32), ("rows", C.c_uint32), ("cols", C.c_uint32),
+                ("reps", C.c_void_p)]
+
+
 class pyrit_plan_stats(C.Structure):
     _fields_ = [("rows", C.c_uint32), ("cols", C.c_uint32), ("matrix_ones", C.c_uint64),
                 ("ref_region_ops", C.c_uint64), ("naive_xors", C.c_uint64), ("xors", C.c_uint64),
@@ -57,7 +62,7 @@ EXPORTS = (
     "pyrit_field_id", "pyrit_field_from_id", "pyrit_shard_path", "pyrit_encode_file", "pyrit_decode_file",
     "pyrit_set_file_chunk", "pyrit_cu_encode_crs", "pyrit_encode_crs_host", "pyrit_encode_host_devices",
     "pyrit_decode_host_devices", "pyrit_plan_from_schedule", "pyrit_apply_host", "pyrit_jit_info",
-    "pyrit_jit_wait", "pyrit_jit_time", "pyrit_rt_interpret",
+    "pyrit_jit_wait", "pyrit_jit_time", "pyrit_rt_interpret", "pyrit_plan_from_ringmat", "pyrit_cu_apply_ringmat",
 )
 
 HEADER_SIZE = 29
@@ -114,6 +119,8 @@ def load():
     lib.pyrit_jit_compiles.restype = u64
     lib.pyrit_jit_time.argtypes = [P(C.c_double), P(C.c_double)]
     lib.pyrit_rt_interpret.argtypes = [vp, vp, vp, u64, u64, u64, u64, u64, u64]
+    lib.pyrit_plan_from_ringmat.argtypes = [P(pyrit_ringmat), vp]
+    lib.pyrit_cu_apply_ringmat.argtypes = [P(pyrit_ringmat), vp, vp, u64, u64, u64, vp]
     lib.pyrit_kernel_launches.restype = u64
     lib.pyrit_field_named.argtypes = [C.c_char_p, P(pyrit_field)]
     lib.pyrit_field_validate.argtypes = [P(pyrit_field)]

@@ -246,6 +246,28 @@ int pyrit_plan_create(const pyrit_field* f, uint32_t transform, const uint16_t* 
     });
 }
 
+int pyrit_plan_from_ringmat(const pyrit_ringmat* m, pyrit_plan** out) {
+    return guarded([&] {
+        if (!m || !out || (!m->reps && m->rows && m->cols)) raise(Errc::InvalidArgument, "null argument");
+        if (m->transform > 1) raise(Errc::InvalidArgument, "unknown transform");
+        auto plan = std::make_unique<pyrit_plan>();
+        plan->prog = ring_program(to_field(&m->field), static_cast<TransformKind>(m->transform), m->reps, m->rows,
+                                  m->cols);
+        *out = plan.release();
+    });
+}
+
+int pyrit_cu_apply_ringmat(const pyrit_ringmat* m, const uint8_t* const* in, uint8_t* const* out,
+                           uint64_t strip_bytes, uint64_t off, uint64_t len, void* stream) {
+    return guarded([&] {
+        if (!m || !in || !out || (!m->reps && m->rows && m->cols)) raise(Errc::InvalidArgument, "null argument");
+        if (m->transform > 1) raise(Errc::InvalidArgument, "unknown transform");
+        auto p = ringmat_program(to_field(&m->field), static_cast<TransformKind>(m->transform), m->reps, m->rows,
+                                 m->cols);
+        launch_program(*p, in, out, strip_bytes, off, len, static_cast<cudaStream_t>(stream));
+    });
+}
+
 int pyrit_plan_from_schedule(const pyrit_field* f, uint32_t k, uint32_t outputs, const pyrit_xor_op* ops,
                              size_t n_ops, const uint32_t* labels, pyrit_plan** out) {
     return guarded([&] {

@@ -67,6 +67,17 @@ std::shared_ptr<const Program> encode_program(const CodeParams& c) {
     return p;
 }
 
+std::shared_ptr<const Program> ringmat_program(const Field& f, TransformKind kind, const std::uint32_t* reps,
+                                               std::uint32_t rows, std::uint32_t cols) {
+    std::string key("R");
+    key += code_key(CodeParams{cols, rows, f, kind, false});
+    key.append(reinterpret_cast<const char*>(reps), std::size_t(rows) * cols * sizeof(std::uint32_t));
+    if (auto p = cache().get(key)) return p;
+    auto p = std::make_shared<const Program>(ring_program(f, kind, reps, rows, cols));
+    cache().put(key, p);
+    return p;
+}
+
 DecodeProgram decode_program(const CodeParams& c, const std::vector<std::uint32_t>& erased, bool data_only) {
     // looked up by (code, erased list as given) before any algebra: a list that
     // was valid once is valid again; an invalid one raises below and is never cached

@@ -27,6 +27,10 @@ struct DecodeProgram {
     RepairPlan repair;                   // survivors, outputs, matrix
 };
 
+// the program of a raw ring-representative matrix (pyrit_cu_apply_ringmat), cached
+std::shared_ptr<const Program> ringmat_program(const Field& f, TransformKind kind, const std::uint32_t* reps,
+                                               std::uint32_t rows, std::uint32_t cols);
+
 // data_only: rebuild only the erased data symbols (decode_file writes data
 // symbols only, container.hpp:291-296); outputs/matrix are trimmed to them
 DecodeProgram decode_program(const CodeParams& c, const std::vector<std::uint32_t>& erased, bool data_only = false);

@@ -577,6 +577,37 @@ Program light_program(const Field& f, TransformKind kind, const Matrix& m) {
     return p;
 }
 
+Program ring_program(const Field& f, TransformKind kind, const std::uint32_t* reps, std::uint32_t rows,
+                     std::uint32_t cols) {
+    validate_field(f);
+    if (cols == 0) raise(Errc::InvalidArgument, "matrix has no columns");
+    if (rows == 0) raise(Errc::InvalidArgument, "matrix has no rows");
+    Program p;
+    p.field = f;
+    p.kind = kind;
+    p.rows = rows;
+    p.cols = cols;
+    p.fold = fold_table(f);
+    p.reps.assign(reps, reps + std::size_t(rows) * cols);
+    p.matrix.resize(p.reps.size());
+    for (std::size_t i = 0; i < p.reps.size(); ++i) {
+        if (f.n < 32 && (p.reps[i] >> f.n) != 0) raise(Errc::InvalidArgument, "ring element wider than n bits");
+        // the field element this representative stands for: u mod p (phi_E^{-1} of u)
+        p.matrix[i] = static_cast<std::uint16_t>(poly_mod(p.reps[i], f.modulus));
+        // under the Parity transform the ring action is not a function of u mod p
+        // alone (e.g. GF(2^8) in R_{2,17}), so only the canonical representative
+        // (sparse_transform, ring.hpp:77-90) keeps every kernel path equal
+        if (kind == TransformKind::Parity && p.reps[i] != sparse_transform(p.matrix[i], f))
+            raise(Errc::InvalidArgument, "the Parity transform takes the canonical (sparse) representative of each entry");
+        p.stats.matrix_ones += std::uint64_t(std::popcount(p.reps[i])) * f.w;
+    }
+    p.adhoc = true;
+    p.light = true;
+    p.key = plan_key(p);
+    p.lazy = std::make_shared<LazyCompile>();
+    return p;
+}
+
 const Program& full_program(const Program& p) {
     if (!p.light) return p;
     std::call_once(p.lazy->once, [&] {

@@ -135,6 +135,12 @@ struct LazyCompile {
 // interpreter or the statistics.
 Program light_program(const Field& f, TransformKind kind, const Matrix& m);
 const Program& full_program(const Program& p);
+// a light program from ring representatives as given (n-bit shift masks, any
+// element of each coset): the runtime-matrix kernel applies them as they are;
+// a compiled kernel, if one is ever built for it, uses the field matrix
+// u mod p, which computes the same symbols (SURVEY 8(b) pyrit_cu_ringmat)
+Program ring_program(const Field& f, TransformKind kind, const std::uint32_t* reps, std::uint32_t rows,
+                     std::uint32_t cols);
 
 // One region op of a reference XorSchedule (schedule.hpp:40-48); mode is
 // OpMode: 0 Copy, 1 Xor, 2 Zero.

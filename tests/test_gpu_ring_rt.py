@@ -256,3 +256,29 @@ def test_hot_pattern_gets_specialised_kernel(cuda, tmp_path):
     assert all(k.startswith("pyrit_ring_rt_") for k in kernels[:7]), kernels
     assert kernels[-1].startswith("pyrit_ring_k10_e4_w8_n17"), kernels  # the hot pattern, specialised
     assert int(out[1]) == 1  # one compile: the pattern used 4 times, not the one used 3 times
+
+
+@pytest.mark.parametrize("f", [G256, G4096], ids=lambda f: f"w{f.w}n{f.n}")
+def test_apply_ringmat_on_device(cuda, f):
+    """pyrit_cu_apply_ringmat (SURVEY 8(b)'s operator with the ring matrix as operand): raw
+    masks, non-canonical ones included, on the runtime kernel with no compile; on a strip
+    the runtime kernel cannot take (8-byte aligned) the compiled program of the field matrix
+    gives the same symbols."""
+    import torch
+    rng = np.random.default_rng(17)
+    e, k = 4, 12
+    m = rng.integers(0, 1 << f.w, (e, k), dtype=np.uint16)
+    reps = np.array([[P.sparse_transform(int(x), f) ^ (f.modulus if (i + j) % 3 == 0 else 0)
+                      for j, x in enumerate(row)] for i, row in enumerate(m)], dtype=np.uint32)
+    lib = L.load()
+    for strip in (4096 + 64, 4096 + 8):
+        data = rand_symbols(k, f.w * strip, strip)
+        d = torch.from_numpy(data).to(cuda)
+        out = torch.zeros((e, f.w * strip), dtype=torch.uint8, device=cuda)
+        jit0 = lib.pyrit_jit_compiles()
+        P.apply_ringmat(f, reps, [d[j].data_ptr() for j in range(k)], [out[i].data_ptr() for i in range(e)], strip)
+        torch.cuda.synchronize()
+        if strip % 16 == 0:
+            rt_launched()
+            assert lib.pyrit_jit_compiles() == jit0
+        np.testing.assert_array_equal(out.cpu().numpy(), oracle_ring(f, m, data))

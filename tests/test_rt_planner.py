@@ -199,3 +199,61 @@ def test_planner_property(case):
                 np.testing.assert_array_equal(row[lo:hi], want[i, lo:hi])
                 assert (row[s * strip:lo] == 0x5A).all() and (row[hi:(s + 1) * strip] == 0x5A).all()
     plan.close()
+
+
+def _poly_mod(a: int, p: int) -> int:
+    dp = p.bit_length() - 1
+    while a and a.bit_length() - 1 >= dp:
+        a ^= p << (a.bit_length() - 1 - dp)
+    return a
+
+
+def _clmul(a: int, b: int) -> int:
+    r = 0
+    while b:
+        if b & 1:
+            r ^= a
+        a <<= 1
+        b >>= 1
+    return r
+
+
+@pytest.mark.parametrize("f", FIELDS, ids=lambda f: f"w{f.w}n{f.n}")
+@pytest.mark.parametrize("kind", [0, 1])
+def test_ringmat_any_representative(f, kind):
+    """pyrit_plan_from_ringmat (SURVEY 8(b)'s ring-matrix operand): raw n-bit masks, minimal or
+    not -- every element u of a coset stands for the field element u mod p -- give the
+    oracle's symbols for the field matrix, both on the runtime kernel's plan (the masks as
+    given) and through the compiled program (the field matrix)."""
+    rng = np.random.default_rng(13 * f.w + kind)
+    e, k = 5, 9
+    m = rng.integers(0, 1 << f.w, (e, k), dtype=np.uint16)
+    reps = np.zeros((e, k), dtype=np.uint32)
+    for i in range(e):
+        for j in range(k):
+            u = P.sparse_transform(int(m[i, j]), f)
+            # Embedding: any element of the coset; Parity: the canonical one
+            t = int(rng.integers(0, 1 << (f.n - f.w))) if kind == 0 else 0
+            reps[i, j] = u ^ _clmul(t, f.modulus)  # another element of the same coset
+            assert reps[i, j] < (1 << f.n) and _poly_mod(int(reps[i, j]), f.modulus) == m[i, j]
+    plan = P.Plan.from_ringmat(f, reps, P.TransformKind(kind))
+    np.testing.assert_array_equal(plan.reps(), reps)
+    strip = 2048 + 16 * f.w
+    data = aligned((k, f.w * strip))
+    data[...] = rand_symbols(k, f.w * strip, 31)
+    want = oracle_ring(f, m, data, kind=kind)
+    np.testing.assert_array_equal(run_rt(plan, data, e, strip), want)
+    got = np.stack(plan.interpret([data[j] for j in range(k)], strip))  # the compiled program
+    np.testing.assert_array_equal(got, want)
+
+
+def test_ringmat_rejects_wide_elements():
+    f = G256
+    with pytest.raises(P.PyritError):
+        P.Plan.from_ringmat(f, np.array([[1 << 17]], dtype=np.uint32))
+    u = P.sparse_transform(7, f)
+    P.Plan.from_ringmat(f, np.array([[u ^ f.modulus]], dtype=np.uint32))  # Embedding: any coset element
+    with pytest.raises(P.PyritError):  # Parity: only the canonical representative
+        P.Plan.from_ringmat(f, np.array([[u ^ f.modulus]], dtype=np.uint32), P.TransformKind.Parity)
+    with pytest.raises(P.PyritError):
+        P.Plan.from_ringmat(f, np.zeros((0, 3), dtype=np.uint32))
