@@ -14,6 +14,7 @@
  *   compile_schedule     schedule.hpp:94-163        pyrit_plan_create (+ _encode/_decode)
  *   schedule_stats       schedule.hpp:216-223       pyrit_plan_get_stats
  *   replay / parallel_replay codec.hpp:118-193      pyrit_cu_apply, pyrit_apply_host
+ *   RingElem masks (to_shift_set) ring.hpp:94-102   pyrit_ringmat, pyrit_cu_apply_ringmat
  *   (any XorSchedule)    schedule.hpp:40-58         pyrit_plan_from_schedule
  *   encode               codec.hpp:212-220          pyrit_cu_encode   (device buffers)
  *   encode_crs           codec.hpp:223-231          pyrit_cu_encode_crs
