@@ -120,6 +120,8 @@ def run_patterns(n, dev, reps, out):
     ref = buf.clone()
     rng = random.Random(7)
     pats = [(0, 1, 2, 3), (1, 6, 9, 10)] + [tuple(sorted(rng.sample(range(14), 4))) for _ in range(n)]
+    # one and two lost symbols (the common failures) and three
+    pats += [(3,), (11,), (0, 7), (5, 12), (2, 4, 9)]
     jit0 = L.load().pyrit_jit_compiles()
     for er in pats:
         for o in er:
