@@ -261,9 +261,7 @@ cudaError_t launch_grp(const RtArgs& a, const RtLaunch& l) {
 
 template <int W, int N, u32 P, int E, int R, int V, bool PAR>
 cudaError_t launch_one(const RtArgs& a, const RtLaunch& l) {
-    // a single output (R = 1) never has groups
-    if constexpr (R > 1)
-        if (a.ngrp > 1) return launch_grp<W, N, P, E, R, V, PAR, true>(a, l);
+    if (a.ngrp > 1) return launch_grp<W, N, P, E, R, V, PAR, true>(a, l);
     return launch_grp<W, N, P, E, R, V, PAR, false>(a, l);
 }
 

@@ -824,9 +824,14 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
     // PYRIT_B200_RT_PARTS=2: at most two parts per CTA (two CTAs per SM, more groups)
     static const int parts_knob = env_int("PYRIT_B200_RT_PARTS", 4);
     const std::uint32_t max_parts = V == 4 && parts_knob != 2 ? 4u : 2u;
-    const std::uint32_t per_group = max_parts * ep;
+    // PYRIT_B200_RT_SOLO=1: every output its own group of one 256-thread part
+    // (two CTAs per SM, no lockstep between outputs; a tile's inputs re-read from L2)
+    static const bool solo = env_int("PYRIT_B200_RT_SOLO", 0) != 0;
+    const std::uint32_t per_group = solo ? 1u : max_parts * ep;
     LaunchInfo info;
-    auto r_for = [&](std::uint32_t e) { return e == 1 ? 1u : V == 2 || max_parts == 2 ? 2u : e <= 2 * ep ? 2u : 4u; };
+    auto r_for = [&](std::uint32_t e) {
+        return e == 1 || solo ? 1u : V == 2 || max_parts == 2 ? 2u : e <= 2 * ep ? 2u : 4u;
+    };
     for (std::uint32_t i0 = 0, e = 0; i0 < p.rows; i0 += e) {
         // as many groups as fit the op budget (ring terms + one sentinel per list)
         e = std::min(per_group * kRtMaxGroups, p.rows - i0);
@@ -838,7 +843,7 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
             if (terms + lists + 2 < kRtMaxOps || e == 1) break;
             e = e > per_group ? (e - 1) / per_group * per_group : e - 1;
         }
-        if (e == 1) {
+        if (e == 1 || solo) {
             l.V = 2;
             l.R = 1;
         } else if (V == 2) {
