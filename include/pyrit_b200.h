@@ -318,6 +318,10 @@ int pyrit_jit_info(char* buf, size_t cap);
  * kernels serve the next launches): call it before capturing a CUDA graph */
 int pyrit_jit_wait(void);
 uint64_t pyrit_kernel_launches(void);
+/* Load, on `device`, what a first call would otherwise load on its own path: the
+ * runtime-matrix kernel's modules (~29 ms on the first decode of a new pattern in
+ * a process otherwise).  Optional; for services that want flat first-call latency. */
+int pyrit_warmup(int device);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -63,6 +63,7 @@ EXPORTS = (
     "pyrit_set_file_chunk", "pyrit_cu_encode_crs", "pyrit_encode_crs_host", "pyrit_encode_host_devices",
     "pyrit_decode_host_devices", "pyrit_plan_from_schedule", "pyrit_apply_host", "pyrit_jit_info",
     "pyrit_jit_wait", "pyrit_jit_time", "pyrit_rt_interpret", "pyrit_plan_from_ringmat", "pyrit_cu_apply_ringmat",
+    "pyrit_warmup",
 )
 
 HEADER_SIZE = 29
@@ -120,6 +121,7 @@ def load():
     lib.pyrit_jit_time.argtypes = [P(C.c_double), P(C.c_double)]
     lib.pyrit_rt_interpret.argtypes = [vp, vp, vp, u64, u64, u64, u64, u64, u64]
     lib.pyrit_plan_from_ringmat.argtypes = [P(pyrit_ringmat), vp]
+    lib.pyrit_warmup.argtypes = [i32]
     lib.pyrit_cu_apply_ringmat.argtypes = [P(pyrit_ringmat), vp, vp, u64, u64, u64, vp]
     lib.pyrit_kernel_launches.restype = u64
     lib.pyrit_field_named.argtypes = [C.c_char_p, P(pyrit_field)]

@@ -32,8 +32,10 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 HOST_SOURCES = ["algebra.cpp", "program.cpp", "runtime.cpp", "pipeline.cpp", "plans.cpp", "container.cpp", "hostpool.cpp", "capi.cpp"]
-CUDA_SOURCES = ["kernels.cu", "ring_rt.cu"]
-HEADERS = ["algebra.hpp", "program.hpp", "runtime.hpp", "pipeline.hpp", "plans.hpp", "container.hpp", "kernels.hpp"]
+CUDA_SOURCES = ["kernels.cu", "ring_rt.cu", "ring_rt_w4_n5.cu", "ring_rt_w6_n9.cu", "ring_rt_w8_n17.cu",
+                "ring_rt_w10_n11.cu", "ring_rt_w12_n13.cu"]
+HEADERS = ["algebra.hpp", "program.hpp", "runtime.hpp", "pipeline.hpp", "plans.hpp", "container.hpp", "kernels.hpp",
+           "ring_rt.cuh"]
 
 
 def _run(cmd, **kw):
@@ -69,13 +71,21 @@ def build_library(force=False) -> str:
         from paper_1709_00178_b200 import gen_ring_rt
 
         gen_ring_rt.main([inc])
+    # the CUDA translation units (one per runtime-matrix ring geometry) compile in parallel
+    jobs = []
     for src in CUDA_SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         if force or _stale(o, [s, inc] + hdrs):
-            _run([NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", f"-I{gen_dir}", "-Xcompiler",
-                  "-fPIC,-fvisibility=hidden", "-c", s, "-o", o])
+            jobs.append([NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", f"-I{gen_dir}", "-Xcompiler",
+                         "-fPIC,-fvisibility=hidden", "-c", s, "-o", o])
         objs.append(o)
+    if jobs:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1)) as ex:
+            for f in [ex.submit(_run, j) for j in jobs]:
+                f.result()
     # the background-compile helper (tiered compilation runs NVRTC in its own process)
     helper_src = os.path.join(CSRC, "jit_helper.cpp")
     if force or _stale(HELPER, [helper_src]):

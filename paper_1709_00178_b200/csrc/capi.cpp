@@ -842,4 +842,11 @@ int pyrit_jit_time(double* last_ms, double* total_ms) {
 }
 uint64_t pyrit_kernel_launches(void) { return kernel_launches(); }
 
+int pyrit_warmup(int device) {
+    return guarded([&] {
+        check_cuda(cudaSetDevice(device), "cudaSetDevice");
+        check_cuda(warm_ring_rt(), "runtime-matrix kernel modules");
+    });
+}
+
 } // extern "C"

@@ -73,5 +73,8 @@ constexpr int rt_part_outputs(int n, int w, int v) {
 }
 bool rt_supported(std::uint32_t w, std::uint32_t n, std::uint32_t modulus);
 cudaError_t launch_ring_rt(const RtArgs& a, const RtLaunch& l);
+// load the runtime-matrix kernel's modules (one per ring geometry) on the current
+// device now rather than on the first decode of a new pattern
+cudaError_t warm_ring_rt();
 
 } // namespace pyrit_b200

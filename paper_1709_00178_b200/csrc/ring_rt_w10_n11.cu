@@ -1,0 +1,14 @@
+// The runtime-matrix ring kernel's instances for GF(2^10) in R_{2,11} (see ring_rt.cuh).
+#include "ring_rt.cuh"
+
+namespace pyrit_b200 {
+
+cudaError_t launch_ring_rt_w10_n11(const RtArgs& a, const RtLaunch& l) { return rt_detail::launch_wn<10, 11, 0x7FFu>(a, l); }
+
+// load this geometry's module now (cudaFuncGetAttributes on one instance)
+cudaError_t warm_ring_rt_w10_n11() {
+    cudaFuncAttributes fa;
+    return cudaFuncGetAttributes(&fa, rt_detail::ring_rt_kernel<10, 11, 0x7FFu, 1, 1, 2, false, false>);
+}
+
+} // namespace pyrit_b200
