@@ -405,6 +405,7 @@ def main(argv=None):
             e2e_dev = run_e2e_devices(P, wl, world, rank, args.e2e_steps or min(args.steps, 10))
 
     peak, peak_src = measured_peaks()
+    rt_probe = runtime_matrix_probe(P, L, wl, sets[0], sym, Ls, dev, stream, peak) if rank == 0 else None
     alg_bytes = (n_in + n_out) * sym
     achieved = alg_bytes / (ms * 1e-3) / 1e9
     cpu = None
@@ -447,10 +448,63 @@ def main(argv=None):
         }
         if e2e_dev is not None:
             line["e2e_devices"] = e2e_dev
+        if rt_probe is not None:
+            line["runtime_matrix"] = rt_probe
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def runtime_matrix_probe(P, L, wl, s0, sym, Ls, dev, stream, peak):
+    """Outside the timed region: a decode of an erasure pattern this process has never seen
+    (no prebuilt or compiled kernel) on rank 0's shard -- what a new failure costs: it runs on
+    the runtime-matrix ring kernel (csrc/ring_rt.cu, the matrix in kernel parameters) with no
+    compile.  First launch (plan + launch) and the mean of 5 more, CUDA events on the stream;
+    the repaired symbols must equal the originals."""
+    import torch
+    try:
+        lib = L.load()
+        full = torch.empty((wl.k + wl.m, sym), dtype=torch.uint8, device=dev)
+        if wl.op == "encode":
+            full[: wl.k].copy_(s0[2])
+            full[wl.k:].copy_(s0[3])
+            erased = list(range(wl.k - min(wl.m, 4), wl.k))  # the last data symbols
+        else:
+            full.copy_(s0[2])
+            erased = [2, 5, 6, wl.k]  # not the benchmarked pattern
+        ref = [P.digest(full[e]) for e in erased]
+        plan = P.Plan.decode(wl.code, erased)
+        ins = [full[x].data_ptr() for x in plan.survivors]
+        outs = [full[o].data_ptr() for o in plan.outputs]
+        jit0 = lib.pyrit_jit_compiles()
+        full[erased] = 0xA5
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        torch.cuda.synchronize(dev)
+        ev[0].record(stream)
+        h0 = time.perf_counter()
+        plan.apply(ins, outs, Ls, stream=stream.cuda_stream)
+        host_ms = (time.perf_counter() - h0) * 1e3
+        ev[1].record(stream)
+        kern = P.Plan.last_launch()["kernel"]
+        ev[2].record(stream)
+        for _ in range(5):
+            plan.apply(ins, outs, Ls, stream=stream.cuda_stream)
+        ev[3].record(stream)
+        torch.cuda.synchronize(dev)
+        exact = all(int(P.digest(full[e]).item()) == int(r.item()) for e, r in zip(erased, ref))
+        ms = ev[2].elapsed_time(ev[3]) / 5
+        moved = (wl.k + len(erased)) * sym
+        res = {"pattern": erased, "kernel": kern, "first_launch_ms": round(ev[0].elapsed_time(ev[1]), 4),
+               "first_call_host_ms": round(host_ms, 3),
+               "ms": round(ms, 4), "source_GBps": round(wl.k * sym / ms / 1e6, 1),
+               "frac": round(moved / ms / 1e6 / peak, 4), "exact": exact,
+               "nvrtc_compiles": int(lib.pyrit_jit_compiles() - jit0)}
+        del full
+        torch.cuda.empty_cache()
+        return res
+    except Exception as e:  # a probe, never the bench's failure
+        return {"error": str(e)[:200]}
 
 
 def verify(P, wl, plan, s0, sym, Ls, dev, stream, world):

@@ -181,11 +181,12 @@ def _ptr_array(ptrs):
 class Plan:
     """A compiled ring program: the GPU counterpart of XorSchedule (schedule.hpp:50-59)."""
 
-    def __init__(self, handle: C.c_void_p, survivors=None, outputs=None):
+    def __init__(self, handle: C.c_void_p, survivors=None, outputs=None, shape=None):
         self._h = handle
         self.slots = None
         self.survivors = survivors
         self.outputs = outputs
+        self._shape = shape  # (rows, cols) when known at creation: no compile needed to check calls
 
     @classmethod
     def create(cls, f: FieldSpec, matrix: np.ndarray, transform=TransformKind.Embedding, rep=RingRep.Sparse,
@@ -194,7 +195,7 @@ class Plan:
         h = C.c_void_p()
         L.check(_clib().pyrit_plan_create(C.byref(f.c()), int(transform), m.ctypes.data, m.shape[0], m.shape[1],
                                          int(rep), group, C.byref(h)))
-        return cls(h)
+        return cls(h, shape=m.shape)
 
     @classmethod
     def from_ringmat(cls, f: FieldSpec, reps: np.ndarray, transform=TransformKind.Embedding) -> "Plan":
@@ -204,7 +205,7 @@ class Plan:
         m = L.pyrit_ringmat(f.c(), int(transform), r.shape[0], r.shape[1], r.ctypes.data)
         h = C.c_void_p()
         L.check(_clib().pyrit_plan_from_ringmat(C.byref(m), C.byref(h)))
-        return cls(h)
+        return cls(h, shape=r.shape)
 
     @classmethod
     def from_schedule(cls, sched: XorSchedule, labels: Sequence[int] | None = None) -> "Plan":
@@ -223,7 +224,7 @@ class Plan:
     def encode(cls, code: CodeSpec) -> "Plan":
         h = C.c_void_p()
         L.check(_clib().pyrit_plan_encode(C.byref(code.c()), C.byref(h)))
-        return cls(h)
+        return cls(h, shape=(code.r, code.k))
 
     @classmethod
     def decode(cls, code: CodeSpec, erased: Iterable[int]) -> "Plan":
@@ -233,7 +234,7 @@ class Plan:
         h = C.c_void_p()
         L.check(_clib().pyrit_plan_decode(C.byref(code.c()), er.ctypes.data, er.size, C.byref(h), surv.ctypes.data,
                                          outs.ctypes.data))
-        return cls(h, surv.tolist(), outs[: er.size].tolist())
+        return cls(h, surv.tolist(), outs[: er.size].tolist(), shape=(int(er.size), code.k))
 
     def stats(self) -> dict:
         st = L.pyrit_plan_stats()
@@ -288,8 +289,11 @@ class Plan:
     def _counts(self, ins, outs) -> None:
         """The C ABI reads in[]/out[] by slot count: refuse short pointer lists here."""
         if self.slots is None:
-            st = self.stats()
-            n_in, n_out = st["cols"], st["rows"]
+            if self._shape is not None:  # known at creation (stats() would compile a light plan)
+                n_out, n_in = int(self._shape[0]), int(self._shape[1])
+            else:
+                st = self.stats()
+                n_in, n_out = st["cols"], st["rows"]
         else:
             n_in, n_out = self.slots
         if len(ins) < n_in or len(outs) < n_out:
