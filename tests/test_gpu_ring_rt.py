@@ -282,3 +282,22 @@ def test_apply_ringmat_on_device(cuda, f):
             rt_launched()
             assert lib.pyrit_jit_compiles() == jit0
         np.testing.assert_array_equal(out.cpu().numpy(), oracle_ring(f, m, data))
+
+
+def test_warmup_loads_every_geometry(cuda):
+    """pyrit_warmup loads the runtime-matrix modules of all five ring geometries; decoding after
+    it still repairs (and compiles nothing)."""
+    import torch
+    lib = L.load()
+    L.check(lib.pyrit_warmup(cuda.index or 0))
+    wl = WORKLOADS[2]
+    ss = wl.fld.w * 16 * 64
+    data = seeded_symbols(wl.k, ss, wl.fld.w, wl.seed)
+    full = torch.from_numpy(np.concatenate([data, oracle_ring(wl.fld, P.cauchy_parity_matrix(wl.code), data)])).to(cuda)
+    ref = full.clone()
+    jit0 = lib.pyrit_jit_compiles()
+    full[[2, 11]] = 0
+    P.decode(full, (2, 11), wl.code)
+    torch.cuda.synchronize()
+    assert torch.equal(full, ref)
+    assert lib.pyrit_jit_compiles() == jit0
