@@ -758,7 +758,7 @@ struct RtCall {
     std::vector<const std::uint8_t*> in;
     std::vector<std::uint8_t*> out;
     std::uint64_t strip = 0, off = 0, len = 0, nb = 0, ip = 0, op = 0;
-    std::vector<std::unique_ptr<RtArgs>> args; // ~17 KB of kernel parameters each
+    std::vector<std::unique_ptr<RtArgs>> args; // ~24 KB of kernel parameters each
     std::vector<RtLaunch> launches;
     LaunchInfo info;
 };
