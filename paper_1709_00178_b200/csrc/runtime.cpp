@@ -195,8 +195,13 @@ const Nvrtc& nvrtc() {
         if (const char* e = std::getenv("PYRIT_B200_NVRTC"); e && *e) tries.emplace_back(e);
         tries.emplace_back(PYRIT_NVRTC_PATH);
         tries.emplace_back("libnvrtc.so.12");
+#if defined(__SANITIZE_ADDRESS__) || defined(__SANITIZE_THREAD__)
+        const int deepbind = 0; // the sanitizer runtimes refuse RTLD_DEEPBIND (tests/test_host_sanitizers.py)
+#else
+        const int deepbind = RTLD_DEEPBIND;
+#endif
         for (const std::string& t : tries) {
-            n.handle = dlopen(t.c_str(), RTLD_NOW | RTLD_LOCAL | RTLD_DEEPBIND);
+            n.handle = dlopen(t.c_str(), RTLD_NOW | RTLD_LOCAL | deepbind);
             if (n.handle) {
                 n.path = t;
                 break;

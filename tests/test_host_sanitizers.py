@@ -34,7 +34,7 @@ MODES = {
 }
 
 
-def _build(mode: str) -> str:
+def _build(mode: str, driver: str = "host_sanitize_check") -> str:
     out = os.path.join(BUILD, mode)
     os.makedirs(out, exist_ok=True)
     flags = ["-std=c++20", "-O1", "-g", "-fno-omit-frame-pointer", *MODES[mode]]
@@ -47,8 +47,9 @@ def _build(mode: str) -> str:
 
     with ThreadPoolExecutor(max_workers=min(len(HOST), os.cpu_count() or 1)) as ex:
         objs = list(ex.map(cc, HOST))
-    exe = os.path.join(out, "host_sanitize_check")
-    subprocess.run(["g++", *flags, f"-I{os.path.join(ROOT, 'include')}", os.path.join(ROOT, "tests", "host_sanitize_check.cpp"),
+    exe = os.path.join(out, driver)
+    subprocess.run(["g++", *flags, f"-I{os.path.join(ROOT, 'include')}", f"-I{CUDA}/include",
+                    os.path.join(ROOT, "tests", driver + ".cpp"),
                     *objs, *[os.path.join(BUILD, o) for o in CUDA_OBJS], f"-L{CUDA}/lib64", "-lcudart_static", "-ldl",
                     "-lpthread", "-lrt", "-o", exe], check=True, capture_output=True, text=True)
     return exe
@@ -81,4 +82,20 @@ def test_host_sources_clean_under_sanitizer(cuda_objects, mode):
     assert r.returncode == 0, tail
     assert " 0 failed" in r.stdout, tail
     for word in ("ERROR: AddressSanitizer", "runtime error:", "WARNING: ThreadSanitizer", "ERROR: LeakSanitizer"):
+        assert word not in r.stderr, tail
+
+
+@pytest.mark.gpu
+def test_host_buffer_paths_clean_under_asan_on_gpu(cuda_objects):
+    """tests/host_sanitize_gpu.cpp: the host-buffer C ABI (pipeline, shards over devices, stripe
+    batches, runtime-matrix decode, file codec, concurrent callers) with the host sources under
+    ASan+UBSan, on the device, every result checked against the host interpreter."""
+    exe = _build("asan", "host_sanitize_gpu")
+    env = dict(os.environ, ASAN_OPTIONS="protect_shadow_gap=0:detect_leaks=0:halt_on_error=1",
+               UBSAN_OPTIONS="print_stacktrace=1:halt_on_error=1", PYRIT_B200_JIT_CACHE="0")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900, env=env)
+    tail = (r.stdout + r.stderr)[-4000:]
+    assert r.returncode == 0, tail
+    assert " 0 failed" in r.stdout, tail
+    for word in ("ERROR: AddressSanitizer", "runtime error:"):
         assert word not in r.stderr, tail
