@@ -149,6 +149,12 @@ int pyrit_plan_interpret(const pyrit_plan* plan, const uint8_t* const* in, uint8
  * aligned, strip/off/len multiples of 16, a ring geometry with an AOT kernel. */
 int pyrit_rt_interpret(const pyrit_plan* plan, const uint8_t* const* in, uint8_t* const* out, uint64_t strip_bytes,
                        uint64_t off, uint64_t len, uint64_t stripes, uint64_t in_pitch, uint64_t out_pitch);
+/* verification aid: how the runtime-matrix planner would run this plan, no device
+ * involved: info[0] launches, info[1] ring terms of the matrix (set bits of the
+ * representatives, schedule.hpp:132-161), info[2] ops the launches run for them (a
+ * paired-shift op covers two terms with 3-input XORs), info[3] bytes of dispatch-case
+ * code the largest launch names (kept within the instruction cache) */
+int pyrit_rt_plan_info(const pyrit_plan* plan, uint32_t info[4]);
 void pyrit_plan_destroy(pyrit_plan* plan);
 
 /* ---- a raw ring-representative matrix (SURVEY 8(b) pyrit_cu_ringmat) --- */

@@ -286,6 +286,13 @@ class Plan:
         L.check(_clib().pyrit_rt_interpret(self._h, _ptr_array(in_ptrs), _ptr_array(out_ptrs), strip, off, length,
                                            stripes, in_pitch, out_pitch))
 
+    def rt_info(self) -> dict:
+        """How the runtime-matrix planner runs this plan (host only): launches, ring terms,
+        ops (a paired-shift op covers two terms) and bytes of dispatch-case code named."""
+        info = (C.c_uint32 * 4)()
+        L.check(_clib().pyrit_rt_plan_info(self._h, info))
+        return {"launches": info[0], "terms": info[1], "ops": info[2], "case_bytes": info[3]}
+
     def _counts(self, ins, outs) -> None:
         """The C ABI reads in[]/out[] by slot count: refuse short pointer lists here."""
         if self.slots is None:

@@ -32,6 +32,17 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 HOST_SOURCES = ["algebra.cpp", "program.cpp", "runtime.cpp", "pipeline.cpp", "plans.cpp", "container.cpp", "hostpool.cpp", "capi.cpp"]
+# paired-shift cases of the runtime-matrix kernel: shifts up to this far apart share one
+# case (kernels.hpp PYRIT_RT_PAIR_D); a build-time constant of the library
+# (default: the #define in csrc/kernels.hpp; PYRIT_B200_BUILD_RT_PAIR_D overrides it for A/B builds)
+def _default_pair_d() -> int:
+    import re
+
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "csrc", "kernels.hpp")) as f:
+        return int(re.search(r"#define PYRIT_RT_PAIR_D (\d+)", f.read()).group(1))
+
+
+RT_PAIR_D = int(os.environ.get("PYRIT_B200_BUILD_RT_PAIR_D", "") or _default_pair_d())
 CUDA_SOURCES = ["kernels.cu", "ring_rt.cu", "ring_rt_w4_n5.cu", "ring_rt_w6_n9.cu", "ring_rt_w8_n17.cu",
                 "ring_rt_w10_n11.cu", "ring_rt_w12_n13.cu"]
 HEADERS = ["algebra.hpp", "program.hpp", "runtime.hpp", "pipeline.hpp", "plans.hpp", "container.hpp", "kernels.hpp",
@@ -53,31 +64,39 @@ def _stale(target, deps):
 def build_library(force=False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "pyrit_b200.h")]
+    stamp = os.path.join(BUILD, "rt_pair_d.stamp")  # objects depend on the -D value they were built with
+    if not os.path.exists(stamp) or open(stamp).read() != str(RT_PAIR_D):
+        with open(stamp, "w") as f:
+            f.write(str(RT_PAIR_D))
+    hdrs.append(stamp)
     objs = []
     for src in HOST_SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         if force or _stale(o, [s] + hdrs):
             _run(["g++", "-std=c++20", "-O2", "-g", "-fPIC", "-fvisibility=hidden", "-Wall", "-Wextra",
-                  f"-I{CUDA}/include", f'-DPYRIT_NVRTC_PATH="{CUDA}/lib64/libnvrtc.so.12"', "-c", s, "-o", o])
+                  f"-I{CUDA}/include", f"-DPYRIT_RT_PAIR_D={RT_PAIR_D}", f'-DPYRIT_NVRTC_PATH="{CUDA}/lib64/libnvrtc.so.12"', "-c", s, "-o", o])
         objs.append(o)
     # dispatch tables of the runtime-matrix ring kernel (generated, build/generated)
     gen_dir = os.path.join(BUILD, "generated")
     os.makedirs(gen_dir, exist_ok=True)
     inc = os.path.join(gen_dir, "ring_rt_ops.inc")
     gen = os.path.join(PKG, "gen_ring_rt.py")
-    if force or _stale(inc, [gen]):
-        sys.path.insert(0, ROOT)
-        from paper_1709_00178_b200 import gen_ring_rt
+    sys.path.insert(0, ROOT)
+    from paper_1709_00178_b200 import gen_ring_rt
 
-        gen_ring_rt.main([inc])
+    text = gen_ring_rt.generate(RT_PAIR_D)
+    if force or not os.path.exists(inc) or open(inc).read() != text:
+        with open(inc, "w") as f:
+            f.write(text)
     # the CUDA translation units (one per runtime-matrix ring geometry) compile in parallel
     jobs = []
     for src in CUDA_SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         if force or _stale(o, [s, inc] + hdrs):
-            jobs.append([NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", f"-I{gen_dir}", "-Xcompiler",
+            jobs.append([NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", f"-I{gen_dir}", f"-DPYRIT_RT_PAIR_D={RT_PAIR_D}",
+                         "-Xcompiler",
                          "-fPIC,-fvisibility=hidden", "-c", s, "-o", o])
         objs.append(o)
     if jobs:

@@ -536,6 +536,14 @@ int pyrit_rt_interpret(const pyrit_plan* plan, const uint8_t* const* in, uint8_t
     });
 }
 
+int pyrit_rt_plan_info(const pyrit_plan* plan, uint32_t info[4]) {
+    return guarded([&] {
+        if (!plan || !info) raise(Errc::InvalidArgument, "null argument");
+        if (plan->sched) raise(Errc::InvalidArgument, "replayed schedules do not run on the runtime-matrix kernel");
+        ring_rt_plan_info(plan->prog, info);
+    });
+}
+
 int pyrit_cu_apply_batch(const pyrit_plan* plan, const uint8_t* const* in, uint8_t* const* out,
                          uint64_t strip_bytes, uint64_t off, uint64_t len, uint64_t stripes, uint64_t in_pitch,
                          uint64_t out_pitch, void* stream) {

@@ -50,9 +50,10 @@ struct alignas(64) RtArgs {
     std::uint32_t ngrp;                  // output groups (units per tile)
     std::uint32_t epart[kRtMaxGroups][kRtParts]; // outputs of each part of each group
     std::uint32_t fm[256]; // Parity: fm[q*w + i] = ~0 when strip i feeds the parity strip w+q (i = q mod s)
-    // op list of input j for part p of group g: ops[opoff[g][p][j] ..], each c = i*n + sh
-    // (output i of the part accumulates input j rotated by sh ring positions, a
-    // set bit of the representative of entry (i, j)), terminated by E*n
+    // op list of input j for part p of group g: ops[opoff[g][p][j] ..], each
+    // c = (i*(D+1) + ds)*n + sh with D = rt_pair_d(n, V): output i of the part
+    // accumulates input j rotated by sh ring positions (ds = 0) or by sh and sh+ds
+    // (a pair) -- set bits of the representative of entry (i, j) -- terminated by E*(D+1)*n
     std::uint16_t opoff[kRtMaxGroups][kRtParts][kRtMaxK + 1];
     std::uint8_t ops[kRtMaxOps];
 };
@@ -70,6 +71,18 @@ struct RtLaunch {
 constexpr int rt_clamp_e(int e) { return e < 1 ? 1 : (e > 8 ? 8 : e); }
 constexpr int rt_part_outputs(int n, int w, int v) {
     return v == 4 ? rt_clamp_e((104 - 4 * w) / (4 * n)) : rt_clamp_e(36 / n);
+}
+// Paired-shift cases: two shifts (sh, sh+d) of one representative are one op whose
+// ring rows reached by both take a 3-input LOP3 (gen_ring_rt.py).  The V = 4 instances
+// carry a case for every pair distance d <= min(PYRIT_RT_PAIR_D, (n-1)/2) -- a
+// build-time constant (0: no pair cases); which of them a launch uses is the
+// planner's choice (runtime.cpp rt_select_pairs: the cases that pay most within the
+// instruction-cache budget).  V = 2 instances (single output, HBM-bound) have none.
+#ifndef PYRIT_RT_PAIR_D
+#define PYRIT_RT_PAIR_D 3
+#endif
+constexpr std::uint32_t rt_pair_d(std::uint32_t n, std::uint32_t v) {
+    return v != 4 ? 0u : (n - 1) / 2 < PYRIT_RT_PAIR_D ? (n - 1) / 2 : PYRIT_RT_PAIR_D;
 }
 bool rt_supported(std::uint32_t w, std::uint32_t n, std::uint32_t modulus);
 cudaError_t launch_ring_rt(const RtArgs& a, const RtLaunch& l);

@@ -30,6 +30,8 @@
 //     fragment's op list -- each op (i, sh) a warp-uniform jump (brx.idx)
 //     into a compile-time XOR block "acc_i ^= x rotated by sh", so every
 //     accumulator index is a fixed register although the matrix is runtime;
+//     two shifts sh, sh+d (d <= PYRIT_RT_PAIR_D) of one representative may be
+//     one op (i, sh, d): rows both reach take one 3-input LOP3;
 //   * after the last fragment the accumulators are folded (Embedding:
 //     x^t mod p, compile-time per field) and stored once with st.global.cs.
 // Every input byte is read from HBM once and every output byte written once.
@@ -91,8 +93,8 @@ __device__ __forceinline__ void st_cs(std::uint8_t* p, const u32 (&v)[V]) {
     else asm volatile("st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]) : "memory");
 }
 
-// One pipeline op: c = i*N + sh XORs the input, rotated by sh ring positions,
-// into the accumulators of output i (Embedding: W nonzero input strips, all N
+// One pipeline op: c = (i*(D+1) + ds)*N + sh XORs the input, rotated by sh ring
+// positions (ds = 0) or by sh and sh+ds (a pair), into the accumulators of output i (Embedding: W nonzero input strips, all N
 // rows kept for the fold; Parity: N input strips, rows >= W dropped).  The
 // specialisations (build/generated/ring_rt_ops.inc, gen_ring_rt.py) are one
 // inline-PTX brx.idx jump table each: warp-uniform, and every accumulator
@@ -187,6 +189,9 @@ __global__ void __launch_bounds__(R * (kRtTile / (4 * V)), 512 / (R * (kRtTile /
         // inputs 0..k-1 follow each other, each ended by its sentinel
         u32 q = list0 + 1, d;
         asm volatile("ld.shared.u8 %0, [%1];" : "=r"(d) : "r"(list0));
+        // not unrolled: ptxas would duplicate the whole case table per copy of the
+        // body (the instruction cache holds one)
+#pragma unroll 1
         for (u32 j = 0; j < k; ++j) {
             if (threadIdx.x == PROD) produce();
             mbar_wait(FULL(sl), ph);

@@ -765,21 +765,20 @@ struct RtCall {
     std::uint64_t strip = 0, off = 0, len = 0, nb = 0, ip = 0, op = 0;
     std::vector<std::unique_ptr<RtArgs>> args; // ~24 KB of kernel parameters each
     std::vector<RtLaunch> launches;
+    // per launch: the program rows of every (group, part) bin and the CTAs an SM holds --
+    // what bind_ring_rt needs to point a planned launch at other buffers
+    std::vector<std::vector<std::vector<std::uint32_t>>> bins;
+    std::vector<std::uint32_t> ctas_per_sm;
+    std::vector<std::uint32_t> case_bytes, op_count; // per launch: bytes of case code named, ops (without sentinels)
     LaunchInfo info;
 };
 
-// device = false: the same launch plan without tensor maps or a device query
-// (interpret_ring_rt, the host check of the planner)
-void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
-                   std::uint64_t strip, std::uint64_t off, std::uint64_t len, std::uint64_t nb, std::uint64_t in_pitch,
-                   std::uint64_t out_pitch, bool device = true) {
-    call.args.clear();
-    call.launches.clear();
-    RtArgs tmpl;
-    RtArgs& a = tmpl;
-    const std::uint32_t w = p.field.w, n = p.field.n, k = p.cols;
-    const std::uint32_t tile = kRtTile, elem = 8, slot = w * tile;
-    const std::uint64_t tpb = (len + tile - 1) / tile;
+// The buffer-dependent kernel parameters: tensor maps of the inputs and the window.
+void bind_rt_geometry(RtArgs& a, const Program& p, const std::uint8_t* const* in, std::uint64_t strip, std::uint64_t off,
+                      std::uint64_t len, std::uint64_t nb, std::uint64_t in_pitch, std::uint64_t out_pitch, bool device) {
+    const std::uint32_t w = p.field.w, k = p.cols;
+    const std::uint32_t elem = 8;
+    const std::uint64_t tpb = (len + kRtTile - 1) / kRtTile;
     static const int promo_knob = env_int("PYRIT_B200_TMA_PROMO", 3);
     const CUtensorMapL2promotion promo = static_cast<CUtensorMapL2promotion>(std::min(3, std::max(0, promo_knob)));
     for (std::uint32_t j = 0; device && j < k; ++j) {
@@ -802,6 +801,139 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
     a.k = k;
     a.tpb = static_cast<std::uint32_t>(tpb);
     a.ntiles = static_cast<std::uint32_t>(tpb * nb);
+}
+
+unsigned rt_blocks(std::uint64_t units, std::uint32_t ctas_per_sm, bool device) {
+    return !device ? 1u
+                   : static_cast<unsigned>(std::max<std::uint64_t>(
+                         1, std::min<std::uint64_t>(units, std::uint64_t(ctas_per_sm) * sm_count())));
+}
+
+// A planned call (op lists, parts, groups: functions of the matrix only) pointed at
+// other buffers or another window: new tensor maps, output bases and grid sizes.
+void bind_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
+                  std::uint64_t strip, std::uint64_t off, std::uint64_t len, std::uint64_t nb, std::uint64_t in_pitch,
+                  std::uint64_t out_pitch) {
+    for (std::size_t c = 0; c < call.launches.size(); ++c) {
+        RtArgs& a = *call.args[c];
+        RtLaunch& l = call.launches[c];
+        if (c == 0)
+            bind_rt_geometry(a, p, in, strip, off, len, nb, in_pitch, out_pitch, true);
+        else {
+            const RtArgs& a0 = *call.args[0];
+            std::memcpy(a.tm, a0.tm, sizeof a.tm);
+            a.S = a0.S, a.off = a0.off, a.len = a0.len, a.nb = a0.nb, a.obp = a0.obp, a.k = a0.k, a.tpb = a0.tpb,
+            a.ntiles = a0.ntiles;
+        }
+        const auto& bins = call.bins[c];
+        for (std::size_t q = 0; q < bins.size(); ++q)
+            for (std::size_t i = 0; i < bins[q].size(); ++i)
+                a.out[q / l.R][(q % l.R) * kRtPartE + i] = out[bins[q][i]];
+        l.blocks = rt_blocks(std::uint64_t(a.ntiles) * a.ngrp, call.ctas_per_sm[c], true);
+        call.info.blocks = l.blocks;
+    }
+}
+
+// One matrix entry of a part: the representative (set bits = shifts) of local output
+// i, and the ops chosen for it: singles (sh, 0) and pairs (sh, d) standing for the
+// shifts sh and (sh + d) mod n.
+struct RtEntry {
+    std::uint32_t i, mask;
+    std::vector<std::pair<std::uint32_t, std::uint32_t>> ops;
+};
+
+// Choose the pair cases of a launch.  A case (i, sh, d) serves every entry of local
+// output i whose representative has both shifts still unpaired; taking it removes,
+// per use, the rows both shifts reach (one 3-input LOP3 instead of two XORs) and one
+// dispatch.  Greedy: the case with the largest total saving first, applied wherever it
+// fits, until the distinct cases named (pairs chosen + singles still needed) would
+// outgrow `budget` bytes of case code.  Returns the bytes of cases named.
+template <class Rows>
+std::uint32_t rt_select_pairs(std::vector<RtEntry>& entries, std::uint32_t n, std::uint32_t D, std::uint32_t E,
+                              std::uint32_t V, std::uint32_t budget, Rows case_rows) {
+    constexpr std::uint32_t kDispatch = 6; // instructions of a case besides its LOP3s
+    auto bytes_of = [&](std::uint32_t sh, std::uint32_t ds) { return 16u * (case_rows(sh, ds) * V + kDispatch); };
+    std::vector<std::uint32_t> rem(entries.size());
+    for (std::size_t x = 0; x < entries.size(); ++x) rem[x] = entries[x].mask, entries[x].ops.clear();
+    auto singles_bytes = [&]() {
+        std::uint32_t b = 0;
+        std::vector<std::uint32_t> seen(E, 0);
+        for (std::size_t x = 0; x < entries.size(); ++x) {
+            for (std::uint32_t m = rem[x] & ~seen[entries[x].i]; m; m &= m - 1)
+                b += bytes_of(static_cast<std::uint32_t>(std::countr_zero(m)), 0);
+            seen[entries[x].i] |= rem[x];
+        }
+        return b;
+    };
+    std::uint32_t pair_bytes = 0;
+    if (D > 0) {
+        // per-use saving of a pair at distance d (independent of sh for the Embedding; the
+        // Parity transform truncates rows, so take sh = 0 as the estimate)
+        std::vector<std::uint32_t> saving(D + 1, 0);
+        for (std::uint32_t d = 1; d <= D; ++d) {
+            const std::uint32_t two = case_rows(0, 0) + case_rows(d % n, 0), one = case_rows(0, d);
+            saving[d] = (two > one ? two - one : 0) * V + kDispatch;
+        }
+        std::vector<std::uint32_t> cnt(std::size_t(E) * (D + 1) * n);
+        std::vector<bool> taken(cnt.size(), false);
+        for (;;) {
+            std::fill(cnt.begin(), cnt.end(), 0);
+            for (std::size_t x = 0; x < entries.size(); ++x)
+                for (std::uint32_t m = rem[x]; m; m &= m - 1) {
+                    const std::uint32_t sh = static_cast<std::uint32_t>(std::countr_zero(m));
+                    for (std::uint32_t d = 1; d <= D; ++d)
+                        if ((rem[x] >> ((sh + d) % n)) & 1u) ++cnt[(entries[x].i * (D + 1) + d) * n + sh];
+                }
+            std::size_t best = cnt.size();
+            std::uint64_t best_score = 0;
+            static const std::uint32_t min_uses = static_cast<std::uint32_t>(std::max(1, env_int("PYRIT_B200_RT_PAIR_MINUSE", 1)));
+            for (std::size_t c = 0; c < cnt.size(); ++c) {
+                if (cnt[c] < min_uses && !taken[c]) continue; // a case hardly used only adds instruction-cache misses
+                const std::uint64_t score = std::uint64_t(cnt[c]) * saving[(c / n) % (D + 1)];
+                if (score > best_score) best = c, best_score = score;
+            }
+            if (best == cnt.size()) break;
+            const std::uint32_t sh = static_cast<std::uint32_t>(best % n), d = static_cast<std::uint32_t>((best / n) % (D + 1)),
+                                i = static_cast<std::uint32_t>(best / n / (D + 1));
+            const std::uint32_t both = (1u << sh) | (1u << ((sh + d) % n));
+            const std::uint32_t add = taken[best] ? 0u : bytes_of(sh, d);
+            // apply, then check the budget with the singles that remain
+            std::vector<std::size_t> hit;
+            for (std::size_t x = 0; x < entries.size(); ++x)
+                if (entries[x].i == i && (rem[x] & both) == both) rem[x] &= ~both, hit.push_back(x);
+            if (pair_bytes + add + singles_bytes() > budget) {
+                for (std::size_t x : hit) rem[x] |= both;
+                break;
+            }
+            for (std::size_t x : hit) entries[x].ops.emplace_back(sh, d);
+            pair_bytes += add;
+            taken[best] = true;
+        }
+    }
+    const std::uint32_t total = pair_bytes + singles_bytes();
+    for (std::size_t x = 0; x < entries.size(); ++x)
+        for (std::uint32_t m = rem[x]; m; m &= m - 1)
+            entries[x].ops.emplace_back(static_cast<std::uint32_t>(std::countr_zero(m)), 0u);
+    return total;
+}
+
+// device = false: the same launch plan without tensor maps or a device query
+// (interpret_ring_rt, the host check of the planner)
+void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
+                   std::uint64_t strip, std::uint64_t off, std::uint64_t len, std::uint64_t nb, std::uint64_t in_pitch,
+                   std::uint64_t out_pitch, bool device = true) {
+    call.args.clear();
+    call.launches.clear();
+    call.bins.clear();
+    call.ctas_per_sm.clear();
+    call.case_bytes.clear();
+    call.op_count.clear();
+    RtArgs tmpl;
+    RtArgs& a = tmpl;
+    const std::uint32_t w = p.field.w, n = p.field.n, k = p.cols;
+    const std::uint32_t tile = kRtTile, slot = w * tile;
+    const std::uint64_t tpb = (len + tile - 1) / tile;
+    bind_rt_geometry(a, p, in, strip, off, len, nb, in_pitch, out_pitch, device);
     std::memset(a.fm, 0, sizeof a.fm);
     const bool par = p.kind == TransformKind::Parity;
     if (par) // strip w+q of the extended input = XOR of strips i = q (mod s) (phi_P, transform.hpp:50-60)
@@ -895,8 +1027,35 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
         a.prod = light * rt_part_threads(l.V);
         const std::uint32_t cta_threads = l.R * rt_part_threads(l.V);
         const std::uint32_t ctas_per_sm = 512 / cta_threads;
-        // op lists, one per (group, part, input), each ended by the sentinel E*n
+        // op lists, one per (group, part, input), each ended by the sentinel E*(D+1)*n;
+        // with paired-shift cases (D > 0) two set bits of a representative at most D
+        // ring positions apart become one op
+        // Which pair cases THIS matrix uses: the jumps are data dependent, so the hot
+        // code is every case the op lists name, and it has to stay well inside the
+        // instruction cache (measured on config 5: ~36 KB of cases 0.68 of peak, 23-32 KB
+        // 0.75-0.79; profiles/r02/ring_rt_pairs/).  rt_select_pairs spends the budget on
+        // the cases that remove most instructions.  Knobs for A/B runs only:
+        // PYRIT_B200_RT_PAIRS=0 (singles only), _RT_CODE_KB, _RT_PAIR_DMAX, _RT_PAIR_MINUSE.
+        static const int pairs_knob = env_int("PYRIT_B200_RT_PAIRS", 1);
+        static const int code_kb = env_int("PYRIT_B200_RT_CODE_KB", 26);
+        const std::uint32_t D = rt_pair_d(n, l.V);
+        const std::uint32_t xr = par ? n : w, ar = par ? w : n;
+        auto case_rows = [&](std::uint32_t sh, std::uint32_t ds) { // gen_ring_rt.py emit(): one LOP3 per reached row and word
+            std::uint32_t rows = 0;
+            for (std::uint32_t r = 0; r < ar; ++r)
+                rows += (r + n - sh) % n < xr || (ds && (r + 2 * n - sh - ds) % n < xr);
+            return rows;
+        };
+        std::vector<RtEntry> entries;
+        for (std::uint32_t q = 0; q < bins; ++q)
+            for (std::uint32_t j = 0; j < k; ++j)
+                for (std::uint32_t i = 0; i < rows_of[q].size(); ++i)
+                    entries.push_back({i, p.reps[std::size_t(rows_of[q][i]) * k + j], {}});
+        static const int dmax_knob = env_int("PYRIT_B200_RT_PAIR_DMAX", 64);
+        const std::uint32_t code = rt_select_pairs(entries, n, pairs_knob ? std::min<std::uint32_t>(D, static_cast<std::uint32_t>(std::max(0, dmax_knob))) : 0, l.E, l.V,
+                                                   static_cast<std::uint32_t>(code_kb) * 1024u, case_rows);
         std::uint32_t nops = 0;
+        std::size_t ent = 0;
         for (std::uint32_t g = 0; g < G; ++g)
             for (std::uint32_t part = 0; part < l.R; ++part) {
                 const std::vector<std::uint32_t>& pr = rows_of[g * l.R + part];
@@ -904,17 +1063,19 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
                 for (std::uint32_t j = 0; j < k; ++j) {
                     a.opoff[g][part][j] = static_cast<std::uint16_t>(nops);
                     for (std::uint32_t i = 0; i < ne; ++i)
-                        for (std::uint32_t m = p.reps[std::size_t(pr[i]) * k + j]; m; m &= m - 1) {
+                        for (const auto& [sh, ds] : entries[ent++].ops) {
                             if (nops + 2 >= kRtMaxOps)
                                 raise(Errc::InvalidArgument, "ring_rt: too many ring terms per launch");
-                            a.ops[nops++] =
-                                static_cast<std::uint8_t>(i * n + static_cast<std::uint32_t>(std::countr_zero(m)));
+                            a.ops[nops++] = static_cast<std::uint8_t>((i * (D + 1) + ds) * n + sh);
                         }
-                    a.ops[nops++] = static_cast<std::uint8_t>(l.E * n);
+                    a.ops[nops++] = static_cast<std::uint8_t>(l.E * (D + 1) * n);
                 }
                 a.opoff[g][part][k] = static_cast<std::uint16_t>(nops);
                 for (std::uint32_t i = 0; i < ne; ++i) a.out[g][part * kRtPartE + i] = out[pr[i]];
             }
+        static const bool trace = env_int("PYRIT_B200_RT_TRACE", 0) != 0;
+        if (trace)
+            std::fprintf(stderr, "ring_rt w%u n%u e%u k%u: %u ops, %u B of cases\n", w, n, e, k, nops - G * l.R * k, code);
         a.ops[nops] = 0; // the byte the last list's look-ahead reads
         a.nops = nops + 1;
         // shared memory: mbarriers, op lists, then as many fragment slots as fit (<= 32)
@@ -927,10 +1088,13 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
         a.nslot = ns;
         a.slot0 = bar;
         l.smem = bar + ns * slot;
-        l.blocks = !device ? 1u : static_cast<unsigned>(std::max<std::uint64_t>(
-            1, std::min<std::uint64_t>(tpb * nb * G, std::uint64_t(ctas_per_sm) * sm_count())));
+        l.blocks = rt_blocks(tpb * nb * G, ctas_per_sm, device);
         call.args.push_back(std::make_unique<RtArgs>(a));
         call.launches.push_back(l);
+        call.bins.push_back(rows_of);
+        call.ctas_per_sm.push_back(ctas_per_sm);
+        call.case_bytes.push_back(code);
+        call.op_count.push_back(nops - G * l.R * k);
         info.blocks = l.blocks;
         info.threads = l.R * rt_part_threads(l.V);
     }
@@ -970,7 +1134,7 @@ void interpret_ring_rt(const Program& p, const std::uint8_t* const* in, std::uin
     for (std::size_t c = 0; c < call.launches.size(); ++c) {
         const RtArgs& a = *call.args[c];
         const RtLaunch& l = call.launches[c];
-        const std::uint32_t E = l.E, G = a.ngrp;
+        const std::uint32_t E = l.E, G = a.ngrp, D = rt_pair_d(n, l.V);
         std::vector<std::uint64_t> acc(std::size_t(E) * ar), x(n);
         for (std::uint64_t u = 0; u < std::uint64_t(a.ntiles) * G; ++u) {
             const std::uint64_t t = u / G, g = u % G, b = t / a.tpb, tt = t - b * a.tpb;
@@ -992,13 +1156,14 @@ void interpret_ring_rt(const Program& p, const std::uint8_t* const* in, std::uin
                             }
                         for (;;) {
                             const std::uint32_t op = a.ops[q++];
-                            if (op == E * n) break;
-                            const std::uint32_t i = op / n, sh = op % n;
-                            for (std::uint32_t s2 = 0; s2 < xr; ++s2) {
-                                const std::uint32_t r = (s2 + sh) % n;
-                                if (par && r >= w) continue;
-                                acc[std::size_t(i) * ar + r] ^= x[s2];
-                            }
+                            if (op == E * (D + 1) * n) break;
+                            const std::uint32_t ids = op / n, sh = op % n, i = ids / (D + 1), ds = ids % (D + 1);
+                            for (std::uint32_t half = 0; half < (ds ? 2u : 1u); ++half)
+                                for (std::uint32_t s2 = 0; s2 < xr; ++s2) {
+                                    const std::uint32_t r = (s2 + sh + half * ds) % n;
+                                    if (par && r >= w) continue;
+                                    acc[std::size_t(i) * ar + r] ^= x[s2];
+                                }
                         }
                     }
                     for (std::uint32_t i = 0; i < ep; ++i) {
@@ -1016,6 +1181,25 @@ void interpret_ring_rt(const Program& p, const std::uint8_t* const* in, std::uin
     }
 }
 
+// launches, ring terms of the matrix, ops the launches run for them (a pair op covers
+// two terms), and the largest case-code footprint of a launch
+void ring_rt_plan_info(const Program& p, std::uint32_t info[4]) {
+    if (p.crs || p.sched || p.reps.empty() || p.rows == 0 || p.cols > kRtMaxK ||
+        !rt_supported(p.field.w, p.field.n, p.field.modulus))
+        raise(Errc::InvalidArgument, "not a runtime-matrix kernel program");
+    std::vector<const std::uint8_t*> in(p.cols, nullptr);
+    std::vector<std::uint8_t*> out(p.rows, nullptr);
+    RtCall call;
+    build_ring_rt(call, p, in.data(), out.data(), kRtTile, 0, kRtTile, 1, 0, 0, false);
+    info[0] = static_cast<std::uint32_t>(call.launches.size());
+    info[1] = info[2] = info[3] = 0;
+    for (std::uint32_t m : p.reps) info[1] += static_cast<std::uint32_t>(std::popcount(m));
+    for (std::size_t c = 0; c < call.launches.size(); ++c) {
+        info[2] += call.op_count[c];
+        info[3] = std::max(info[3], call.case_bytes[c]);
+    }
+}
+
 LaunchInfo launch_ring_rt_program(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out,
                                   std::uint64_t strip, std::uint64_t off, std::uint64_t len, std::uint64_t nb,
                                   std::uint64_t in_pitch, std::uint64_t out_pitch, cudaStream_t stream) {
@@ -1028,8 +1212,43 @@ LaunchInfo launch_ring_rt_program(const Program& p, const std::uint8_t* const* i
     for (std::uint32_t j = 0; same && j < p.cols; ++j) same = last.in[j] == in[j];
     for (std::uint32_t i = 0; same && i < p.rows; ++i) same = last.out[i] == out[i];
     if (!same) {
+        // the planned launches of the last programs of this thread (a function of the
+        // matrix only): a known program on new buffers is re-bound, not re-planned
+        struct Planned {
+            std::vector<RtArgs> args;
+            std::vector<RtLaunch> launches;
+            std::vector<std::vector<std::vector<std::uint32_t>>> bins;
+            std::vector<std::uint32_t> ctas_per_sm;
+            LaunchInfo info;
+        };
+        thread_local std::unordered_map<std::string, std::shared_ptr<Planned>> planned;
+        const bool keep = last.key == p.key && !p.key.empty(); // same program, other buffers: args are in place
         last.key.clear(); // invalid until fully built
-        build_ring_rt(last, p, in, out, strip, off, len, nb, in_pitch, out_pitch);
+        auto hit = keep || p.key.empty() ? planned.end() : planned.find(p.key);
+        if (keep)
+            bind_ring_rt(last, p, in, out, strip, off, len, nb, in_pitch, out_pitch);
+        else if (hit != planned.end()) {
+            const Planned& pl = *hit->second;
+            last.args.clear();
+            for (const RtArgs& a : pl.args) last.args.push_back(std::make_unique<RtArgs>(a));
+            last.launches = pl.launches;
+            last.bins = pl.bins;
+            last.ctas_per_sm = pl.ctas_per_sm;
+            last.info = pl.info;
+            bind_ring_rt(last, p, in, out, strip, off, len, nb, in_pitch, out_pitch);
+        } else {
+            build_ring_rt(last, p, in, out, strip, off, len, nb, in_pitch, out_pitch);
+            if (!p.key.empty()) {
+                if (planned.size() >= 32) planned.clear();
+                auto pl = std::make_shared<Planned>();
+                for (const auto& a : last.args) pl->args.push_back(*a);
+                pl->launches = last.launches;
+                pl->bins = last.bins;
+                pl->ctas_per_sm = last.ctas_per_sm;
+                pl->info = last.info;
+                planned.emplace(p.key, std::move(pl));
+            }
+        }
         last.key = p.key;
         last.dev = dev;
         last.strip = strip;

@@ -79,6 +79,7 @@ int kernel_mode();
 int rt_policy();
 // can the runtime-matrix ring kernel run this launch (prebuilt geometry,
 // 16-byte alignment, k <= 64, outputs aliasing inputs only column for column)
+void ring_rt_plan_info(const Program& p, std::uint32_t info[4]);
 void interpret_ring_rt(const Program& p, const std::uint8_t* const* in, std::uint8_t* const* out, std::uint64_t strip,
                        std::uint64_t off, std::uint64_t len, std::uint64_t nb, std::uint64_t in_pitch,
                        std::uint64_t out_pitch);

@@ -1,14 +1,16 @@
 """Generate the dispatch blocks of the runtime-matrix ring kernel (csrc/ring_rt.cu).
 
-    python -m paper_1709_00178_b200.gen_ring_rt <out.inc>
+    python -m paper_1709_00178_b200.gen_ring_rt <out.inc> [pair distance]
 
 For every kernel instance (w, n, E outputs, V words per thread, transform) this
-emits RtOps<...>::apply(c, acc, x): one inline-PTX block whose `brx.idx` jumps
-through a table of E*n targets; target c = i*n + sh XORs the input strips,
-rotated by sh ring positions, into the accumulators of output i
-(schedule.hpp:132-161: ring row t of output i accumulates input strip
-(t - sh) mod n).  Every register index inside a case is fixed, so the runtime
-matrix never indexes registers dynamically, and the jump is warp-uniform.
+emits RtOps<...>::run(q, d, acc, x): one inline-PTX block whose `brx.idx` jumps
+through a table of E*(D+1)*n targets; target c = (i*(D+1) + ds)*n + sh XORs the
+input strips, rotated by sh ring positions (ds = 0) or by sh and sh+ds (a
+paired-shift case, rows reached by both with one 3-input LOP3), into the
+accumulators of output i (schedule.hpp:132-161: ring row t of output i
+accumulates input strip (t - sh) mod n).  Every register index inside a case is
+fixed, so the runtime matrix never indexes registers dynamically, and the jump
+is warp-uniform.  D = pair_d(n, v, PYRIT_RT_PAIR_D) (csrc/kernels.hpp rt_pair_d).
 The instance list (FIELDS) must match PYRIT_RT_FIELDS in csrc/ring_rt.cu.
 """
 from __future__ import annotations
@@ -31,11 +33,19 @@ def instances():
                     yield w, n, e, v, par
 
 
-def emit(w: int, n: int, e: int, v: int, par: bool) -> str:
+def pair_d(n: int, v: int, d: int) -> int:  # kernels.hpp rt_pair_d
+    """Paired-shift cases exist for the V = 4 instances only (the single-output
+    V = 2 shape is HBM-bound without them), for every distance up to (n-1)/2."""
+    return min(d, (n - 1) // 2) if v == 4 else 0
+
+
+def emit(w: int, n: int, e: int, v: int, par: bool, dmax: int = 0) -> str:
     """RtOps<...>::run(q, d, acc, x): threaded dispatch of one op list (bytes
-    c = i*n + sh, terminated by e*n) read from shared memory at q, with d the op
-    already loaded.  Every case ends with the jump to the next op: the op after it
-    is loaded one case ahead, so a case costs its XORs plus a move, a byte load, an
+    c = (i*(D+1) + ds)*n + sh, terminated by e*(D+1)*n) read from shared memory at
+    q, with d the op already loaded.  ds = 0 is the single shift sh; ds = 1..D is
+    the pair of shifts (sh, sh+ds) of one representative as ONE case: a ring row
+    both shifts reach takes one 3-input `lop3 0x96` instead of two XORs.  Every case
+    ends with the jump to the next op: the op after it is loaded one case ahead, so a case costs its XORs plus a move, a byte load, an
     add and the indexed jump.  The lists of one part lie back to back, so on
     return (at the sentinel) d already holds the first op of the next input's list
     and the next call jumps without waiting on shared memory."""
@@ -54,16 +64,21 @@ def emit(w: int, n: int, e: int, v: int, par: bool) -> str:
     xbase = nacc + 2
     lines = []
     targets = []
-    for c in range(e * n):
-        i, sh = divmod(c, n)
+    dd = pair_d(n, v, dmax)
+    for c in range(e * (dd + 1) * n):
+        ids, sh = divmod(c, n)
+        i, ds = divmod(ids, dd + 1)
         body = [f"mov.b32 c, %{dop}; ld.shared.u8 %{dop}, [%{qop}]; add.u32 %{qop}, %{qop}, 1;"]
-        for t in range(xr):
-            r = (t + sh) % n
-            if par and r >= w:
-                continue
+        for r in range(ar):
+            # input strips that land on accumulator row r: (r - sh) and, for a pair, (r - sh - ds) mod n
+            ts = [t for t in {(r - sh) % n, (r - sh - ds) % n} if t < xr] if ds else [t for t in [(r - sh) % n] if t < xr]
+            ts.sort()
             for l in range(v):
                 a = acc(i, r, l)
-                body.append(f"xor.b32 %{a}, %{a}, %{xop(t, l)};")
+                if len(ts) == 1:
+                    body.append(f"xor.b32 %{a}, %{a}, %{xop(ts[0], l)};")
+                elif len(ts) == 2:
+                    body.append(f"lop3.b32 %{a}, %{a}, %{xop(ts[0], l)}, %{xop(ts[1], l)}, 0x96;")
         body.append("brx.idx.uni c, T;")
         lab = f"L{c}"
         targets.append(lab)
@@ -90,16 +105,17 @@ def emit(w: int, n: int, e: int, v: int, par: bool) -> str:
     return "\n".join(s) + "\n"
 
 
-def generate() -> str:
-    out = ["// generated by paper_1709_00178_b200/gen_ring_rt.py -- do not edit\n"]
+def generate(dmax: int = 0) -> str:
+    out = ["// generated by paper_1709_00178_b200/gen_ring_rt.py -- do not edit\n",
+           f"static_assert(PYRIT_RT_PAIR_D == {dmax}, \"ring_rt_ops.inc was generated for another PYRIT_RT_PAIR_D\");\n"]
     for inst in instances():
-        out.append(emit(*inst))
+        out.append(emit(*inst, dmax=dmax))
     return "".join(out)
 
 
 def main(argv=None):
     argv = sys.argv[1:] if argv is None else argv
-    text = generate()
+    text = generate(int(argv[1]) if len(argv) > 1 else 0)
     with open(argv[0], "w") as f:
         f.write(text)
 

@@ -257,3 +257,20 @@ def test_ringmat_rejects_wide_elements():
         P.Plan.from_ringmat(f, np.array([[u ^ f.modulus]], dtype=np.uint32), P.TransformKind.Parity)
     with pytest.raises(P.PyritError):
         P.Plan.from_ringmat(f, np.zeros((0, 3), dtype=np.uint32))
+
+
+def test_planner_pairs_shifts_within_the_case_budget():
+    """Paired-shift cases (runtime.cpp rt_select_pairs): a four-output plan runs fewer ops
+    than its matrix has ring terms (a pair op covers two shifts of one representative),
+    the dispatch-case code the ops name stays within the instruction-cache budget, and a
+    single-output plan (V = 2 instance, no pair cases) runs one op per term."""
+    for c in (2, 3, 4, 5):
+        wl = WORKLOADS[c]
+        plan = P.Plan.decode(wl.code, list(wl.erased)) if wl.op == "decode" else P.Plan.encode(wl.code)
+        info = plan.rt_info()
+        assert info["launches"] == 1
+        assert info["terms"] // 2 <= info["ops"] < info["terms"], info
+        assert 0 < info["case_bytes"] <= 26 * 1024, info
+    wl = WORKLOADS[4]
+    one = P.Plan.decode(wl.code, [3]).rt_info()
+    assert one["ops"] == one["terms"]
