@@ -853,18 +853,21 @@ std::uint32_t rt_select_pairs(std::vector<RtEntry>& entries, std::uint32_t n, st
                               std::uint32_t V, std::uint32_t budget, Rows case_rows) {
     constexpr std::uint32_t kDispatch = 6; // instructions of a case besides its LOP3s
     auto bytes_of = [&](std::uint32_t sh, std::uint32_t ds) { return 16u * (case_rows(sh, ds) * V + kDispatch); };
+    static const std::uint32_t min_uses = static_cast<std::uint32_t>(std::max(1, env_int("PYRIT_B200_RT_PAIR_MINUSE", 1)));
     std::vector<std::uint32_t> rem(entries.size());
-    for (std::size_t x = 0; x < entries.size(); ++x) rem[x] = entries[x].mask, entries[x].ops.clear();
-    auto singles_bytes = [&]() {
-        std::uint32_t b = 0;
-        std::vector<std::uint32_t> seen(E, 0);
-        for (std::size_t x = 0; x < entries.size(); ++x) {
-            for (std::uint32_t m = rem[x] & ~seen[entries[x].i]; m; m &= m - 1)
-                b += bytes_of(static_cast<std::uint32_t>(std::countr_zero(m)), 0);
-            seen[entries[x].i] |= rem[x];
+    // need[i*n + sh]: entries of local output i whose shift sh is still unpaired (a single
+    // case (i, sh) is named while it is > 0); singles: bytes of those cases
+    std::vector<std::uint32_t> need(std::size_t(E) * n, 0), single_bytes(n);
+    for (std::uint32_t sh = 0; sh < n; ++sh) single_bytes[sh] = bytes_of(sh, 0);
+    std::uint32_t singles = 0;
+    for (std::size_t x = 0; x < entries.size(); ++x) {
+        rem[x] = entries[x].mask;
+        entries[x].ops.clear();
+        for (std::uint32_t m = rem[x]; m; m &= m - 1) {
+            const std::uint32_t sh = static_cast<std::uint32_t>(std::countr_zero(m));
+            if (need[entries[x].i * n + sh]++ == 0) singles += single_bytes[sh];
         }
-        return b;
-    };
+    }
     std::uint32_t pair_bytes = 0;
     if (D > 0) {
         // per-use saving of a pair at distance d (independent of sh for the Embedding; the
@@ -874,47 +877,56 @@ std::uint32_t rt_select_pairs(std::vector<RtEntry>& entries, std::uint32_t n, st
             const std::uint32_t two = case_rows(0, 0) + case_rows(d % n, 0), one = case_rows(0, d);
             saving[d] = (two > one ? two - one : 0) * V + kDispatch;
         }
-        std::vector<std::uint32_t> cnt(std::size_t(E) * (D + 1) * n);
+        // cnt[(i*(D+1) + d)*n + sh]: entries of output i with shifts sh and sh+d both unpaired
+        std::vector<std::uint32_t> cnt(std::size_t(E) * (D + 1) * n, 0);
         std::vector<bool> taken(cnt.size(), false);
+        for (std::size_t x = 0; x < entries.size(); ++x)
+            for (std::uint32_t m = rem[x]; m; m &= m - 1) {
+                const std::uint32_t sh = static_cast<std::uint32_t>(std::countr_zero(m));
+                for (std::uint32_t d = 1; d <= D; ++d)
+                    if ((rem[x] >> ((sh + d) % n)) & 1u) ++cnt[(entries[x].i * (D + 1) + d) * n + sh];
+            }
+        auto drop_bit = [&](std::size_t x, std::uint32_t b) { // shift b of entry x is now paired
+            const std::uint32_t i = entries[x].i;
+            for (std::uint32_t d = 1; d <= D; ++d) {
+                if ((rem[x] >> ((b + d) % n)) & 1u) --cnt[(i * (D + 1) + d) * n + b];
+                const std::uint32_t q = (b + n - d) % n;
+                if ((rem[x] >> q) & 1u) --cnt[(i * (D + 1) + d) * n + q];
+            }
+            rem[x] &= ~(1u << b);
+            if (--need[i * n + b] == 0) singles -= single_bytes[b];
+        };
         for (;;) {
-            std::fill(cnt.begin(), cnt.end(), 0);
-            for (std::size_t x = 0; x < entries.size(); ++x)
-                for (std::uint32_t m = rem[x]; m; m &= m - 1) {
-                    const std::uint32_t sh = static_cast<std::uint32_t>(std::countr_zero(m));
-                    for (std::uint32_t d = 1; d <= D; ++d)
-                        if ((rem[x] >> ((sh + d) % n)) & 1u) ++cnt[(entries[x].i * (D + 1) + d) * n + sh];
-                }
             std::size_t best = cnt.size();
             std::uint64_t best_score = 0;
-            static const std::uint32_t min_uses = static_cast<std::uint32_t>(std::max(1, env_int("PYRIT_B200_RT_PAIR_MINUSE", 1)));
             for (std::size_t c = 0; c < cnt.size(); ++c) {
-                if (cnt[c] < min_uses && !taken[c]) continue; // a case hardly used only adds instruction-cache misses
+                if (cnt[c] < min_uses && !taken[c]) continue; // (A/B knob: a case hardly used only adds code)
                 const std::uint64_t score = std::uint64_t(cnt[c]) * saving[(c / n) % (D + 1)];
                 if (score > best_score) best = c, best_score = score;
             }
             if (best == cnt.size()) break;
             const std::uint32_t sh = static_cast<std::uint32_t>(best % n), d = static_cast<std::uint32_t>((best / n) % (D + 1)),
-                                i = static_cast<std::uint32_t>(best / n / (D + 1));
-            const std::uint32_t both = (1u << sh) | (1u << ((sh + d) % n));
+                                i = static_cast<std::uint32_t>(best / n / (D + 1)), sh2 = (sh + d) % n;
+            const std::uint32_t both = (1u << sh) | (1u << sh2), hits = cnt[best];
+            // the budget with the singles that would remain: every hit entry drops both shifts
             const std::uint32_t add = taken[best] ? 0u : bytes_of(sh, d);
-            // apply, then check the budget with the singles that remain
-            std::vector<std::size_t> hit;
+            const std::uint32_t freed = (need[i * n + sh] == hits ? single_bytes[sh] : 0u) +
+                                        (need[i * n + sh2] == hits ? single_bytes[sh2] : 0u);
+            if (pair_bytes + add + singles - freed > budget) break;
             for (std::size_t x = 0; x < entries.size(); ++x)
-                if (entries[x].i == i && (rem[x] & both) == both) rem[x] &= ~both, hit.push_back(x);
-            if (pair_bytes + add + singles_bytes() > budget) {
-                for (std::size_t x : hit) rem[x] |= both;
-                break;
-            }
-            for (std::size_t x : hit) entries[x].ops.emplace_back(sh, d);
+                if (entries[x].i == i && (rem[x] & both) == both) {
+                    drop_bit(x, sh);
+                    drop_bit(x, sh2);
+                    entries[x].ops.emplace_back(sh, d);
+                }
             pair_bytes += add;
             taken[best] = true;
         }
     }
-    const std::uint32_t total = pair_bytes + singles_bytes();
     for (std::size_t x = 0; x < entries.size(); ++x)
         for (std::uint32_t m = rem[x]; m; m &= m - 1)
             entries[x].ops.emplace_back(static_cast<std::uint32_t>(std::countr_zero(m)), 0u);
-    return total;
+    return pair_bytes + singles;
 }
 
 // device = false: the same launch plan without tensor maps or a device query

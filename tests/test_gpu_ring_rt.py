@@ -301,3 +301,32 @@ def test_warmup_loads_every_geometry(cuda):
     torch.cuda.synchronize()
     assert torch.equal(full, ref)
     assert lib.pyrit_jit_compiles() == jit0
+
+
+@pytest.mark.parametrize("f", [G256, G4096], ids=lambda f: f"w{f.w}n{f.n}")
+def test_planned_launches_rebind_to_new_buffers(cuda, f):
+    """The planner's result (op lists, parts, pair cases) is kept per program and thread;
+    the same program on other buffers, another window or after another program only gets
+    new tensor maps and output bases (runtime.cpp bind_ring_rt).  Alternate two programs
+    over two buffer sets and two windows; every result against the oracle."""
+    rng = np.random.default_rng(100 + f.w)
+    k, e = 7, 4
+    strip = 16 * 520
+    ss = f.w * strip
+    mats = [rng.integers(1, 1 << f.w, (e, k), dtype=np.uint16) for _ in range(2)]
+    plans = [P.Plan.create(f, m) for m in mats]
+    datas = [rand_symbols(k, ss, 40 + i) for i in range(2)]
+    wants = [[oracle_ring(f, m, d) for d in datas] for m in mats]
+    with mode(4):
+        for step, (pi, di, win) in enumerate([(0, 0, None), (1, 0, None), (0, 1, None), (1, 1, (16 * 9, 16 * 200)),
+                                              (0, 0, (0, 16 * 131)), (0, 1, None), (1, 0, None)]):
+            off, length = win if win else (0, strip)
+            init = rand_symbols(e, ss, 60 + step)
+            got = run_plan(cuda, plans[pi], datas[di], e, strip, off, length, init=init)
+            rt_launched()
+            exp = init.copy()
+            for i in range(e):
+                for s in range(f.w):
+                    a = s * strip + off
+                    exp[i, a:a + length] = wants[pi][di][i, a:a + length]
+            np.testing.assert_array_equal(got, exp, err_msg=f"step {step}")
