@@ -645,7 +645,12 @@ def run_e2e_devices(P, wl, world, rank, steps):
 def run_e2e(P, wl, s0, sym, Ls, dev, world, steps):
     import torch
     import torch.distributed as dist
+    from paper_1709_00178_b200 import _lib as L
     local = dev.index
+    # multi-GPU hosts: this rank's pinned buffers and its copies belong on the NUMA node of
+    # its GPU's PCIe slot (best effort; -1 = unknown or a single node: nothing changed)
+    saved_cpus = os.sched_getaffinity(0)
+    numa_node = int(L.load().pyrit_numa_bind_thread(local))
     if wl.op == "encode":
         host_in = torch.empty((wl.k, sym), dtype=torch.uint8, pin_memory=True)
         host_in.copy_(s0[2])
@@ -679,7 +684,9 @@ def run_e2e(P, wl, s0, sym, Ls, dev, world, steps):
     ok = True
     if wl.op == "encode":
         ok = bool(torch.equal(host_out.to(dev), s0[3]))
-    return {"value": wl.source_bytes() / t.item() / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
+    if numa_node >= 0:
+        os.sched_setaffinity(0, saved_cpus)
+    return {"numa_node": numa_node, "value": wl.source_bytes() / t.item() / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": t.item() * 1e3, "steps": steps,
             "api": "pyrit_encode_host" if wl.op == "encode" else "pyrit_decode_host", "pinned": True,
             "matches_device_path": ok}

@@ -261,6 +261,14 @@ int pyrit_decode_host(const pyrit_code* code, uint8_t* symbols, const uint32_t* 
                       uint64_t symbol_size, int device);
 /* bytes per strip per pipeline chunk (0 = automatic) */
 int pyrit_set_host_chunk(uint64_t strip_chunk_bytes);
+/* Multi-GPU hosts: restrict the CALLING thread to the CPUs of the NUMA node the device's
+ * PCIe slot belongs to, so the host buffers it allocates and touches next (and the copies it
+ * makes) are local to that GPU's link -- call it in each per-GPU worker before allocating its
+ * pinned buffers (the reference's parallel_replay workers, codec.hpp:176-193, have no such
+ * notion: they share one memory).  Best effort: returns the node, or -1 (and changes nothing)
+ * when the platform does not say, PYRIT_B200_NUMA=0, or the node's CPUs are outside the
+ * process's cpuset.  pyrit_*_host_devices does this for its per-device threads. */
+int pyrit_numa_bind_thread(int device);
 
 /* ---- shard container and file codec (container.hpp) ------------------ */
 #define PYRIT_HEADER_SIZE 29 /* container.hpp:38 */

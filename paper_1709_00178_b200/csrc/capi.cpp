@@ -536,6 +536,8 @@ int pyrit_rt_interpret(const pyrit_plan* plan, const uint8_t* const* in, uint8_t
     });
 }
 
+int pyrit_numa_bind_thread(int device) { return numa_bind_thread(device); }
+
 int pyrit_rt_plan_info(const pyrit_plan* plan, uint32_t info[4]) {
     return guarded([&] {
         if (!plan || !info) raise(Errc::InvalidArgument, "null argument");

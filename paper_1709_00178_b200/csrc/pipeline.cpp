@@ -6,6 +6,7 @@
 #include "pipeline.hpp"
 
 #include <immintrin.h>
+#include <sched.h>
 
 #include <cstdio>
 #include <cstring>
@@ -13,6 +14,7 @@
 #include "hostpool.hpp"
 
 #include <algorithm>
+#include <cctype>
 #include <cstdlib>
 #include <map>
 #include <memory>
@@ -69,6 +71,69 @@ DeviceCtx& ctx_for(int device) {
 
 void set_host_chunk(std::uint64_t bytes) { g_chunk = bytes; }
 
+namespace {
+
+// "0-13,28-41" -> cpu set (sysfs cpulist)
+bool parse_cpulist(const std::string& text, cpu_set_t& set) {
+    CPU_ZERO(&set);
+    bool any = false;
+    std::size_t i = 0;
+    while (i < text.size()) {
+        while (i < text.size() && !std::isdigit(static_cast<unsigned char>(text[i]))) ++i;
+        if (i >= text.size()) break;
+        long a = 0, b;
+        while (i < text.size() && std::isdigit(static_cast<unsigned char>(text[i]))) a = a * 10 + (text[i++] - '0');
+        b = a;
+        if (i < text.size() && text[i] == '-') {
+            ++i;
+            b = 0;
+            while (i < text.size() && std::isdigit(static_cast<unsigned char>(text[i]))) b = b * 10 + (text[i++] - '0');
+        }
+        for (long c = a; c <= b && c < CPU_SETSIZE; ++c) CPU_SET(static_cast<int>(c), &set), any = true;
+    }
+    return any;
+}
+
+std::string read_small_file(const std::string& path) {
+    std::string out;
+    if (FILE* f = std::fopen(path.c_str(), "r")) {
+        char buf[4096];
+        const std::size_t n = std::fread(buf, 1, sizeof buf, f);
+        out.assign(buf, n);
+        std::fclose(f);
+    }
+    return out;
+}
+
+} // namespace
+
+int numa_bind_thread(int device) {
+    static const bool enabled = [] {
+        const char* e = std::getenv("PYRIT_B200_NUMA");
+        return !e || std::atoi(e) != 0;
+    }();
+    if (!enabled) return -1;
+    char bus[32] = {};
+    if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    std::string id(bus);
+    for (char& c : id) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+    const std::string node_text = read_small_file("/sys/bus/pci/devices/" + id + "/numa_node");
+    if (node_text.empty()) return -1;
+    const int node = std::atoi(node_text.c_str());
+    if (node < 0) return -1; // one node, or the platform does not say
+    cpu_set_t want, have, both;
+    if (!parse_cpulist(read_small_file("/sys/devices/system/node/node" + std::to_string(node) + "/cpulist"), want))
+        return -1;
+    if (sched_getaffinity(0, sizeof have, &have) != 0) return -1;
+    CPU_AND(&both, &want, &have);
+    if (CPU_COUNT(&both) == 0) return -1; // the node's CPUs are outside this process's cpuset
+    if (sched_setaffinity(0, sizeof both, &both) != 0) return -1;
+    return node;
+}
+
 void run_host(const Program& p, const std::vector<const std::uint8_t*>& host_in,
               const std::vector<std::uint8_t*>& host_out, std::uint64_t strip, int device) {
     run_host_window(p, host_in, host_out, strip, 0, strip, device);
@@ -89,6 +154,9 @@ void run_host_devices(const Program& p, const std::vector<const std::uint8_t*>& 
         const std::uint64_t hi = d + 1 == n ? strip : strip * (d + 1) / n / 16 * 16;
         th.emplace_back([&, d, lo, hi] {
             try {
+                // staging copies and pinned staging buffers of this shard stay on the
+                // NUMA node its GPU hangs off (best effort)
+                if (n > 1) numa_bind_thread(devices[d]);
                 run_host_window(p, host_in, host_out, strip, lo, hi - lo, devices[d]);
             } catch (...) {
                 errs[d] = std::current_exception();

@@ -25,5 +25,10 @@ void run_host_devices(const Program& p, const std::vector<const std::uint8_t*>& 
                       const std::vector<int>& devices);
 
 void set_host_chunk(std::uint64_t bytes);
+// Best effort: restrict the calling thread to the CPUs of the NUMA node the device's
+// PCIe slot belongs to (sysfs), so host buffers it touches first and its staging copies
+// are local to that GPU's link.  Returns the node, or -1 when unknown, disabled
+// (PYRIT_B200_NUMA=0) or outside the process's cpuset; the affinity is then unchanged.
+int numa_bind_thread(int device);
 
 } // namespace pyrit_b200

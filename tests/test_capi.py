@@ -148,3 +148,13 @@ def test_header_is_plain_c(tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0, (out.returncode, out.stderr)
     assert "sm_100a" in out.stdout
+
+
+def test_numa_bind_without_a_device_changes_nothing():
+    """pyrit_numa_bind_thread is best effort: with no usable device (or an unknown node) it
+    returns -1 and leaves the calling thread's affinity as it was."""
+    lib = L.load()
+    before = os.sched_getaffinity(0)
+    node = lib.pyrit_numa_bind_thread(1 << 20)
+    assert node == -1
+    assert os.sched_getaffinity(0) == before
