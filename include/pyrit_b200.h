@@ -269,6 +269,10 @@ int pyrit_set_host_chunk(uint64_t strip_chunk_bytes);
  * when the platform does not say, PYRIT_B200_NUMA=0, or the node's CPUs are outside the
  * process's cpuset.  pyrit_*_host_devices does this for its per-device threads. */
 int pyrit_numa_bind_thread(int device);
+/* the same from a sysfs-style CPU list ("0-13,28-41") for callers that know their topology:
+ * the calling thread keeps the listed CPUs it is allowed on; returns the CPUs listed, or -1
+ * (nothing changed) for an empty or malformed list or one disjoint from the thread's cpuset */
+int pyrit_bind_thread_cpulist(const char* cpulist);
 
 /* ---- shard container and file codec (container.hpp) ------------------ */
 #define PYRIT_HEADER_SIZE 29 /* container.hpp:38 */

@@ -63,7 +63,7 @@ EXPORTS = (
     "pyrit_set_file_chunk", "pyrit_cu_encode_crs", "pyrit_encode_crs_host", "pyrit_encode_host_devices",
     "pyrit_decode_host_devices", "pyrit_plan_from_schedule", "pyrit_apply_host", "pyrit_jit_info",
     "pyrit_jit_wait", "pyrit_jit_time", "pyrit_rt_interpret", "pyrit_plan_from_ringmat", "pyrit_cu_apply_ringmat",
-    "pyrit_warmup", "pyrit_rt_plan_info", "pyrit_numa_bind_thread",
+    "pyrit_warmup", "pyrit_rt_plan_info", "pyrit_numa_bind_thread", "pyrit_bind_thread_cpulist",
 )
 
 HEADER_SIZE = 29
@@ -124,6 +124,7 @@ def load():
     lib.pyrit_plan_from_ringmat.argtypes = [P(pyrit_ringmat), vp]
     lib.pyrit_warmup.argtypes = [i32]
     lib.pyrit_numa_bind_thread.argtypes = [i32]
+    lib.pyrit_bind_thread_cpulist.argtypes = [C.c_char_p]
     lib.pyrit_cu_apply_ringmat.argtypes = [P(pyrit_ringmat), vp, vp, u64, u64, u64, vp]
     lib.pyrit_kernel_launches.restype = u64
     lib.pyrit_field_named.argtypes = [C.c_char_p, P(pyrit_field)]

@@ -537,6 +537,7 @@ int pyrit_rt_interpret(const pyrit_plan* plan, const uint8_t* const* in, uint8_t
 }
 
 int pyrit_numa_bind_thread(int device) { return numa_bind_thread(device); }
+int pyrit_bind_thread_cpulist(const char* cpulist) { return bind_thread_cpulist(cpulist); }
 
 int pyrit_rt_plan_info(const pyrit_plan* plan, uint32_t info[4]) {
     return guarded([&] {

@@ -94,6 +94,16 @@ bool parse_cpulist(const std::string& text, cpu_set_t& set) {
     return any;
 }
 
+// the calling thread keeps only those of its CPUs that are in `want`; false (nothing
+// changed) when none is
+bool bind_thread_to(const cpu_set_t& want) {
+    cpu_set_t have, both;
+    if (sched_getaffinity(0, sizeof have, &have) != 0) return false;
+    CPU_AND(&both, &want, &have);
+    if (CPU_COUNT(&both) == 0) return false;
+    return sched_setaffinity(0, sizeof both, &both) == 0;
+}
+
 std::string read_small_file(const std::string& path) {
     std::string out;
     if (FILE* f = std::fopen(path.c_str(), "r")) {
@@ -113,25 +123,45 @@ int numa_bind_thread(int device) {
         return !e || std::atoi(e) != 0;
     }();
     if (!enabled) return -1;
-    char bus[32] = {};
-    if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) {
-        cudaGetLastError();
-        return -1;
+    // the node and its CPUs per device, looked up in sysfs once per process
+    struct Node {
+        int node = -1;
+        cpu_set_t cpus;
+    };
+    static std::mutex mu;
+    static std::map<int, Node> known;
+    Node nd;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = known.find(device);
+        if (it == known.end()) {
+            Node found;
+            CPU_ZERO(&found.cpus);
+            char bus[32] = {};
+            if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) == cudaSuccess) {
+                std::string id(bus);
+                for (char& c : id) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+                const std::string node_text = read_small_file("/sys/bus/pci/devices/" + id + "/numa_node");
+                const int node = node_text.empty() ? -1 : std::atoi(node_text.c_str()); // < 0: one node, or not said
+                if (node >= 0 &&
+                    parse_cpulist(read_small_file("/sys/devices/system/node/node" + std::to_string(node) + "/cpulist"),
+                                  found.cpus))
+                    found.node = node;
+            } else {
+                (void)cudaGetLastError();
+            }
+            it = known.emplace(device, found).first;
+        }
+        nd = it->second;
     }
-    std::string id(bus);
-    for (char& c : id) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
-    const std::string node_text = read_small_file("/sys/bus/pci/devices/" + id + "/numa_node");
-    if (node_text.empty()) return -1;
-    const int node = std::atoi(node_text.c_str());
-    if (node < 0) return -1; // one node, or the platform does not say
-    cpu_set_t want, have, both;
-    if (!parse_cpulist(read_small_file("/sys/devices/system/node/node" + std::to_string(node) + "/cpulist"), want))
-        return -1;
-    if (sched_getaffinity(0, sizeof have, &have) != 0) return -1;
-    CPU_AND(&both, &want, &have);
-    if (CPU_COUNT(&both) == 0) return -1; // the node's CPUs are outside this process's cpuset
-    if (sched_setaffinity(0, sizeof both, &both) != 0) return -1;
-    return node;
+    if (nd.node < 0) return -1;
+    return bind_thread_to(nd.cpus) ? nd.node : -1;
+}
+
+int bind_thread_cpulist(const char* cpulist) {
+    cpu_set_t want;
+    if (!cpulist || !parse_cpulist(cpulist, want)) return -1;
+    return bind_thread_to(want) ? CPU_COUNT(&want) : -1;
 }
 
 void run_host(const Program& p, const std::vector<const std::uint8_t*>& host_in,

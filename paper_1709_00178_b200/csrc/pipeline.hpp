@@ -30,5 +30,9 @@ void set_host_chunk(std::uint64_t bytes);
 // are local to that GPU's link.  Returns the node, or -1 when unknown, disabled
 // (PYRIT_B200_NUMA=0) or outside the process's cpuset; the affinity is then unchanged.
 int numa_bind_thread(int device);
+// The same restriction from a sysfs-style CPU list ("0-13,28-41"): the calling thread keeps
+// the listed CPUs it is allowed on.  Returns the CPUs listed, or -1 (nothing changed) when
+// the list is empty, malformed or disjoint from the thread's cpuset.
+int bind_thread_cpulist(const char* cpulist);
 
 } // namespace pyrit_b200

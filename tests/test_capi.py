@@ -158,3 +158,36 @@ def test_numa_bind_without_a_device_changes_nothing():
     node = lib.pyrit_numa_bind_thread(1 << 20)
     assert node == -1
     assert os.sched_getaffinity(0) == before
+
+
+def test_bind_thread_cpulist():
+    """The affinity step of pyrit_numa_bind_thread on its own: a sysfs-style CPU list is
+    intersected with the thread's cpuset; a disjoint, empty or malformed list changes nothing."""
+    import threading
+    lib = L.load()
+    allowed = sorted(os.sched_getaffinity(0))
+    seen = {}
+
+    def worker():  # affinity is per thread: do it off the main thread
+        lo = allowed[0]
+        seen["one"] = (lib.pyrit_bind_thread_cpulist(f"{lo}\n".encode()), os.sched_getaffinity(0))
+        seen["disjoint"] = (lib.pyrit_bind_thread_cpulist(b"100000-100003"), os.sched_getaffinity(0))
+        seen["empty"] = lib.pyrit_bind_thread_cpulist(b"")
+        seen["junk"] = lib.pyrit_bind_thread_cpulist(b"abc")
+
+    t = threading.Thread(target=worker)
+    t.start()
+    t.join()
+    assert seen["one"] == (1, {allowed[0]})
+    assert seen["disjoint"] == (-1, {allowed[0]})
+    assert seen["empty"] == -1 and seen["junk"] == -1
+    assert sorted(os.sched_getaffinity(0)) == allowed  # the main thread is untouched
+
+    def ranges():
+        seen["range"] = (lib.pyrit_bind_thread_cpulist(f"{allowed[0]}-{allowed[-1]},{allowed[0]}".encode()),
+                         os.sched_getaffinity(0))
+
+    t = threading.Thread(target=ranges)
+    t.start()
+    t.join()
+    assert seen["range"][1] == set(allowed)
