@@ -43,6 +43,7 @@ def _default_pair_d() -> int:
 
 
 RT_PAIR_D = int(os.environ.get("PYRIT_B200_BUILD_RT_PAIR_D", "") or _default_pair_d())
+RT_PAIR_AOP_ALL = int(os.environ.get("PYRIT_B200_BUILD_RT_PAIR_AOP_ALL", "0"))
 CUDA_SOURCES = ["kernels.cu", "ring_rt.cu", "ring_rt_w4_n5.cu", "ring_rt_w6_n9.cu", "ring_rt_w8_n17.cu",
                 "ring_rt_w10_n11.cu", "ring_rt_w12_n13.cu"]
 HEADERS = ["algebra.hpp", "program.hpp", "runtime.hpp", "pipeline.hpp", "plans.hpp", "container.hpp", "kernels.hpp",
@@ -65,9 +66,9 @@ def build_library(force=False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "pyrit_b200.h")]
     stamp = os.path.join(BUILD, "rt_pair_d.stamp")  # objects depend on the -D value they were built with
-    if not os.path.exists(stamp) or open(stamp).read() != str(RT_PAIR_D):
+    if not os.path.exists(stamp) or open(stamp).read() != f"{RT_PAIR_D},{RT_PAIR_AOP_ALL}":
         with open(stamp, "w") as f:
-            f.write(str(RT_PAIR_D))
+            f.write(f"{RT_PAIR_D},{RT_PAIR_AOP_ALL}")
     hdrs.append(stamp)
     objs = []
     for src in HOST_SOURCES:
@@ -75,7 +76,7 @@ def build_library(force=False) -> str:
         o = os.path.join(BUILD, src + ".o")
         if force or _stale(o, [s] + hdrs):
             _run(["g++", "-std=c++20", "-O2", "-g", "-fPIC", "-fvisibility=hidden", "-Wall", "-Wextra",
-                  f"-I{CUDA}/include", f"-DPYRIT_RT_PAIR_D={RT_PAIR_D}", f'-DPYRIT_NVRTC_PATH="{CUDA}/lib64/libnvrtc.so.12"', "-c", s, "-o", o])
+                  f"-I{CUDA}/include", f"-DPYRIT_RT_PAIR_D={RT_PAIR_D}", f"-DPYRIT_RT_PAIR_AOP_ALL={RT_PAIR_AOP_ALL}", f'-DPYRIT_NVRTC_PATH="{CUDA}/lib64/libnvrtc.so.12"', "-c", s, "-o", o])
         objs.append(o)
     # dispatch tables of the runtime-matrix ring kernel (generated, build/generated)
     gen_dir = os.path.join(BUILD, "generated")
@@ -85,7 +86,7 @@ def build_library(force=False) -> str:
     sys.path.insert(0, ROOT)
     from paper_1709_00178_b200 import gen_ring_rt
 
-    text = gen_ring_rt.generate(RT_PAIR_D)
+    text = gen_ring_rt.generate(RT_PAIR_D, bool(RT_PAIR_AOP_ALL))
     if force or not os.path.exists(inc) or open(inc).read() != text:
         with open(inc, "w") as f:
             f.write(text)
@@ -95,7 +96,7 @@ def build_library(force=False) -> str:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         if force or _stale(o, [s, inc] + hdrs):
-            jobs.append([NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", f"-I{gen_dir}", f"-DPYRIT_RT_PAIR_D={RT_PAIR_D}",
+            jobs.append([NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", f"-I{gen_dir}", f"-DPYRIT_RT_PAIR_D={RT_PAIR_D}", f"-DPYRIT_RT_PAIR_AOP_ALL={RT_PAIR_AOP_ALL}",
                          "-Xcompiler",
                          "-fPIC,-fvisibility=hidden", "-c", s, "-o", o])
         objs.append(o)

@@ -51,7 +51,7 @@ struct alignas(64) RtArgs {
     std::uint32_t epart[kRtMaxGroups][kRtParts]; // outputs of each part of each group
     std::uint32_t fm[256]; // Parity: fm[q*w + i] = ~0 when strip i feeds the parity strip w+q (i = q mod s)
     // op list of input j for part p of group g: ops[opoff[g][p][j] ..], each
-    // c = (i*(D+1) + ds)*n + sh with D = rt_pair_d(n, V): output i of the part
+    // c = (i*(D+1) + ds)*n + sh with D = rt_pair_d(w, n, V): output i of the part
     // accumulates input j rotated by sh ring positions (ds = 0) or by sh and sh+ds
     // (a pair) -- set bits of the representative of entry (i, j) -- terminated by E*(D+1)*n
     std::uint16_t opoff[kRtMaxGroups][kRtParts][kRtMaxK + 1];
@@ -74,15 +74,24 @@ constexpr int rt_part_outputs(int n, int w, int v) {
 }
 // Paired-shift cases: two shifts (sh, sh+d) of one representative are one op whose
 // ring rows reached by both take a 3-input LOP3 (gen_ring_rt.py).  The V = 4 instances
-// carry a case for every pair distance d <= min(PYRIT_RT_PAIR_D, (n-1)/2) -- a
-// build-time constant (0: no pair cases); which of them a launch uses is the
-// planner's choice (runtime.cpp rt_select_pairs: the cases that pay most within the
-// instruction-cache budget).  V = 2 instances (single output, HBM-bound) have none.
+// carry a case for every pair distance d <= PYRIT_RT_PAIR_D, a build-time constant
+// (0: no pair cases).  PYRIT_RT_PAIR_AOP_ALL=1 builds every distance, (n-1)/2, in the
+// all-one-polynomial fields (w = n-1), where two windows of w strips on the ring of n
+// overlap in w-1 rows at ANY distance; measured no better (config 5 encode +2%, its
+// four-symbol decode patterns -2%, profiles/r02/ring_rt_pairs/aop_all_distances/), so
+// it is off.  Which cases a launch uses is the planner's choice (runtime.cpp
+// rt_select_pairs: the cases that pay most within the instruction-cache budget).
+// V = 2 instances (single output, HBM-bound) have none.
 #ifndef PYRIT_RT_PAIR_D
 #define PYRIT_RT_PAIR_D 3
 #endif
-constexpr std::uint32_t rt_pair_d(std::uint32_t n, std::uint32_t v) {
-    return v != 4 ? 0u : (n - 1) / 2 < PYRIT_RT_PAIR_D ? (n - 1) / 2 : PYRIT_RT_PAIR_D;
+#ifndef PYRIT_RT_PAIR_AOP_ALL
+#define PYRIT_RT_PAIR_AOP_ALL 0
+#endif
+constexpr std::uint32_t rt_pair_d(std::uint32_t w, std::uint32_t n, std::uint32_t v) {
+    return v != 4 || PYRIT_RT_PAIR_D == 0 ? 0u
+           : (PYRIT_RT_PAIR_AOP_ALL && w + 1 == n) || (n - 1) / 2 < PYRIT_RT_PAIR_D ? (n - 1) / 2
+                                                                                    : PYRIT_RT_PAIR_D;
 }
 bool rt_supported(std::uint32_t w, std::uint32_t n, std::uint32_t modulus);
 cudaError_t launch_ring_rt(const RtArgs& a, const RtLaunch& l);

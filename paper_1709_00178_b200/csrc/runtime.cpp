@@ -1050,7 +1050,7 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
         // PYRIT_B200_RT_PAIRS=0 (singles only), _RT_CODE_KB, _RT_PAIR_DMAX, _RT_PAIR_MINUSE.
         static const int pairs_knob = env_int("PYRIT_B200_RT_PAIRS", 1);
         static const int code_kb = env_int("PYRIT_B200_RT_CODE_KB", 26);
-        const std::uint32_t D = rt_pair_d(n, l.V);
+        const std::uint32_t D = rt_pair_d(w, n, l.V);
         const std::uint32_t xr = par ? n : w, ar = par ? w : n;
         auto case_rows = [&](std::uint32_t sh, std::uint32_t ds) { // gen_ring_rt.py emit(): one LOP3 per reached row and word
             std::uint32_t rows = 0;
@@ -1146,7 +1146,7 @@ void interpret_ring_rt(const Program& p, const std::uint8_t* const* in, std::uin
     for (std::size_t c = 0; c < call.launches.size(); ++c) {
         const RtArgs& a = *call.args[c];
         const RtLaunch& l = call.launches[c];
-        const std::uint32_t E = l.E, G = a.ngrp, D = rt_pair_d(n, l.V);
+        const std::uint32_t E = l.E, G = a.ngrp, D = rt_pair_d(w, n, l.V);
         std::vector<std::uint64_t> acc(std::size_t(E) * ar), x(n);
         for (std::uint64_t u = 0; u < std::uint64_t(a.ntiles) * G; ++u) {
             const std::uint64_t t = u / G, g = u % G, b = t / a.tpb, tt = t - b * a.tpb;

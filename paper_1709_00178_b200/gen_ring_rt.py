@@ -10,7 +10,7 @@ paired-shift case, rows reached by both with one 3-input LOP3), into the
 accumulators of output i (schedule.hpp:132-161: ring row t of output i
 accumulates input strip (t - sh) mod n).  Every register index inside a case is
 fixed, so the runtime matrix never indexes registers dynamically, and the jump
-is warp-uniform.  D = pair_d(n, v, PYRIT_RT_PAIR_D) (csrc/kernels.hpp rt_pair_d).
+is warp-uniform.  D = pair_d(w, n, v, PYRIT_RT_PAIR_D) (csrc/kernels.hpp rt_pair_d).
 The instance list (FIELDS) must match PYRIT_RT_FIELDS in csrc/ring_rt.cu.
 """
 from __future__ import annotations
@@ -33,13 +33,16 @@ def instances():
                     yield w, n, e, v, par
 
 
-def pair_d(n: int, v: int, d: int) -> int:  # kernels.hpp rt_pair_d
+def pair_d(w: int, n: int, v: int, d: int, aop_all: bool = True) -> int:  # kernels.hpp rt_pair_d
     """Paired-shift cases exist for the V = 4 instances only (the single-output
-    V = 2 shape is HBM-bound without them), for every distance up to (n-1)/2."""
-    return min(d, (n - 1) // 2) if v == 4 else 0
+    V = 2 shape is HBM-bound without them): distances up to d, or every distance
+    in the all-one-polynomial fields (w = n-1), where any pair overlaps in w-1 rows."""
+    if v != 4 or d == 0:
+        return 0
+    return (n - 1) // 2 if (aop_all and w + 1 == n) else min(d, (n - 1) // 2)
 
 
-def emit(w: int, n: int, e: int, v: int, par: bool, dmax: int = 0) -> str:
+def emit(w: int, n: int, e: int, v: int, par: bool, dmax: int = 0, aop_all: bool = True) -> str:
     """RtOps<...>::run(q, d, acc, x): threaded dispatch of one op list (bytes
     c = (i*(D+1) + ds)*n + sh, terminated by e*(D+1)*n) read from shared memory at
     q, with d the op already loaded.  ds = 0 is the single shift sh; ds = 1..D is
@@ -64,7 +67,7 @@ def emit(w: int, n: int, e: int, v: int, par: bool, dmax: int = 0) -> str:
     xbase = nacc + 2
     lines = []
     targets = []
-    dd = pair_d(n, v, dmax)
+    dd = pair_d(w, n, v, dmax, aop_all)
     for c in range(e * (dd + 1) * n):
         ids, sh = divmod(c, n)
         i, ds = divmod(ids, dd + 1)
@@ -87,7 +90,8 @@ def emit(w: int, n: int, e: int, v: int, par: bool, dmax: int = 0) -> str:
     outs = ", ".join(f'"+r"(acc[{i}][{r}][{l}])' for i in range(e) for r in range(ar) for l in range(v))
     ins = ", ".join(f'"r"(x[{t}][{l}])' for t in range(xr) for l in range(v))
     tpl = f"{w}, {n}, {e}, {v}, {'true' if par else 'false'}"
-    s = [f"template <> struct RtOps<{tpl}> {{"]
+    s = [f"static_assert(rt_pair_d({w}, {n}, {v}) == {dd}, \"gen_ring_rt.py pair_d and kernels.hpp rt_pair_d disagree\");",
+         f"template <> struct RtOps<{tpl}> {{"]
     s.append(f"  static __device__ __forceinline__ void run(u32& q, u32& d, u32 (&acc)[{e}][{ar}][{v}], "
              f"const u32 (&x)[{xr}][{v}]) {{")
     s.append('    asm volatile("{\\n .reg .b32 c;\\n"')
@@ -105,17 +109,18 @@ def emit(w: int, n: int, e: int, v: int, par: bool, dmax: int = 0) -> str:
     return "\n".join(s) + "\n"
 
 
-def generate(dmax: int = 0) -> str:
+def generate(dmax: int = 0, aop_all: bool = True) -> str:
     out = ["// generated by paper_1709_00178_b200/gen_ring_rt.py -- do not edit\n",
-           f"static_assert(PYRIT_RT_PAIR_D == {dmax}, \"ring_rt_ops.inc was generated for another PYRIT_RT_PAIR_D\");\n"]
+           f"static_assert(PYRIT_RT_PAIR_D == {dmax} && PYRIT_RT_PAIR_AOP_ALL == {int(aop_all)}, "
+           "\"ring_rt_ops.inc was generated for other PYRIT_RT_PAIR_* values\");\n"]
     for inst in instances():
-        out.append(emit(*inst, dmax=dmax))
+        out.append(emit(*inst, dmax=dmax, aop_all=aop_all))
     return "".join(out)
 
 
 def main(argv=None):
     argv = sys.argv[1:] if argv is None else argv
-    text = generate(int(argv[1]) if len(argv) > 1 else 0)
+    text = generate(int(argv[1]) if len(argv) > 1 else 0, bool(int(argv[2])) if len(argv) > 2 else True)
     with open(argv[0], "w") as f:
         f.write(text)
 

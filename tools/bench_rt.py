@@ -111,15 +111,16 @@ def run_config(cfg, dev, reps, out):
     return same
 
 
-def run_patterns(n, dev, reps, out):
-    """Random config-4 erasure patterns on the runtime kernel, first launch timed (never compiled)."""
-    wl = WORKLOADS[4]
+def run_patterns(n, dev, reps, out, cfg=4):
+    """Random erasure patterns of config 4 (or --pattern-config 5: the config-5 code) on the
+    runtime kernel, first launch timed (never compiled)."""
+    wl = WORKLOADS[cfg]
     buf = setup(wl, dev)
     rows = [buf[j].data_ptr() for j in range(wl.k + wl.m)]
     P.Plan.encode(wl.code).apply(rows[: wl.k], rows[wl.k:], wl.strip)
     ref = buf.clone()
     rng = random.Random(7)
-    pats = [(0, 1, 2, 3), (1, 6, 9, 10)] + [tuple(sorted(rng.sample(range(14), 4))) for _ in range(n)]
+    pats = [(0, 1, 2, 3), (1, 6, 9, 10)] + [tuple(sorted(rng.sample(range(wl.k + wl.m), 4))) for _ in range(n)]
     # one and two lost symbols (the common failures) and three
     pats += [(3,), (11,), (0, 7), (5, 12), (2, 4, 9)]
     jit0 = L.load().pyrit_jit_compiles()
@@ -140,7 +141,7 @@ def run_patterns(n, dev, reps, out):
         outs = [rows[o] for o in plan.outputs]
         ms, _, kern4 = time_plan(plan, ins, outs, wl.strip, reps, 4)
         moved = (wl.k + len(er)) * wl.frag
-        line = {"pattern": list(er), "first_call_ms": round(first, 4), "kernel_first": kern, "kernel_ms": round(ms, 4),
+        line = {"pattern_cfg": cfg, "pattern": list(er), "first_call_ms": round(first, 4), "kernel_first": kern, "kernel_ms": round(ms, 4),
                 "moved_gbs": round(moved / ms / 1e6, 1), "frac": round(moved / ms / 1e6 / peak(), 4),
                 "repaired_ok": ok}
         print(json.dumps(line), flush=True)
@@ -196,6 +197,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="2,3,4,5")
     ap.add_argument("--patterns", type=int, default=0)
+    ap.add_argument("--pattern-config", type=int, default=4, choices=[4, 5],
+                    help="the code whose erasure patterns --patterns draws (4: k10 m4 GF(2^8); 5: k16 m4 GF(2^12))")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--out", default="")
     ap.add_argument("--paper", action="store_true", help="also the paper's (60,40) GF(2^6) code")
@@ -206,7 +209,7 @@ def main():
     for c in [int(x) for x in a.configs.split(",") if x]:
         ok &= run_config(c, dev, a.reps, out)
     if a.patterns:
-        run_patterns(a.patterns, dev, a.reps, out)
+        run_patterns(a.patterns, dev, a.reps, out, a.pattern_config)
     if a.paper:
         run_paper(dev, a.reps, out)
     sys.exit(0 if ok else 1)
