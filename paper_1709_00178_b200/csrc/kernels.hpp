@@ -60,6 +60,7 @@ struct alignas(64) RtArgs {
 struct RtLaunch {
     std::uint32_t w = 0, n = 0, modulus = 0, E = 0, R = 2, V = 2; // E outputs in each of R parts, V words
     bool parity = false, pdl = true;
+    bool pw = false; // R = 4, V = 4 only: a producer warp group issues the TMA copies (ring_rt.cuh)
     unsigned blocks = 1;
     std::uint32_t smem = 0;
     cudaStream_t stream = nullptr;

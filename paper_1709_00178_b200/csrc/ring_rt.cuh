@@ -22,8 +22,11 @@
 // Layout of the work (persistent CTAs, 16 warps per SM):
 //   * one elected thread streams every input fragment tile (all w strips x
 //     2 KiB) into a ring of shared-memory slots with one TMA tensor box
-//     (cp.async.bulk.tensor.3d) per (tile, fragment), NSLOT-1 ahead of the
-//     consumers, tracked by FULL/EMPTY mbarriers;
+//     (cp.async.bulk.tensor.3d) per (tile, fragment), tracked by FULL/EMPTY
+//     mbarriers: in the four-part shape a thread of a producer warp group that
+//     has handed its registers to the consumers (setmaxnreg), filling slots as
+//     fast as they empty; in the smaller shapes the first thread of the
+//     lightest part, NSLOT-1 fragments ahead;
 //   * R parts of 2048/(4V) threads split the outputs (E accumulated outputs
 //     each); a thread owns 4V bytes of every strip of the tile: it reads the w strip
 //     words of a fragment from shared memory into registers and runs the
@@ -117,8 +120,14 @@ __host__ __device__ constexpr u32 xpow_mod(int t, u32 p, int w) {
 // 256 or 512 threads and an SM holds 512 (16 warps, <= 128 registers each)
 // GRP: more than one output group (units = tiles x groups); without it the
 // group is the constant 0 and its parameters are loop invariant
-template <int W, int N, u32 P, int E, int R, int V, bool PAR, bool GRP>
-__global__ void __launch_bounds__(R * (kRtTile / (4 * V)), 512 / (R * (kRtTile / (4 * V))))
+// PW (the four-part shape only): a producer warp group of 128 threads after the R parts;
+// lane 0 of its first warp issues every TMA copy, so the consumer loop carries no producer
+// code and no consumer warp waits on an EMPTY barrier.  20 warps would cap every thread at
+// 96 registers, so the producer group gives its registers back (setmaxnreg.dec 24) and
+// the consumers take them (setmaxnreg.inc 112): the CTA was given 640 x 96 registers
+// and 512 x 112 + 128 x 24 fit in them (120 would not: the increase would wait for ever).
+template <int W, int N, u32 P, int E, int R, int V, bool PAR, bool GRP, bool PW>
+__global__ void __launch_bounds__(R * (kRtTile / (4 * V)) + (PW ? 128 : 0), 512 / (R * (kRtTile / (4 * V))))
     ring_rt_kernel(const __grid_constant__ RtArgs a) {
     constexpr u32 TILE = kTile, CPP = kRtTile / (4u * V);
     constexpr u32 SLOT = W * TILE;  // one fragment tile
@@ -167,8 +176,18 @@ __global__ void __launch_bounds__(R * (kRtTile / (4 * V)), 512 / (R * (kRtTile /
         if (++pj == k) pj = 0, pu += gridDim.x;
     };
     const u32 PROD = a.prod;
-    if (threadIdx.x == PROD)
-        for (u32 u2 = 0; u2 + 1 < ns; ++u2) produce();
+    if constexpr (PW) {
+        if (threadIdx.x >= R * CPP) { // the producer group: slots fill as fast as they empty
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 24;");
+            if (threadIdx.x == R * CPP)
+                while (pu < nunits) produce();
+            return; // (exited threads count as having let dependents launch)
+        }
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
+    } else {
+        if (threadIdx.x == PROD)
+            for (u32 u2 = 0; u2 + 1 < ns; ++u2) produce();
+    }
     const u32 part = R == 1 ? 0u : threadIdx.x / CPP;
     const u32 col = R == 1 ? threadIdx.x : threadIdx.x % CPP;
     const u64 S = a.S;
@@ -193,7 +212,8 @@ __global__ void __launch_bounds__(R * (kRtTile / (4 * V)), 512 / (R * (kRtTile /
         // body (the instruction cache holds one)
 #pragma unroll 1
         for (u32 j = 0; j < k; ++j) {
-            if (threadIdx.x == PROD) produce();
+            if constexpr (!PW)
+                if (threadIdx.x == PROD) produce();
             mbar_wait(FULL(sl), ph);
             u32 x[XR][V];
             const u32 src = a.slot0 + sbase + sl * SLOT + col * (4u * V);
@@ -246,9 +266,9 @@ __global__ void __launch_bounds__(R * (kRtTile / (4 * V)), 512 / (R * (kRtTile /
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-template <int W, int N, u32 P, int E, int R, int V, bool PAR, bool GRP>
-cudaError_t launch_grp(const RtArgs& a, const RtLaunch& l) {
-    auto fn = ring_rt_kernel<W, N, P, E, R, V, PAR, GRP>;
+template <int W, int N, u32 P, int E, int R, int V, bool PAR, bool GRP, bool PW>
+cudaError_t launch_pw(const RtArgs& a, const RtLaunch& l) {
+    auto fn = ring_rt_kernel<W, N, P, E, R, V, PAR, GRP, PW>;
     static bool attr_set[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -259,7 +279,7 @@ cudaError_t launch_grp(const RtArgs& a, const RtLaunch& l) {
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(l.blocks);
-    cfg.blockDim = dim3(R * rt_part_threads(V));
+    cfg.blockDim = dim3(R * rt_part_threads(V) + (PW ? 128 : 0));
     cfg.dynamicSmemBytes = l.smem;
     cfg.stream = l.stream;
     cudaLaunchAttribute attr[1];
@@ -268,6 +288,13 @@ cudaError_t launch_grp(const RtArgs& a, const RtLaunch& l) {
     cfg.attrs = attr;
     cfg.numAttrs = l.pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, fn, a);
+}
+
+template <int W, int N, u32 P, int E, int R, int V, bool PAR, bool GRP>
+cudaError_t launch_grp(const RtArgs& a, const RtLaunch& l) {
+    if constexpr (R == 4 && V == 4)
+        if (l.pw) return launch_pw<W, N, P, E, R, V, PAR, GRP, true>(a, l);
+    return launch_pw<W, N, P, E, R, V, PAR, GRP, false>(a, l);
 }
 
 template <int W, int N, u32 P, int E, int R, int V, bool PAR>

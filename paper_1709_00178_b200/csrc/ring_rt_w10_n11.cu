@@ -8,7 +8,7 @@ cudaError_t launch_ring_rt_w10_n11(const RtArgs& a, const RtLaunch& l) { return 
 // load this geometry's module now (cudaFuncGetAttributes on one instance)
 cudaError_t warm_ring_rt_w10_n11() {
     cudaFuncAttributes fa;
-    return cudaFuncGetAttributes(&fa, rt_detail::ring_rt_kernel<10, 11, 0x7FFu, 1, 1, 2, false, false>);
+    return cudaFuncGetAttributes(&fa, rt_detail::ring_rt_kernel<10, 11, 0x7FFu, 1, 1, 2, false, false, false>);
 }
 
 } // namespace pyrit_b200

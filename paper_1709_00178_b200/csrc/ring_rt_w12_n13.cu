@@ -8,7 +8,7 @@ cudaError_t launch_ring_rt_w12_n13(const RtArgs& a, const RtLaunch& l) { return 
 // load this geometry's module now (cudaFuncGetAttributes on one instance)
 cudaError_t warm_ring_rt_w12_n13() {
     cudaFuncAttributes fa;
-    return cudaFuncGetAttributes(&fa, rt_detail::ring_rt_kernel<12, 13, 0x1FFFu, 1, 1, 2, false, false>);
+    return cudaFuncGetAttributes(&fa, rt_detail::ring_rt_kernel<12, 13, 0x1FFFu, 1, 1, 2, false, false, false>);
 }
 
 } // namespace pyrit_b200

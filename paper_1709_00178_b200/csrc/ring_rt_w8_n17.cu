@@ -8,7 +8,7 @@ cudaError_t launch_ring_rt_w8_n17(const RtArgs& a, const RtLaunch& l) { return r
 // load this geometry's module now (cudaFuncGetAttributes on one instance)
 cudaError_t warm_ring_rt_w8_n17() {
     cudaFuncAttributes fa;
-    return cudaFuncGetAttributes(&fa, rt_detail::ring_rt_kernel<8, 17, 0x139u, 1, 1, 2, false, false>);
+    return cudaFuncGetAttributes(&fa, rt_detail::ring_rt_kernel<8, 17, 0x139u, 1, 1, 2, false, false, false>);
 }
 
 } // namespace pyrit_b200

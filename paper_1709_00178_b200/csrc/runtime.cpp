@@ -1002,6 +1002,11 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
             l.V = 4;
             l.R = r_for(e);
         }
+        // the four-part shape feeds its slots from a producer warp group (ring_rt.cuh; measured
+        // config 4 0.785 -> 0.946 of peak, profiles/r02/ring_rt_pairs/producer_group/);
+        // PYRIT_B200_RT_PW=0: from the first thread of the lightest part, as the smaller shapes do
+        static const bool pw_knob = env_int("PYRIT_B200_RT_PW", 1) != 0;
+        l.pw = pw_knob && l.R == 4 && l.V == 4;
         const std::uint32_t G = (e + per_group - 1) / per_group;
         l.E = (e + l.R * G - 1) / (l.R * G);
         a.ngrp = G;
