@@ -1113,7 +1113,7 @@ void build_ring_rt(RtCall& call, const Program& p, const std::uint8_t* const* in
         call.case_bytes.push_back(code);
         call.op_count.push_back(nops - G * l.R * k);
         info.blocks = l.blocks;
-        info.threads = l.R * rt_part_threads(l.V);
+        info.threads = l.R * rt_part_threads(l.V) + (l.pw ? 128u : 0u); // + the producer warp group
     }
     info.kernel = "pyrit_ring_rt_w" + std::to_string(w) + "_n" + std::to_string(n) + (par ? "_par" : "");
     info.lanes = 2;

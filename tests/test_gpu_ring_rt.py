@@ -330,3 +330,20 @@ def test_planned_launches_rebind_to_new_buffers(cuda, f):
                     a = s * strip + off
                     exp[i, a:a + length] = wants[pi][di][i, a:a + length]
             np.testing.assert_array_equal(got, exp, err_msg=f"step {step}")
+
+
+def test_launch_shapes(cuda):
+    """The shapes the planner picks (runtime.cpp build_ring_rt): one output -> one 256-thread
+    part; two -> two 128-thread parts; three or more -> four parts plus the 128-thread
+    producer warp group that issues the TMA copies (640 threads, setmaxnreg in ring_rt.cuh)."""
+    f = G256
+    rng = np.random.default_rng(5)
+    k, strip = 6, 16 * 256
+    data = rand_symbols(k, f.w * strip, 77)
+    with mode(4):
+        for e, threads in [(1, 256), (2, 256), (3, 640), (4, 640)]:
+            m = rng.integers(1, 1 << f.w, (e, k), dtype=np.uint16)
+            got = run_plan(cuda, P.Plan.create(f, m), data, e, strip)
+            rt_launched()
+            assert P.Plan.last_launch()["threads"] == threads, (e, P.Plan.last_launch())
+            np.testing.assert_array_equal(got, oracle_ring(f, m, data))
